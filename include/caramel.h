@@ -1,0 +1,162 @@
+/*
+ * caramel.h -- C ABI of the B200 data-parallel aggregation hot path.
+ *
+ * The reference (overlapsim, /root/reference/pkg/src/overlapsim) has no FFI:
+ * its aggregation is an analytic call, `collective_time(spec, model, reduce)`
+ * (collective.py:106-157), made once per fusion bucket from the pipeline's
+ * bucket loop (pipeline.py:80-94).  This library is what replaces that call
+ * with a real launch.  Every entry point below names the reference interface
+ * it stands in for.  Conventions:
+ *   - plain C types only (no torch types); device memory is passed as
+ *     uint64_t device addresses or typed pointers, streams as `void*`
+ *     (a cudaStream_t);
+ *   - every function returns 0 on success and a negative CARAMEL_E* code on
+ *     failure, with a message retrievable through caramel_last_error();
+ *     no C++ exception ever crosses the ABI;
+ *   - all GPU work is stream ordered; only init/import/finalize/status block.
+ *
+ * Element type is fp32 throughout (gradients and parameters).
+ */
+#ifndef CARAMEL_H
+#define CARAMEL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CARAMEL_ABI_VERSION 1
+#define CARAMEL_MAX_RANKS 8     /* one 8xB200 NVSwitch box */
+#define CARAMEL_MAX_DEPTH 8     /* MAX_DEPTH, collective.py:32 */
+
+/* Error codes. */
+#define CARAMEL_OK 0
+#define CARAMEL_EINVAL -1       /* bad argument (mirrors ValueError) */
+#define CARAMEL_EWORKERS -2     /* UnsupportedWorkerCount, collective.py:77-81 */
+#define CARAMEL_ECUDA -3        /* CUDA runtime failure */
+#define CARAMEL_ETIMEOUT -4     /* a cross-rank flag wait hit the watchdog */
+#define CARAMEL_ESTATE -5       /* call made in the wrong context state */
+
+/* Aggregation patterns, same values/order as overlapsim Pattern
+ * (collective.py:35-38: ring, hd, shuffle). */
+#define CARAMEL_RING 0
+#define CARAMEL_HD 1
+#define CARAMEL_SHUFFLE 2
+
+/* What the shard owner applies to the rank-ordered sum before all-gather. */
+#define CARAMEL_EPI_SUM 0       /* out = sum_r g_r                              */
+#define CARAMEL_EPI_SCALE 1     /* out = (sum_r g_r) * scale                    */
+#define CARAMEL_EPI_SGD 2       /* out = theta - lr * ((sum_r g_r) * scale)     */
+                                /* the postponed update (transfer.py:156-160)   */
+
+/* Bucket flags. */
+#define CARAMEL_F_PACK 1u        /* gather member grads into the bucket (K1)   */
+#define CARAMEL_F_UNPACK 2u      /* scatter the result back to the members:
+                                    into .grad for SUM/SCALE, .param for SGD   */
+#define CARAMEL_F_PARAM_ARENA 4u /* SGD result is stored straight into every
+                                    rank's symmetric parameter arena            */
+
+/* One member tensor of a fusion bucket.  Members are listed in bucket order
+ * (BatchGroup.param_ids, batching.py:28-33) with contiguous offsets. */
+typedef struct caramel_segment {
+  uint64_t grad;    /* device address of the member's fp32 gradient          */
+  uint64_t param;   /* device address of the member's fp32 parameter, or 0   */
+  uint64_t offset;  /* element offset of the member inside the bucket        */
+  uint64_t numel;   /* element count                                         */
+} caramel_segment;
+
+/* One fusion bucket's collective: BatchGroup (batching.py:27-34) +
+ * CollectiveSpec (collective.py:70-83) + its placement in the arenas. */
+typedef struct caramel_bucket {
+  uint64_t numel;       /* bucket elements (= total_bytes / 4)                  */
+  uint64_t bucket_off;  /* byte offset of the bucket in each rank's arena (16B)  */
+  uint64_t param_off;   /* byte offset in each rank's param arena (PARAM_ARENA)  */
+  uint64_t flag_off;    /* byte offset of the bucket's flag block in the arena   */
+  uint64_t segs;        /* device address of caramel_segment[nlocal][nseg]       */
+  int32_t nseg;
+  int32_t depth;        /* chunks, 1..8: adaptive_depth (collective.py:160-164)  */
+  int32_t pattern;      /* CARAMEL_RING / _HD / _SHUFFLE                         */
+  int32_t epilogue;     /* CARAMEL_EPI_*                                         */
+  uint32_t flags;       /* CARAMEL_F_*                                           */
+  int32_t ctas;         /* CTAs per rank; from caramel_bucket_layout()           */
+  float lr;             /* SGD learning rate                                     */
+  float scale;          /* multiplier on the sum (1/p for a mean)                */
+} caramel_bucket;
+
+typedef struct caramel_ctx caramel_ctx;
+
+/* ---- library ----------------------------------------------------------- */
+int caramel_abi_version(void);
+const char* caramel_last_error(void);
+
+/* Integer chunk/shard rule.  The reference only defines float bytes per chunk
+ * (stage.transfer_bytes / k, collective.py:124, with transfer_bytes = d/p,
+ * collective.py:90).  Chunk c of an n-element bucket is
+ * [floor(c*n/k), floor((c+1)*n/k)); shard s of an m-element chunk is
+ * [floor(s*m/p), floor((s+1)*m/p)).  Writes depth*(workers+1) absolute
+ * element bounds, row c = shard starts of chunk c plus the chunk end. */
+int caramel_chunk_bounds(uint64_t numel, int depth, int workers, uint64_t* out);
+
+/* Launch geometry and arena footprint of one bucket (identical on every
+ * rank, so every rank launches the same grid): CTAs per rank, bytes of the
+ * bucket region (ring/hd keep a second, output half so a fast neighbour never
+ * overwrites a partial sum still to be pulled; shuffle all-gathers in place)
+ * and bytes of its flag block. */
+int caramel_bucket_layout(uint64_t numel, int depth, int pattern, int world,
+                          int32_t* ctas, uint64_t* bucket_bytes,
+                          uint64_t* flag_bytes);
+
+/* ---- context: symmetric arenas + bootstrap ----------------------------- */
+/* Allocates this process's arenas on the current CUDA device.  `nlocal` is
+ * 1 for one-process-per-GPU; nlocal == world hosts every rank in this process
+ * on one GPU (rank emulation, used when fewer GPUs than ranks are present).
+ * Arenas are zero-filled (flag words start at epoch 0). */
+int caramel_init(int rank, int world, int nlocal, uint64_t arena_bytes,
+                 uint64_t param_arena_bytes, caramel_ctx** out);
+/* Bytes of one rank's bootstrap blob (CUDA IPC handles). */
+int caramel_handle_size(void);
+/* Writes this rank's bootstrap blob; exchanged by the caller (torch.distributed
+ * all_gather over NCCL/gloo: bootstrap only, never on the data path). */
+int caramel_export(caramel_ctx* ctx, void* blob);
+/* Maps every peer's arenas from `world` blobs in rank order. */
+int caramel_import(caramel_ctx* ctx, const void* blobs);
+/* Device addresses of local rank `lr`'s arenas (lr < nlocal). */
+int caramel_arena(caramel_ctx* ctx, int lr, uint64_t* bucket_arena,
+                  uint64_t* param_arena);
+/* Watchdog state: 0, or CARAMEL_ETIMEOUT if a flag wait timed out since the
+ * last call (synchronizes the device; clears the word). */
+int caramel_status(caramel_ctx* ctx);
+int caramel_set_timeout_ms(caramel_ctx* ctx, uint64_t ms);
+int caramel_finalize(caramel_ctx* ctx);
+
+/* ---- K1 / K4: bucket pack and unpack ----------------------------------- */
+/* Gather members' .grad into `bucket` in member order (batching.py:76,122).
+ * 128-bit vectorised where the member is 16-byte aligned. */
+int caramel_pack(const caramel_segment* segs, int32_t nseg, uint64_t numel,
+                 float* bucket, void* stream);
+/* Scatter `bucket` back into the members' .grad (to_param == 0) or
+ * .param (to_param != 0). */
+int caramel_unpack(const caramel_segment* segs, int32_t nseg, uint64_t numel,
+                   const float* bucket, int32_t to_param, void* stream);
+
+/* ---- K2/K3 (+K4): the per-bucket collective ------------------------------ */
+/* Replaces collective_time(CollectiveSpec(pattern, world, 4*numel, depth))
+ * (collective.py:106-157) at pipeline.py:94 with a real launch: a chunked
+ * ring / halving-doubling / two-shot all-reduce that loads and stores peer
+ * HBM over NVLink with per-chunk epoch flags, the reduction fused in, summing
+ * each element in the pattern's fixed order.  `epoch` must be identical on
+ * every rank and strictly increase per bucket (1, 2, 3, ...).  Result lands
+ * in every rank's bucket (and members, with CARAMEL_F_UNPACK). */
+int caramel_allreduce(caramel_ctx* ctx, const caramel_bucket* bucket,
+                      uint32_t epoch, void* stream);
+/* Same collective with the postponed SGD update fused into the all-gather
+ * epilogue: the shard owner computes theta - lr*(sum*scale) once and stores
+ * it to every rank (transfer.py:156-160). */
+int caramel_allreduce_update(caramel_ctx* ctx, const caramel_bucket* bucket,
+                             uint32_t epoch, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CARAMEL_H */

@@ -1,0 +1,1038 @@
+// caramel.cu -- sm_100a kernels + C ABI for the data-parallel aggregation
+// hot path (fusion-bucket pack, chunked ring / halving-doubling / two-shot
+// all-reduce over NVLink peer memory, postponed SGD update fused into the
+// all-gather epilogue).  See include/caramel.h for the contract and DESIGN.md
+// for the data layout.
+//
+// Reference semantics followed (all under /root/reference/pkg/src/overlapsim):
+//   bucket membership / member order ..... batching.py:76,122 (BatchGroup.param_ids)
+//   chunking into `depth` pieces ......... collective.py:18-21,121-124
+//   per-stage bytes of each pattern ....... collective.py:86-103 (stage_plan)
+//   depth cap ............................ collective.py:32 (MAX_DEPTH = 8)
+//   worker-count validation .............. collective.py:77-83
+//   postponed update ..................... transfer.py:156-160
+//
+// Layout (per rank; every rank allocates identical sizes so offsets are
+// symmetric): one "bucket arena" = [bucket buffers | flag blocks], plus an
+// optional parameter arena.  Peers' arenas are mapped with CUDA IPC; all
+// cross-rank traffic is plain ld/st on the mapped addresses (NVLink 5 via
+// NVSwitch).  Flags are 32-bit epochs written by the producer into the
+// consumer's flag block with st.release.sys and polled with ld.acquire.sys.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <stdarg.h>
+
+#include "../../include/caramel.h"
+
+#define THREADS 512
+#define MAXR CARAMEL_MAX_RANKS
+
+// ---------------------------------------------------------------------------
+// error plumbing (host)
+// ---------------------------------------------------------------------------
+static thread_local char g_err[512] = "";
+
+static int set_err(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                       \
+  do {                                                                       \
+    cudaError_t _e = (expr);                                                 \
+    if (_e != cudaSuccess)                                                   \
+      return set_err(CARAMEL_ECUDA, "%s failed: %s (%s:%d)", #expr,          \
+                     cudaGetErrorString(_e), __FILE__, __LINE__);            \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t split_at(uint64_t n, uint64_t parts, uint64_t i) {
+  // floor(i * n / parts): the integer chunk/shard rule
+  return (n * i) / parts;
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ float4 ld4(const float* p) { return __ldcg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ void st4(float* p, float4 v) { __stcg(reinterpret_cast<float4*>(p), v); }
+__device__ __forceinline__ float ld1(const float* p) { return __ldcg(p); }
+__device__ __forceinline__ void st1(float* p, float v) { __stcg(p, v); }
+
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
+                     __fadd_rn(a.w, b.w));
+}
+
+// Epilogue applied by the shard owner.  Separate roundings, never an FMA, so
+// the CPU oracle (numpy / C with -ffp-contract=off) is matched bit for bit.
+__device__ __forceinline__ float epi1(int epi, float s, float theta, float scale, float lr) {
+  if (epi == CARAMEL_EPI_SUM) return s;
+  float g = __fmul_rn(s, scale);
+  if (epi == CARAMEL_EPI_SCALE) return g;
+  return __fsub_rn(theta, __fmul_rn(lr, g));
+}
+
+__device__ __forceinline__ float4 epi4(int epi, float4 s, float4 t, float scale, float lr) {
+  return make_float4(epi1(epi, s.x, t.x, scale, lr), epi1(epi, s.y, t.y, scale, lr),
+                     epi1(epi, s.z, t.z, scale, lr), epi1(epi, s.w, t.w, scale, lr));
+}
+
+// Segment cursor: maps a bucket element position to its member tensor.
+// Segments are sorted by offset and tile [0, numel) without gaps.
+struct Cursor {
+  const caramel_segment* s;
+  int n;
+  int i;
+  uint64_t lo, hi, g, p;
+};
+
+__device__ __forceinline__ void cur_init(Cursor& c, const caramel_segment* s, int n) {
+  c.s = s;
+  c.n = n;
+  c.i = -1;
+  c.lo = 1;
+  c.hi = 0;
+  c.g = 0;
+  c.p = 0;
+}
+
+__device__ __forceinline__ void cur_load(Cursor& c, int i) {
+  const unsigned long long* e = reinterpret_cast<const unsigned long long*>(c.s + i);
+  c.i = i;
+  c.g = __ldg(e + 0);
+  c.p = __ldg(e + 1);
+  c.lo = __ldg(e + 2);
+  c.hi = c.lo + __ldg(e + 3);
+}
+
+__device__ __forceinline__ void cur_seek(Cursor& c, uint64_t pos) {
+  if (pos >= c.lo && pos < c.hi) return;
+  int a = 0, b = c.n - 1;
+  if (c.i >= 0 && pos >= c.hi) {
+    if (c.i + 1 < c.n) {
+      cur_load(c, c.i + 1);  // common case: the next member
+      if (pos < c.hi) return;
+    }
+    a = c.i;
+  }
+  while (a < b) {
+    int m = (a + b + 1) >> 1;
+    uint64_t off = __ldg(reinterpret_cast<const unsigned long long*>(c.s + m) + 2);
+    if (off <= pos) a = m; else b = m - 1;
+  }
+  cur_load(c, a);
+}
+
+// which: 0 = member .grad, 1 = member .param
+__device__ __forceinline__ float seg_ld1(Cursor& c, uint64_t pos, int which) {
+  cur_seek(c, pos);
+  const float* b = reinterpret_cast<const float*>(which ? c.p : c.g);
+  return ld1(b + (pos - c.lo));
+}
+
+__device__ __forceinline__ void seg_st1(Cursor& c, uint64_t pos, int which, float v) {
+  cur_seek(c, pos);
+  float* b = reinterpret_cast<float*>(which ? c.p : c.g);
+  st1(b + (pos - c.lo), v);
+}
+
+__device__ __forceinline__ float4 seg_ld4(Cursor& c, uint64_t v, int which) {
+  cur_seek(c, v);
+  const float* ptr = reinterpret_cast<const float*>(which ? c.p : c.g) + (v - c.lo);
+  if (v + 4 <= c.hi && (reinterpret_cast<uintptr_t>(ptr) & 15) == 0) return ld4(ptr);
+  float4 r;
+  r.x = seg_ld1(c, v + 0, which);
+  r.y = seg_ld1(c, v + 1, which);
+  r.z = seg_ld1(c, v + 2, which);
+  r.w = seg_ld1(c, v + 3, which);
+  return r;
+}
+
+__device__ __forceinline__ void seg_st4(Cursor& c, uint64_t v, int which, float4 x) {
+  cur_seek(c, v);
+  float* ptr = reinterpret_cast<float*>(which ? c.p : c.g) + (v - c.lo);
+  if (v + 4 <= c.hi && (reinterpret_cast<uintptr_t>(ptr) & 15) == 0) {
+    st4(ptr, x);
+    return;
+  }
+  seg_st1(c, v + 0, which, x.x);
+  seg_st1(c, v + 1, which, x.y);
+  seg_st1(c, v + 2, which, x.z);
+  seg_st1(c, v + 3, which, x.w);
+}
+
+// Cut [lo, hi) into `parts` tiles whose interior cuts fall on absolute
+// 4-element boundaries (so tile interiors vectorise); tile `j` is returned.
+__device__ __forceinline__ void tile_of(uint64_t lo, uint64_t hi, int parts, int j,
+                                        uint64_t& tlo, uint64_t& thi) {
+  auto cut = [&](int k) -> uint64_t {
+    if (k <= 0) return lo;
+    if (k >= parts) return hi;
+    uint64_t x = lo + split_at(hi - lo, parts, k);
+    x = (x + 3) & ~3ull;
+    return x < hi ? x : hi;
+  };
+  tlo = cut(j);
+  thi = cut(j + 1);
+  if (thi < tlo) thi = tlo;
+}
+
+// Visit [lo, hi): scalar head up to a 4-aligned position, float4 body, scalar tail.
+template <class FV, class FS>
+__device__ __forceinline__ void walk(uint64_t lo, uint64_t hi, FV fv, FS fs) {
+  if (lo >= hi) return;
+  uint64_t a = (lo + 3) & ~3ull;
+  if (a > hi) a = hi;
+  uint64_t b = hi & ~3ull;
+  if (b < a) b = a;
+  for (uint64_t i = lo + threadIdx.x; i < a; i += blockDim.x) fs(i);
+  for (uint64_t v = a + 4ull * threadIdx.x; v < b; v += 4ull * blockDim.x) fv(v);
+  for (uint64_t i = b + threadIdx.x; i < hi; i += blockDim.x) fs(i);
+}
+
+// ---------------------------------------------------------------------------
+// K1 / K4 standalone: pack and unpack
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(THREADS) k_pack(const caramel_segment* segs, int nseg,
+                                                  uint64_t numel, float* bucket) {
+  uint64_t lo, hi;
+  tile_of(0, numel, gridDim.x, blockIdx.x, lo, hi);
+  Cursor c;
+  cur_init(c, segs, nseg);
+  walk(lo, hi, [&](uint64_t v) { st4(bucket + v, seg_ld4(c, v, 0)); },
+       [&](uint64_t i) { st1(bucket + i, seg_ld1(c, i, 0)); });
+}
+
+__global__ void __launch_bounds__(THREADS) k_unpack(const caramel_segment* segs, int nseg,
+                                                    uint64_t numel, const float* bucket,
+                                                    int to_param) {
+  uint64_t lo, hi;
+  tile_of(0, numel, gridDim.x, blockIdx.x, lo, hi);
+  Cursor c;
+  cur_init(c, segs, nseg);
+  walk(lo, hi, [&](uint64_t v) { seg_st4(c, v, to_param, ld4(bucket + v)); },
+       [&](uint64_t i) { seg_st1(c, i, to_param, ld1(bucket + i)); });
+}
+
+// ---------------------------------------------------------------------------
+// the per-bucket collective kernel
+// ---------------------------------------------------------------------------
+struct KParams {
+  uint64_t arena[MAXR];   // bucket arena base of every rank, mapped on this device
+  uint64_t parena[MAXR];  // parameter arena base of every rank (0 if none)
+  caramel_bucket b;
+  int world;
+  int rank_base;          // first rank hosted by this launch (blockIdx.y adds)
+  uint32_t epoch;
+  uint64_t timeout_ns;
+  int* status;
+};
+
+// flag slots
+#define SLOT_READY 0
+#define SLOT_DONE 1  // shuffle
+
+__host__ __device__ __forceinline__ int ilog2i(int p) {
+  int l = 0;
+  while ((1 << l) < p) ++l;
+  return l;
+}
+
+__host__ __device__ __forceinline__ int nslots(int pattern, int world) {
+  if (pattern == CARAMEL_SHUFFLE) return 2;
+  if (pattern == CARAMEL_RING) return 2 * world;           // ready, 2(p-1) steps, exit
+  return 2 * ilog2i(world) + 2;                             // ready, L halving, L doubling, exit
+}
+
+// elements between a ring/hd bucket's input region and its output region
+__host__ __device__ __forceinline__ uint64_t out_region_elems(uint64_t numel) {
+  return (numel + 3) & ~3ull;
+}
+
+struct Ctx {
+  const KParams* P;
+  int me, world, j, G, ns;
+  uint32_t epoch;
+  __device__ __forceinline__ uint32_t* flag(int rank, int c, int slot, int src) const {
+    uint32_t* base = reinterpret_cast<uint32_t*>(P->arena[rank] + P->b.flag_off);
+    return base + ((((uint64_t)c * G + j) * ns + slot) * world + src);
+  }
+  // every thread calls; thread t < ntargets publishes to targets[t]
+  __device__ __forceinline__ void publish(int c, int slot, const int* targets, int ntargets) const {
+    __syncthreads();
+    if ((int)threadIdx.x < ntargets) {
+      __threadfence_system();
+      st_release_sys(flag(targets[threadIdx.x], c, slot, me), epoch);
+    }
+  }
+  __device__ __forceinline__ void publish_all(int c, int slot) const {
+    __syncthreads();
+    if ((int)threadIdx.x < world) {
+      __threadfence_system();
+      st_release_sys(flag(threadIdx.x, c, slot, me), epoch);
+    }
+  }
+  // every thread calls; waits until src's flag (in my block) reaches `want`
+  __device__ __forceinline__ void wait_from(int c, int slot, const int* srcs, int nsrc,
+                                            uint32_t want) const {
+    if ((int)threadIdx.x < nsrc) {
+      const uint32_t* f = flag(me, c, slot, srcs[threadIdx.x]);
+      if (ld_acquire_sys(f) < want) {
+        uint64_t t0 = globaltimer();
+        uint32_t spins = 0;
+        while (ld_acquire_sys(f) < want) {
+          if ((++spins & 1023u) == 0 && globaltimer() - t0 > P->timeout_ns) {
+            atomicExch(P->status, CARAMEL_ETIMEOUT);
+            break;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  __device__ __forceinline__ void wait_all(int c, int slot, uint32_t want) const {
+    if ((int)threadIdx.x < world) {
+      const uint32_t* f = flag(me, c, slot, threadIdx.x);
+      if (ld_acquire_sys(f) < want) {
+        uint64_t t0 = globaltimer();
+        uint32_t spins = 0;
+        while (ld_acquire_sys(f) < want) {
+          if ((++spins & 1023u) == 0 && globaltimer() - t0 > P->timeout_ns) {
+            atomicExch(P->status, CARAMEL_ETIMEOUT);
+            break;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+};
+
+// Reduce [lo, hi) of the bucket across all P ranks in ascending rank order
+// (acc = g0; acc += g1; ...), apply the epilogue once, store the result to
+// every rank's output buffer.  Two float4 per thread per trip so 2*P 128-bit
+// loads are in flight before the first add.
+template <int P>
+__device__ __forceinline__ void rs_ag_range(const float* const* src, float* const* dst,
+                                            const float* theta_flat, Cursor& tc,
+                                            uint64_t lo, uint64_t hi, int epi,
+                                            float scale, float lr, bool seg_theta) {
+  if (lo >= hi) return;
+  uint64_t a = (lo + 3) & ~3ull;
+  if (a > hi) a = hi;
+  uint64_t b = hi & ~3ull;
+  if (b < a) b = a;
+  const bool need_theta = (epi == CARAMEL_EPI_SGD);
+  for (uint64_t i = lo + threadIdx.x; i < a; i += blockDim.x) {
+    float s = ld1(src[0] + i);
+#pragma unroll
+    for (int q = 1; q < P; ++q) s = __fadd_rn(s, ld1(src[q] + i));
+    float t = 0.f;
+    if (need_theta) t = seg_theta ? seg_ld1(tc, i, 1) : ld1(theta_flat + i);
+    float o = epi1(epi, s, t, scale, lr);
+#pragma unroll
+    for (int q = 0; q < P; ++q) st1(dst[q] + i, o);
+  }
+  const uint64_t step = 4ull * blockDim.x;
+  uint64_t v = a + 4ull * threadIdx.x;
+  for (; v + step < b; v += 2 * step) {
+    float4 x0[P], x1[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      x0[q] = ld4(src[q] + v);
+      x1[q] = ld4(src[q] + v + step);
+    }
+    float4 t0 = make_float4(0.f, 0.f, 0.f, 0.f), t1 = t0;
+    if (need_theta) {
+      if (seg_theta) {
+        t0 = seg_ld4(tc, v, 1);
+        t1 = seg_ld4(tc, v + step, 1);
+      } else {
+        t0 = ld4(theta_flat + v);
+        t1 = ld4(theta_flat + v + step);
+      }
+    }
+    float4 s0 = x0[0], s1 = x1[0];
+#pragma unroll
+    for (int q = 1; q < P; ++q) {
+      s0 = add4(s0, x0[q]);
+      s1 = add4(s1, x1[q]);
+    }
+    float4 o0 = epi4(epi, s0, t0, scale, lr), o1 = epi4(epi, s1, t1, scale, lr);
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      st4(dst[q] + v, o0);
+      st4(dst[q] + v + step, o1);
+    }
+  }
+  if (v < b) {
+    float4 s = ld4(src[0] + v);
+#pragma unroll
+    for (int q = 1; q < P; ++q) s = add4(s, ld4(src[q] + v));
+    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (need_theta) t = seg_theta ? seg_ld4(tc, v, 1) : ld4(theta_flat + v);
+    float4 o = epi4(epi, s, t, scale, lr);
+#pragma unroll
+    for (int q = 0; q < P; ++q) st4(dst[q] + v, o);
+  }
+  for (uint64_t i = b + threadIdx.x; i < hi; i += blockDim.x) {
+    float s = ld1(src[0] + i);
+#pragma unroll
+    for (int q = 1; q < P; ++q) s = __fadd_rn(s, ld1(src[q] + i));
+    float t = 0.f;
+    if (need_theta) t = seg_theta ? seg_ld1(tc, i, 1) : ld1(theta_flat + i);
+    float o = epi1(epi, s, t, scale, lr);
+#pragma unroll
+    for (int q = 0; q < P; ++q) st1(dst[q] + i, o);
+  }
+}
+
+// Pairwise step used by ring and halving-doubling: out = a + b (a first),
+// optionally followed by the epilogue (last reduction of the owner's shard).
+__device__ __forceinline__ void pair_range(const float* a_src, const float* b_src, float* out,
+                                           uint64_t lo, uint64_t hi, bool final_epi, int epi,
+                                           float scale, float lr, const float* theta_flat,
+                                           Cursor& tc, bool seg_theta) {
+  const bool need_theta = final_epi && epi == CARAMEL_EPI_SGD;
+  walk(lo, hi,
+       [&](uint64_t v) {
+         float4 x = ld4(a_src + v), y = ld4(b_src + v);
+         float4 s = add4(x, y);
+         if (final_epi) {
+           float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+           if (need_theta) t = seg_theta ? seg_ld4(tc, v, 1) : ld4(theta_flat + v);
+           s = epi4(epi, s, t, scale, lr);
+         }
+         st4(out + v, s);
+       },
+       [&](uint64_t i) {
+         float s = __fadd_rn(ld1(a_src + i), ld1(b_src + i));
+         if (final_epi) {
+           float t = 0.f;
+           if (need_theta) t = seg_theta ? seg_ld1(tc, i, 1) : ld1(theta_flat + i);
+           s = epi1(epi, s, t, scale, lr);
+         }
+         st1(out + i, s);
+       });
+}
+
+__device__ __forceinline__ void copy_range(const float* src, float* dst, uint64_t lo, uint64_t hi) {
+  walk(lo, hi, [&](uint64_t v) { st4(dst + v, ld4(src + v)); },
+       [&](uint64_t i) { st1(dst + i, ld1(src + i)); });
+}
+
+// Single-rank path (world == 1): no exchange; gather, epilogue and scatter
+// fused in one pass over the bucket.
+__device__ void local_path(const KParams& P, int lr_idx) {
+  const caramel_bucket& B = P.b;
+  const int me = P.rank_base + lr_idx;
+  float* bkt = reinterpret_cast<float*>(P.arena[me] + B.bucket_off);
+  const bool arena = (B.flags & CARAMEL_F_PARAM_ARENA) && B.epilogue == CARAMEL_EPI_SGD;
+  float* pflat = arena ? reinterpret_cast<float*>(P.parena[me] + B.param_off) : nullptr;
+  const bool pack = B.flags & CARAMEL_F_PACK;
+  const bool unpack = (B.flags & CARAMEL_F_UNPACK) && !arena;
+  const int out_which = (B.epilogue == CARAMEL_EPI_SGD) ? 1 : 0;
+  const caramel_segment* segs = reinterpret_cast<const caramel_segment*>(B.segs) + (uint64_t)lr_idx * B.nseg;
+  Cursor gc, pc;
+  cur_init(gc, segs, B.nseg);
+  cur_init(pc, segs, B.nseg);
+  uint64_t lo, hi;
+  tile_of(0, B.numel, gridDim.x, blockIdx.x, lo, hi);
+  const int epi = B.epilogue;
+  walk(lo, hi,
+       [&](uint64_t v) {
+         float4 g = pack ? seg_ld4(gc, v, 0) : ld4(bkt + v);
+         float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+         if (epi == CARAMEL_EPI_SGD) t = arena ? ld4(pflat + v) : seg_ld4(pc, v, 1);
+         float4 o = epi4(epi, g, t, B.scale, B.lr);
+         if (arena) st4(pflat + v, o);
+         else if (unpack) seg_st4(pc, v, out_which, o);
+         else st4(bkt + v, o);
+       },
+       [&](uint64_t i) {
+         float g = pack ? seg_ld1(gc, i, 0) : ld1(bkt + i);
+         float t = 0.f;
+         if (epi == CARAMEL_EPI_SGD) t = arena ? ld1(pflat + i) : seg_ld1(pc, i, 1);
+         float o = epi1(epi, g, t, B.scale, B.lr);
+         if (arena) st1(pflat + i, o);
+         else if (unpack) seg_st1(pc, i, out_which, o);
+         else st1(bkt + i, o);
+       });
+}
+
+template <int PAT, int NP>
+__global__ void __launch_bounds__(THREADS) k_collective(const __grid_constant__ KParams P) {
+  const int lr_idx = blockIdx.y;
+  if (P.world == 1) {
+    local_path(P, lr_idx);
+    return;
+  }
+  const caramel_bucket& B = P.b;
+  const int p = P.world;
+  Ctx X;
+  X.P = &P;
+  X.me = P.rank_base + lr_idx;
+  X.world = p;
+  X.j = blockIdx.x;
+  X.G = gridDim.x;
+  X.ns = nslots(PAT, p);
+  X.epoch = P.epoch;
+  const int me = X.me;
+
+  const float* bsrc[MAXR];
+  float* bdst[MAXR];
+  float* odst[MAXR];  // where the final result goes on each rank
+  const bool arena = (B.flags & CARAMEL_F_PARAM_ARENA) && B.epilogue == CARAMEL_EPI_SGD;
+  // shuffle all-gathers in place; ring/hd write results to a second region
+  // of the bucket so a fast neighbour never overwrites a partial sum that a
+  // slower one has yet to pull
+  const uint64_t out_off = (PAT == CARAMEL_SHUFFLE) ? 0 : out_region_elems(B.numel);
+#pragma unroll
+  for (int q = 0; q < MAXR; ++q) {
+    if (q < p) {
+      bdst[q] = reinterpret_cast<float*>(P.arena[q] + B.bucket_off);
+      bsrc[q] = bdst[q];
+      odst[q] = arena ? reinterpret_cast<float*>(P.parena[q] + B.param_off) : bdst[q] + out_off;
+    } else {
+      bdst[q] = nullptr;
+      bsrc[q] = nullptr;
+      odst[q] = nullptr;
+    }
+  }
+  float* mine = bdst[me];
+  const float* theta_flat = arena ? reinterpret_cast<const float*>(P.parena[me] + B.param_off) : nullptr;
+  const bool seg_theta = !arena;
+  const caramel_segment* segs = reinterpret_cast<const caramel_segment*>(B.segs) + (uint64_t)lr_idx * B.nseg;
+  Cursor gc, tc;
+  cur_init(gc, segs, B.nseg);
+  cur_init(tc, segs, B.nseg);
+  const int k = B.depth;
+  const int epi = B.epilogue;
+  const uint64_t n = B.numel;
+
+  auto chunk_lo = [&](int c) { return split_at(n, k, c); };
+  auto shard = [&](int c, int s, uint64_t& lo, uint64_t& hi) {
+    uint64_t c0 = chunk_lo(c), m = chunk_lo(c + 1) - c0;
+    uint64_t a = c0 + split_at(m, p, s), b = c0 + split_at(m, p, s + 1);
+    tile_of(a, b, X.G, X.j, lo, hi);  // this CTA's tile of shard s
+  };
+  // range of shards [s0, s1) of chunk c, tiled for this CTA (shard-wise tiles)
+  auto for_shards = [&](int c, int s0, int s1, auto fn) {
+    for (int s = s0; s < s1; ++s) {
+      uint64_t lo, hi;
+      shard(c, s, lo, hi);
+      fn(lo, hi);
+    }
+  };
+
+  // ring / hd: wait until every rank that read my buffers last epoch is done
+  if (PAT != CARAMEL_SHUFFLE && P.epoch > 1) {
+    int srcs[MAXR];
+    int ns = 0;
+    if (PAT == CARAMEL_RING) {
+      srcs[ns++] = (me + 1) % p;
+    } else {
+      for (int d = 1; d < p; d <<= 1) srcs[ns++] = me ^ d;
+    }
+    X.wait_from(0, X.ns - 1, srcs, ns, P.epoch - 1);
+  }
+
+  // ---- pack (K1, fused) + ready ------------------------------------------
+  const bool pack = B.flags & CARAMEL_F_PACK;
+  for (int c = 0; c < k; ++c) {
+    if (pack) {
+      for_shards(c, 0, p, [&](uint64_t lo, uint64_t hi) {
+        walk(lo, hi, [&](uint64_t v) { st4(mine + v, seg_ld4(gc, v, 0)); },
+             [&](uint64_t i) { st1(mine + i, seg_ld1(gc, i, 0)); });
+      });
+    }
+    if (PAT == CARAMEL_SHUFFLE) {
+      X.publish_all(c, SLOT_READY);
+    } else if (PAT == CARAMEL_RING) {
+      int t = (me + 1) % p;
+      X.publish(c, SLOT_READY, &t, 1);
+    } else {
+      int t = me ^ (p >> 1);
+      X.publish(c, SLOT_READY, &t, 1);
+    }
+  }
+
+  if (PAT == CARAMEL_SHUFFLE) {
+    // ---- two-shot: RS own shard in rank order, epilogue, AG store --------
+    for (int c = 0; c < k; ++c) {
+      X.wait_all(c, SLOT_READY, P.epoch);
+      uint64_t lo, hi;
+      shard(c, me, lo, hi);
+      rs_ag_range<NP>(bsrc, odst, theta_flat, tc, lo, hi, epi, B.scale, B.lr, seg_theta);
+      X.publish_all(c, SLOT_DONE);
+    }
+    for (int c = 0; c < k; ++c) X.wait_all(c, SLOT_DONE, P.epoch);
+  } else if (PAT == CARAMEL_RING) {
+    const int left = (me + p - 1) % p, right = (me + 1) % p;
+    for (int c = 0; c < k; ++c) {
+      // reduce-scatter: at step t rank r folds its own share of shard
+      // (r-1-t) mod p into the left neighbour's running sum (the chain of
+      // shard s starts at rank s+1 and ends at its owner s).
+      for (int t = 1; t <= p - 1; ++t) {
+        X.wait_from(c, t == 1 ? SLOT_READY : t - 1, &left, 1, P.epoch);
+        int s = ((me - 1 - t) % p + p) % p;
+        const bool last = (t == p - 1);
+        uint64_t lo, hi;
+        shard(c, s, lo, hi);
+        pair_range(bsrc[left], mine, last ? odst[me] : mine, lo, hi, last, epi, B.scale, B.lr,
+                   theta_flat, tc, seg_theta);
+        X.publish(c, t, &right, 1);
+      }
+      // all-gather: at step t copy shard (r-t) mod p from the left neighbour
+      for (int t = 1; t <= p - 1; ++t) {
+        X.wait_from(c, (p - 1) + (t - 1), &left, 1, P.epoch);
+        int s = ((me - t) % p + p) % p;
+        uint64_t lo, hi;
+        shard(c, s, lo, hi);
+        copy_range(odst[left], odst[me], lo, hi);
+        X.publish(c, (p - 1) + t, &right, 1);
+      }
+    }
+  } else {  // halving-doubling (p a power of two)
+    // Stages: 0 = pack, 1..L = halving rounds, L+1..2L = doubling rounds.
+    // Stage s reads from partner(s); finishing stage s signals slot s to the
+    // rank that reads from me next, partner(s+1).
+    const int L = ilog2i(p);
+    auto partner_of = [&](int stage) {
+      return stage <= L ? (me ^ (p >> stage)) : (me ^ (1 << (stage - L - 1)));
+    };
+    for (int c = 0; c < k; ++c) {
+      // vector halving, distance halving: round i pairs r with r ^ (p >> (i+1));
+      // r keeps the half of its active block range that contains block r and
+      // sums it as (lower rank's value) + (higher rank's value)
+      for (int i = 0; i < L; ++i) {
+        const int stage = i + 1;
+        const int dist = p >> (i + 1);
+        const int partner = partner_of(stage);
+        X.wait_from(c, stage - 1, &partner, 1, P.epoch);
+        const int base = me & ~(2 * dist - 1);
+        const int s0 = (me & dist) ? base + dist : base;
+        const bool last = (i == L - 1);
+        const float* lo_src = (me < partner) ? mine : bsrc[partner];
+        const float* hi_src = (me < partner) ? bsrc[partner] : mine;
+        for_shards(c, s0, s0 + dist, [&](uint64_t lo, uint64_t hi) {
+          pair_range(lo_src, hi_src, last ? odst[me] : mine, lo, hi, last, epi, B.scale, B.lr,
+                     theta_flat, tc, seg_theta);
+        });
+        const int nxt = partner_of(stage + 1);
+        X.publish(c, stage, &nxt, 1);
+      }
+      // vector doubling: round i pairs r with r ^ (1 << i); copy the partner's
+      // finished blocks into my output
+      for (int i = 0; i < L; ++i) {
+        const int stage = L + 1 + i;
+        const int dist = 1 << i;
+        const int partner = partner_of(stage);
+        X.wait_from(c, stage - 1, &partner, 1, P.epoch);
+        const int s0 = partner & ~(dist - 1);
+        for_shards(c, s0, s0 + dist, [&](uint64_t lo, uint64_t hi) {
+          copy_range(odst[partner], odst[me], lo, hi);
+        });
+        if (i + 1 < L) {
+          const int nxt = partner_of(stage + 1);
+          X.publish(c, stage, &nxt, 1);
+        }
+      }
+    }
+  }
+
+  // ---- unpack (fused K4 scatter) ------------------------------------------
+  if ((B.flags & CARAMEL_F_UNPACK) && !arena) {
+    const int which = (epi == CARAMEL_EPI_SGD) ? 1 : 0;
+    Cursor uc;
+    cur_init(uc, segs, B.nseg);
+    for (int c = 0; c < k; ++c) {
+      for_shards(c, 0, p, [&](uint64_t lo, uint64_t hi) {
+        walk(lo, hi, [&](uint64_t v) { seg_st4(uc, v, which, ld4(odst[me] + v)); },
+             [&](uint64_t i) { seg_st1(uc, i, which, ld1(odst[me] + i)); });
+      });
+    }
+  }
+
+  // ring / hd: tell every rank I read from that I am done with its buffers
+  if (PAT != CARAMEL_SHUFFLE) {
+    int tg[MAXR];
+    int nt = 0;
+    if (PAT == CARAMEL_RING) {
+      tg[nt++] = (me + p - 1) % p;
+    } else {
+      for (int d = 1; d < p; d <<= 1) tg[nt++] = me ^ d;
+    }
+    X.publish(0, X.ns - 1, tg, nt);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+struct caramel_ctx {
+  int rank, world, nlocal, device, sms;
+  uint64_t arena_bytes, param_bytes;
+  void* arena_local[MAXR];
+  void* param_local[MAXR];
+  uint64_t arena[MAXR];
+  uint64_t parena[MAXR];
+  bool imported;
+  bool opened[MAXR];
+  int* status;
+  uint64_t timeout_ns;
+};
+
+struct Blob {
+  uint32_t magic, rank, world, has_param;
+  uint64_t arena_bytes, param_bytes;
+  cudaIpcMemHandle_t arena, param;
+};
+
+extern "C" {
+
+int caramel_abi_version(void) { return CARAMEL_ABI_VERSION; }
+const char* caramel_last_error(void) { return g_err; }
+
+int caramel_chunk_bounds(uint64_t numel, int depth, int workers, uint64_t* out) {
+  if (depth < 1 || depth > CARAMEL_MAX_DEPTH)
+    return set_err(CARAMEL_EINVAL, "depth must be in [1, %d]", CARAMEL_MAX_DEPTH);
+  if (workers < 1 || workers > 64) return set_err(CARAMEL_EINVAL, "bad worker count %d", workers);
+  if (!out) return set_err(CARAMEL_EINVAL, "null output");
+  for (int c = 0; c < depth; ++c) {
+    uint64_t c0 = (numel * (uint64_t)c) / depth, c1 = (numel * (uint64_t)(c + 1)) / depth;
+    uint64_t m = c1 - c0;
+    for (int s = 0; s < workers; ++s) out[(uint64_t)c * (workers + 1) + s] = c0 + (m * s) / workers;
+    out[(uint64_t)c * (workers + 1) + workers] = c1;
+  }
+  return 0;
+}
+
+static int validate_workers(int pattern, int world) {
+  if (world < 1 || world > MAXR)
+    return set_err(CARAMEL_EWORKERS, "world size %d outside [1, %d]", world, MAXR);
+  if (pattern == CARAMEL_HD && (world & (world - 1)))
+    return set_err(CARAMEL_EWORKERS, "halving-doubling requires a power-of-two worker count");
+  if (pattern < 0 || pattern > 2) return set_err(CARAMEL_EINVAL, "unknown pattern %d", pattern);
+  return 0;
+}
+
+static int default_max_ctas() {
+  const char* e = getenv("CARAMEL_MAX_CTAS");
+  if (e && atoi(e) > 0) return atoi(e);
+  return 64;
+}
+
+int caramel_bucket_layout(uint64_t numel, int depth, int pattern, int world, int32_t* ctas,
+                          uint64_t* bucket_bytes, uint64_t* flag_bytes) {
+  int rc = validate_workers(pattern, world);
+  if (rc) return rc;
+  if (depth < 1 || depth > CARAMEL_MAX_DEPTH)
+    return set_err(CARAMEL_EINVAL, "depth must be in [1, %d]", CARAMEL_MAX_DEPTH);
+  uint64_t per = numel / ((uint64_t)depth * world);  // elements per shard per chunk
+  const uint64_t tile = (uint64_t)THREADS * 4 * 2;   // one trip of rs_ag_range
+  uint64_t g;
+  if (world == 1) {
+    g = (numel + 4 * tile - 1) / (4 * tile);
+    if (g > 148 * 4) g = 148 * 4;
+  } else {
+    g = (per + tile - 1) / tile;
+    uint64_t cap = (uint64_t)default_max_ctas();
+    if (g > cap) g = cap;
+  }
+  if (g < 1) g = 1;
+  if (ctas) *ctas = (int32_t)g;
+  if (bucket_bytes) {
+    uint64_t e = out_region_elems(numel);
+    *bucket_bytes = 4 * ((world > 1 && pattern != CARAMEL_SHUFFLE) ? 2 * e : e);
+  }
+  if (flag_bytes) {
+    uint64_t fb = world == 1 ? 0 : (uint64_t)depth * g * nslots(pattern, world) * world * 4;
+    *flag_bytes = (fb + 255) & ~255ull;
+  }
+  return 0;
+}
+
+int caramel_init(int rank, int world, int nlocal, uint64_t arena_bytes, uint64_t param_arena_bytes,
+                 caramel_ctx** out) {
+  if (!out) return set_err(CARAMEL_EINVAL, "null ctx output");
+  *out = nullptr;
+  if (world < 1 || world > MAXR) return set_err(CARAMEL_EWORKERS, "world %d outside [1, %d]", world, MAXR);
+  if (nlocal != 1 && nlocal != world) return set_err(CARAMEL_EINVAL, "nlocal must be 1 or world");
+  if (nlocal == world && rank != 0) return set_err(CARAMEL_EINVAL, "rank emulation requires rank 0");
+  if (rank < 0 || rank >= world) return set_err(CARAMEL_EINVAL, "rank %d outside [0, %d)", rank, world);
+  caramel_ctx* c = (caramel_ctx*)calloc(1, sizeof(caramel_ctx));
+  if (!c) return set_err(CARAMEL_EINVAL, "out of host memory");
+  c->rank = rank;
+  c->world = world;
+  c->nlocal = nlocal;
+  const uint64_t G2 = 2ull << 20;
+  c->arena_bytes = ((arena_bytes ? arena_bytes : 1) + G2 - 1) / G2 * G2;
+  c->param_bytes = param_arena_bytes ? (param_arena_bytes + G2 - 1) / G2 * G2 : 0;
+  c->timeout_ns = 5ull * 1000 * 1000 * 1000;
+  if (const char* e = getenv("CARAMEL_WATCHDOG_MS")) c->timeout_ns = strtoull(e, 0, 10) * 1000000ull;
+  int rc = 0;
+  cudaError_t e;
+  if ((e = cudaGetDevice(&c->device)) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "cudaGetDevice: %s", cudaGetErrorString(e)); goto fail; }
+  if ((e = cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device)) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "attr: %s", cudaGetErrorString(e)); goto fail; }
+  for (int i = 0; i < nlocal; ++i) {
+    if ((e = cudaMalloc(&c->arena_local[i], c->arena_bytes)) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "cudaMalloc arena (%llu B): %s", (unsigned long long)c->arena_bytes, cudaGetErrorString(e)); goto fail; }
+    if ((e = cudaMemset(c->arena_local[i], 0, c->arena_bytes)) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "memset: %s", cudaGetErrorString(e)); goto fail; }
+    if (c->param_bytes) {
+      if ((e = cudaMalloc(&c->param_local[i], c->param_bytes)) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "cudaMalloc param arena: %s", cudaGetErrorString(e)); goto fail; }
+      if ((e = cudaMemset(c->param_local[i], 0, c->param_bytes)) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "memset: %s", cudaGetErrorString(e)); goto fail; }
+    }
+    int r = rank + i;
+    c->arena[r] = (uint64_t)c->arena_local[i];
+    c->parena[r] = (uint64_t)c->param_local[i];
+  }
+  if ((e = cudaMalloc(&c->status, sizeof(int))) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "cudaMalloc status: %s", cudaGetErrorString(e)); goto fail; }
+  if ((e = cudaMemset(c->status, 0, sizeof(int))) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "memset: %s", cudaGetErrorString(e)); goto fail; }
+  if ((e = cudaDeviceSynchronize()) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "sync: %s", cudaGetErrorString(e)); goto fail; }
+  c->imported = (nlocal == world);
+  *out = c;
+  return 0;
+fail:
+  caramel_finalize(c);
+  return rc;
+}
+
+int caramel_handle_size(void) { return (int)sizeof(Blob); }
+
+int caramel_export(caramel_ctx* c, void* blob) {
+  if (!c || !blob) return set_err(CARAMEL_EINVAL, "null argument");
+  if (c->nlocal != 1) return set_err(CARAMEL_ESTATE, "export is for one-rank-per-process contexts");
+  Blob b;
+  memset(&b, 0, sizeof(b));
+  b.magic = 0xCA7A3E1u;
+  b.rank = c->rank;
+  b.world = c->world;
+  b.arena_bytes = c->arena_bytes;
+  b.param_bytes = c->param_bytes;
+  b.has_param = c->param_bytes ? 1 : 0;
+  CUDA_TRY(cudaIpcGetMemHandle(&b.arena, c->arena_local[0]));
+  if (c->param_bytes) CUDA_TRY(cudaIpcGetMemHandle(&b.param, c->param_local[0]));
+  memcpy(blob, &b, sizeof(b));
+  return 0;
+}
+
+int caramel_import(caramel_ctx* c, const void* blobs) {
+  if (!c || !blobs) return set_err(CARAMEL_EINVAL, "null argument");
+  if (c->imported) return set_err(CARAMEL_ESTATE, "peers already mapped");
+  const Blob* bs = (const Blob*)blobs;
+  for (int q = 0; q < c->world; ++q) {
+    const Blob& b = bs[q];
+    if (b.magic != 0xCA7A3E1u || (int)b.rank != q || (int)b.world != c->world)
+      return set_err(CARAMEL_EINVAL, "bootstrap blob %d is malformed or out of rank order", q);
+    if (b.arena_bytes != c->arena_bytes || b.param_bytes != c->param_bytes)
+      return set_err(CARAMEL_EINVAL, "rank %d arena sizes differ (arenas must be symmetric)", q);
+  }
+  for (int q = 0; q < c->world; ++q) {
+    if (q == c->rank) continue;
+    void* p = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&p, bs[q].arena, cudaIpcMemLazyEnablePeerAccess));
+    c->arena[q] = (uint64_t)p;
+    c->opened[q] = true;
+    if (c->param_bytes) {
+      void* pp = nullptr;
+      CUDA_TRY(cudaIpcOpenMemHandle(&pp, bs[q].param, cudaIpcMemLazyEnablePeerAccess));
+      c->parena[q] = (uint64_t)pp;
+    }
+  }
+  c->imported = true;
+  return 0;
+}
+
+int caramel_arena(caramel_ctx* c, int lr, uint64_t* bucket_arena, uint64_t* param_arena) {
+  if (!c || lr < 0 || lr >= c->nlocal) return set_err(CARAMEL_EINVAL, "bad local rank");
+  if (bucket_arena) *bucket_arena = (uint64_t)c->arena_local[lr];
+  if (param_arena) *param_arena = (uint64_t)c->param_local[lr];
+  return 0;
+}
+
+int caramel_status(caramel_ctx* c) {
+  if (!c) return set_err(CARAMEL_EINVAL, "null ctx");
+  CUDA_TRY(cudaDeviceSynchronize());
+  int s = 0;
+  CUDA_TRY(cudaMemcpy(&s, c->status, sizeof(int), cudaMemcpyDeviceToHost));
+  if (s) {
+    CUDA_TRY(cudaMemset(c->status, 0, sizeof(int)));
+    return set_err(s, "a cross-rank flag wait exceeded the %llu ms watchdog",
+                   (unsigned long long)(c->timeout_ns / 1000000ull));
+  }
+  return 0;
+}
+
+int caramel_set_timeout_ms(caramel_ctx* c, uint64_t ms) {
+  if (!c) return set_err(CARAMEL_EINVAL, "null ctx");
+  c->timeout_ns = ms * 1000000ull;
+  return 0;
+}
+
+int caramel_finalize(caramel_ctx* c) {
+  if (!c) return 0;
+  for (int q = 0; q < MAXR; ++q) {
+    if (c->opened[q]) {
+      cudaIpcCloseMemHandle((void*)c->arena[q]);
+      if (c->parena[q]) cudaIpcCloseMemHandle((void*)c->parena[q]);
+    }
+  }
+  for (int i = 0; i < MAXR; ++i) {
+    if (c->arena_local[i]) cudaFree(c->arena_local[i]);
+    if (c->param_local[i]) cudaFree(c->param_local[i]);
+  }
+  if (c->status) cudaFree(c->status);
+  free(c);
+  return 0;
+}
+
+static int grid_for(uint64_t numel) {
+  uint64_t g = (numel + (uint64_t)THREADS * 16 - 1) / ((uint64_t)THREADS * 16);
+  if (g > 148 * 4) g = 148 * 4;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+int caramel_pack(const caramel_segment* segs, int32_t nseg, uint64_t numel, float* bucket, void* stream) {
+  if (!segs || nseg < 1 || !bucket) return set_err(CARAMEL_EINVAL, "pack: null table or bucket");
+  if (((uintptr_t)bucket) & 15) return set_err(CARAMEL_EINVAL, "pack: bucket must be 16-byte aligned");
+  if (numel == 0) return 0;
+  k_pack<<<grid_for(numel), THREADS, 0, (cudaStream_t)stream>>>(segs, nseg, numel, bucket);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int caramel_unpack(const caramel_segment* segs, int32_t nseg, uint64_t numel, const float* bucket,
+                   int32_t to_param, void* stream) {
+  if (!segs || nseg < 1 || !bucket) return set_err(CARAMEL_EINVAL, "unpack: null table or bucket");
+  if (((uintptr_t)bucket) & 15) return set_err(CARAMEL_EINVAL, "unpack: bucket must be 16-byte aligned");
+  if (numel == 0) return 0;
+  k_unpack<<<grid_for(numel), THREADS, 0, (cudaStream_t)stream>>>(segs, nseg, numel, bucket, to_param ? 1 : 0);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+}  // extern "C"
+
+typedef void (*kfn_t)(const KParams);
+
+template <int PAT>
+static kfn_t pick_np(int p) {
+  switch (p) {
+    case 1: return k_collective<PAT, 1>;
+    case 2: return k_collective<PAT, 2>;
+    case 3: return k_collective<PAT, 3>;
+    case 4: return k_collective<PAT, 4>;
+    case 5: return k_collective<PAT, 5>;
+    case 6: return k_collective<PAT, 6>;
+    case 7: return k_collective<PAT, 7>;
+    default: return k_collective<PAT, 8>;
+  }
+}
+
+extern "C" {
+
+static int launch(caramel_ctx* c, const caramel_bucket* b, uint32_t epoch, void* stream) {
+  if (!c || !b) return set_err(CARAMEL_EINVAL, "null argument");
+  if (!c->imported) return set_err(CARAMEL_ESTATE, "peer arenas not mapped (call caramel_import)");
+  int rc = validate_workers(b->pattern, c->world);
+  if (rc) return rc;
+  if (b->depth < 1 || b->depth > CARAMEL_MAX_DEPTH)
+    return set_err(CARAMEL_EINVAL, "depth must be in [1, %d]", CARAMEL_MAX_DEPTH);
+  if (b->epilogue < 0 || b->epilogue > 2) return set_err(CARAMEL_EINVAL, "unknown epilogue %d", b->epilogue);
+  if (epoch == 0) return set_err(CARAMEL_EINVAL, "epoch must start at 1");
+  if (b->ctas < 1) return set_err(CARAMEL_EINVAL, "ctas must be >= 1 (see caramel_bucket_layout)");
+  if (b->bucket_off & 15) return set_err(CARAMEL_EINVAL, "bucket_off must be 16-byte aligned");
+  if (b->numel == 0) return 0;
+  const uint64_t span = 4 * ((c->world > 1 && b->pattern != CARAMEL_SHUFFLE) ? 2 * out_region_elems(b->numel)
+                                                                         : b->numel);
+  if (b->bucket_off + span > c->arena_bytes)
+    return set_err(CARAMEL_EINVAL, "bucket [%llu, +%llu B) exceeds the arena", (unsigned long long)b->bucket_off,
+                   (unsigned long long)(b->numel * 4));
+  const bool arena = (b->flags & CARAMEL_F_PARAM_ARENA) && b->epilogue == CARAMEL_EPI_SGD;
+  if (arena) {
+    if (!c->param_bytes) return set_err(CARAMEL_EINVAL, "PARAM_ARENA requested but no parameter arena");
+    if ((b->param_off & 15) || b->param_off + b->numel * 4 > c->param_bytes)
+      return set_err(CARAMEL_EINVAL, "param_off misaligned or out of the parameter arena");
+  }
+  const bool needs_segs = (b->flags & CARAMEL_F_PACK) || ((b->flags & CARAMEL_F_UNPACK) && !arena) ||
+                          (b->epilogue == CARAMEL_EPI_SGD && !arena);
+  if (needs_segs && (!b->segs || b->nseg < 1)) return set_err(CARAMEL_EINVAL, "segment table required");
+  if (c->world > 1) {
+    uint64_t fb = (uint64_t)b->depth * b->ctas * nslots(b->pattern, c->world) * c->world * 4;
+    if (b->flag_off + fb > c->arena_bytes) return set_err(CARAMEL_EINVAL, "flag block exceeds the arena");
+    if (b->flag_off & 3) return set_err(CARAMEL_EINVAL, "flag_off must be 4-byte aligned");
+  }
+
+  KParams P;
+  memset(&P, 0, sizeof(P));
+  for (int q = 0; q < MAXR; ++q) {
+    P.arena[q] = c->arena[q];
+    P.parena[q] = c->parena[q];
+  }
+  P.b = *b;
+  P.world = c->world;
+  P.rank_base = c->rank;
+  P.epoch = epoch;
+  P.timeout_ns = c->timeout_ns;
+  P.status = c->status;
+
+  kfn_t fn;
+  if (b->pattern == CARAMEL_SHUFFLE) fn = pick_np<CARAMEL_SHUFFLE>(c->world);
+  else if (b->pattern == CARAMEL_RING) fn = pick_np<CARAMEL_RING>(c->world);
+  else fn = pick_np<CARAMEL_HD>(c->world);
+
+  dim3 grid(b->ctas, c->nlocal), block(THREADS);
+  if (c->nlocal > 1) {
+    // rank emulation: all ranks' CTAs spin on each other, so they must be
+    // co-resident -- a cooperative launch guarantees it or fails.
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, THREADS, 0));
+    if ((uint64_t)per_sm * c->sms < (uint64_t)b->ctas * c->nlocal)
+      return set_err(CARAMEL_EINVAL, "emulated launch of %d x %d CTAs exceeds co-residency (%d per SM)", b->ctas,
+                     c->nlocal, per_sm);
+    void* args[] = {(void*)&P};
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fn, grid, block, args, 0, (cudaStream_t)stream));
+  } else {
+    fn<<<grid, block, 0, (cudaStream_t)stream>>>(P);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return 0;
+}
+
+int caramel_allreduce(caramel_ctx* c, const caramel_bucket* b, uint32_t epoch, void* stream) {
+  if (b && b->epilogue == CARAMEL_EPI_SGD)
+    return set_err(CARAMEL_EINVAL, "caramel_allreduce: use caramel_allreduce_update for the SGD epilogue");
+  return launch(c, b, epoch, stream);
+}
+
+int caramel_allreduce_update(caramel_ctx* c, const caramel_bucket* b, uint32_t epoch, void* stream) {
+  if (b && b->epilogue != CARAMEL_EPI_SGD)
+    return set_err(CARAMEL_EINVAL, "caramel_allreduce_update requires CARAMEL_EPI_SGD");
+  return launch(c, b, epoch, stream);
+}
+
+}  // extern "C"
