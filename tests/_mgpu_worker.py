@@ -1,0 +1,98 @@
+"""One rank of the multi-GPU parity check (launched by tests/test_multigpu.py
+under torch.distributed.run).  Every rank packs its own gradients, runs the
+collective through the C ABI with peer arenas mapped over CUDA IPC, and the
+result is compared with the CPU oracle run on all ranks' inputs (gathered to
+every rank over NCCL -- test plumbing only)."""
+
+from __future__ import annotations
+
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "oracle"))
+
+import oracle as O  # noqa: E402
+from paper_2004_14020_b200 import _native as N  # noqa: E402
+from paper_2004_14020_b200 import comm  # noqa: E402
+
+
+def main() -> int:
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    shapes = [(3, 5), (129,), (64, 7), (1,), (100_003,), (256, 1024), (7,)]
+    numel = sum(int(np.prod(s)) for s in shapes)
+    cases = [(N.SHUFFLE, 1), (N.SHUFFLE, 3), (N.SHUFFLE, 8), (N.RING, 2), (N.RING, 8)]
+    if world & (world - 1) == 0:
+        cases += [(N.HD, 1), (N.HD, 4)]
+    # one arena holds every case's bucket + flag block at distinct offsets
+    layout, off = [], 0
+    for pat, depth in cases:
+        ctas, bbytes, fbytes = N.bucket_layout(numel, depth, pat, world)
+        boff = off
+        foff = (boff + bbytes + 255) // 256 * 256
+        off = (foff + fbytes + 255) // 256 * 256
+        layout.append((pat, depth, ctas, boff, foff))
+    ctx = comm.Context(rank, world, arena_bytes=off, param_bytes=4 * numel)
+    ctx.bootstrap()
+    stream = torch.cuda.current_stream().cuda_stream
+    rng = np.random.default_rng(100 + rank)
+    theta_rng = np.random.default_rng(7)
+    theta = [theta_rng.standard_normal(s).astype(np.float32) for s in shapes]
+    failures = 0
+    for pat, depth, ctas, boff, foff in layout:
+        for epi, arena in ((N.EPI_SUM, False), (N.EPI_SGD, False), (N.EPI_SGD, True)):
+            for epoch in (1, 2):
+                key_epoch = epoch + (0 if epi == N.EPI_SUM else 2 if not arena else 4)
+                grads = [rng.standard_normal(s).astype(np.float32) for s in shapes]
+                g_dev = [torch.from_numpy(g).to(dev) for g in grads]
+                th_dev = [torch.from_numpy(t).to(dev) for t in theta]
+                if arena:
+                    ctx.arena_view(0, 0, numel, param=True).copy_(torch.from_numpy(O.np_pack(theta)).to(dev))
+                table = comm.segment_table([comm.segments_for(g_dev, None if arena else th_dev)], dev)
+                flags = N.F_PACK | N.F_UNPACK | (N.F_PARAM_ARENA if arena else 0)
+                b = comm.make_bucket(numel, boff, foff, depth=depth, pattern=pat, epilogue=epi, flags=flags,
+                                     ctas=ctas, segs=table, nseg=len(shapes), lr=0.05, scale=1.0 / world)
+                torch.cuda.synchronize()
+                dist.barrier()
+                ctx.allreduce(b, key_epoch, stream)
+                ctx.status()
+                # oracle on everyone's inputs
+                flat = torch.from_numpy(O.np_pack(grads)).to(dev)
+                allg = [torch.empty_like(flat) for _ in range(world)]
+                dist.all_gather(allg, flat)
+                bufs = [a.cpu().numpy() for a in allg]
+                want = O.np_allreduce(pat, bufs, depth, epi, 1.0 / world, 0.05, O.np_pack(theta))
+                if epi == N.EPI_SUM:
+                    got = torch.cat([t.flatten() for t in g_dev]).cpu().numpy()
+                elif arena:
+                    got = ctx.arena_view(0, 0, numel, param=True).cpu().numpy()
+                else:
+                    got = torch.cat([t.flatten() for t in th_dev]).cpu().numpy()
+                ok = np.array_equal(got.view(np.uint32), want.view(np.uint32))
+                if not ok:
+                    failures += 1
+                    bad = np.nonzero(got.view(np.uint32) != want.view(np.uint32))[0]
+                    print(f"rank {rank}: MISMATCH pattern={pat} depth={depth} epi={epi} arena={arena} "
+                          f"epoch={epoch}: {bad.size} elems, first {bad[:5]}", flush=True)
+    t = torch.tensor([failures], device=dev)
+    dist.all_reduce(t)
+    if rank == 0:
+        print(f"multigpu parity: world={world} cases={len(layout) * 6} failures={int(t.item())}", flush=True)
+    ctx.close()
+    dist.destroy_process_group()
+    return 0 if int(t.item()) == 0 else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

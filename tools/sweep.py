@@ -1,0 +1,77 @@
+"""Bucket-size sweep (config 5): caramel two-shot / ring / hd bus GB/s vs
+NCCL all_reduce, one process per GPU.  Launch with torch.distributed.run."""
+import json, os, sys
+from pathlib import Path
+import torch, torch.distributed as dist
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+from paper_2004_14020_b200 import _native as N, comm
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local); dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    max_bytes = int(os.environ.get("SWEEP_MAX", 1 << 30))
+    sizes = [4096 * 4 ** i for i in range(12) if 4096 * 4 ** i <= max_bytes]
+    pats = [int(x) for x in os.environ.get("SWEEP_PATTERNS", "2").split(",")]
+    depths = [int(x) for x in os.environ.get("SWEEP_DEPTHS", "1").split(",")]
+    iters = int(os.environ.get("SWEEP_ITERS", 20))
+    maxel = max_bytes // 4
+    ctx = comm.Context(rank, world, arena_bytes=2 * max_bytes + (64 << 20))
+    ctx.bootstrap()
+    base, _ = ctx.arena_ptrs(0)
+    buf = comm._view_fp32(base, maxel)
+    buf.normal_()
+    stream = torch.cuda.current_stream()
+    rows = []
+    epoch = {}
+    for size in sizes:
+        n = size // 4
+        for pat in pats:
+            if pat == N.HD and world & (world - 1):
+                continue
+            for depth in depths:
+                ctas, bbytes, fbytes = N.bucket_layout(n, depth, pat, world)
+                if os.environ.get("SWEEP_CTAS"):
+                    ctas = min(ctas, int(os.environ["SWEEP_CTAS"]))
+                foff = 2 * max_bytes + (1 << 20)
+                b = comm.make_bucket(n, 0, foff, depth=depth, pattern=pat, epilogue=N.EPI_SUM, flags=0, ctas=ctas)
+                key = (pat, depth, ctas)
+                # flags region shared across sizes: keep epochs monotone per key
+                # by giving each key its own flag region
+                idx = list(epoch).index(key) if key in epoch else len(epoch)
+                epoch.setdefault(key, 0)
+                b.flag_off = foff + idx * (8 << 20) // 8
+                ts = []
+                for it in range(iters + 5):
+                    epoch[key] += 1
+                    dist.barrier(); torch.cuda.synchronize()
+                    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    s.record(stream); ctx.allreduce(b, epoch[key], stream.cuda_stream); e.record(stream)
+                    e.synchronize()
+                    if it >= 5: ts.append(s.elapsed_time(e))
+                ctx.status()
+                t = torch.tensor(sorted(ts)[len(ts) // 2], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                us = t.item() * 1e3
+                bus = 2 * (world - 1) / world * size / (us * 1e-6) / 1e9
+                rows.append(dict(impl="caramel", pattern=pat, depth=depth, ctas=ctas, bytes=size, us=round(us, 2), busbw=round(bus, 1)))
+        # NCCL
+        x = buf[:n]
+        ts = []
+        for it in range(iters + 5):
+            dist.barrier(); torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream); dist.all_reduce(x); e.record(stream); e.synchronize()
+            if it >= 5: ts.append(s.elapsed_time(e))
+        t = torch.tensor(sorted(ts)[len(ts) // 2], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        us = t.item() * 1e3
+        rows.append(dict(impl="nccl", bytes=size, us=round(us, 2), busbw=round(2 * (world - 1) / world * size / (us * 1e-6) / 1e9, 1)))
+    if rank == 0:
+        for r in rows: print(json.dumps(r), flush=True)
+    ctx.close(); dist.destroy_process_group()
+
+if __name__ == "__main__":
+    main()
