@@ -1,0 +1,525 @@
+"""Benchmark of the data-parallel aggregation hot path (BASELINE.json metric).
+
+One "step" = one aggregation pass over a model's full fp32 gradient set:
+every fusion bucket of the Caramel plan (launch order = TransferSchedule)
+runs its sm_100a kernel -- pack the member gradients, reduce-scatter over
+NVLink peer memory in fixed rank order, postponed SGD update fused into the
+all-gather epilogue (stores straight into every replica's parameters).  At
+N = 1 there is no exchange: the kernel is the fused pack -> update pass.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--model resnet50]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1)
+    python bench.py --impl reference ...   (CPU reference path, rank 0 only)
+
+Prints ONE JSON line on rank 0.  `value` = whole-job aggregated gradient
+bytes per second: N x (gradient bytes of the model) / step time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "exposed comm ms/iter and allreduce bus GB/s at 1/2/4/8 B200 vs NVLink roofline"
+NVLINK_MODEL = (10.0, 1.0 / 460e3)      # latency us, us/B (SURVEY §8a "NVLink-ish")
+REDUCE_MODEL = (400.0, 10.0)            # CLI defaults (cli.py:102-105); only shapes the modelled times
+NVLINK_PEAK_GBS = 770.0                 # B200_PROFILING.md measured peer copy per direction (fallback)
+NVLINK_NOMINAL_GBS = 900.0
+LR = 0.1
+MODEL_INDEX = {"vgg16": 0, "resnet50": 1, "inception_v3": 2, "alexnet": 3}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="caramel", choices=["caramel", "reference"])
+    ap.add_argument("--model", default="resnet50", choices=sorted(MODEL_INDEX))
+    ap.add_argument("--pattern", default="shuffle", choices=["shuffle", "ring", "hd"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-nccl", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+            time.sleep(0.15)
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# shared setup
+# ---------------------------------------------------------------------------
+def build_plan(model: str, world: int, pattern: str):
+    from paper_2004_14020_b200 import gradsets
+    from paper_2004_14020_b200.collective import Pattern, ReduceModel
+    from paper_2004_14020_b200.costmodel import NetworkModel
+    from paper_2004_14020_b200.executor import lower
+    from paper_2004_14020_b200.pipeline import run_pipeline
+    from paper_2004_14020_b200.sim import SimConfig
+
+    tensors = gradsets.gradient_set(model)
+    dag = gradsets.layered_chain_dag(model)
+    cfg = SimConfig(workers=max(2, world), network=NetworkModel(*NVLINK_MODEL), reduce=ReduceModel(*REDUCE_MODEL),
+                    pattern=Pattern(pattern))
+    t0 = time.perf_counter()
+    art = run_pipeline(dag, cfg)
+    plan_s = time.perf_counter() - t0
+    numels = {gradsets.param_id(i, len(tensors)): t.numel for i, t in enumerate(tensors)}
+    plan = lower(art, numels, world, Pattern(pattern))
+    return tensors, art, plan, plan_s
+
+
+def env_rank():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU implementation of the path (oracle port), rank 0
+# ---------------------------------------------------------------------------
+def cpu_pass(buckets, grads_by_worker, params_host, pattern_code, nthreads, scratch):
+    """One CPU aggregation pass over every bucket (launch order, members,
+    depth): pack -> collective on `len(grads_by_worker)` simulated workers ->
+    SGD update -> unpack."""
+    import oracle as O
+
+    p = len(grads_by_worker)
+    for members, depth in buckets:
+        O.c_bucket_step(pattern_code, depth, [[grads_by_worker[r][pid] for pid in members] for r in range(p)],
+                        [params_host[pid] for pid in members], O.EPI_SGD, 1.0 / p, LR, nthreads=nthreads,
+                        scratch=scratch)
+
+
+def reference_plan(model: str, world: int, pattern: str):
+    """Buckets (members, depth) in launch order as planned by the REFERENCE
+    planner (tests/golden/plans.json.gz, written by make_golden.py from
+    overlapsim itself), or None if that configuration was not recorded."""
+    import gzip
+
+    path = ROOT / "tests" / "golden" / "plans.json.gz"
+    if not path.exists():
+        return None
+    with gzip.open(path, "rt", encoding="utf-8") as fh:
+        doc = json.load(fh)
+    for case in doc["models"]:
+        c = case["config"]
+        if (case["model"] == model and c["workers"] == max(2, world) and c["pattern"] == pattern
+                and c["scenario"] is None and tuple(c["network"]) == NVLINK_MODEL):
+            a = case["artifacts"]
+            members = {g[0]: g[1] for g in a["groups"]}
+            return [(members[t[0]], a["depths"][t[0]]) for t in a["transfers"]]
+    return None
+
+
+def make_host_inputs(tensors, world, model, seed_base=1000):
+    import numpy as np
+
+    from paper_2004_14020_b200 import gradsets
+
+    ids = [gradsets.param_id(i, len(tensors)) for i in range(len(tensors))]
+    prng = np.random.default_rng(7)
+    params = {pid: (prng.standard_normal(t.numel, dtype=np.float32) * np.float32(0.01)) for pid, t in zip(ids, tensors)}
+    grads = []
+    for r in range(world):
+        g = np.random.default_rng(seed_base * (MODEL_INDEX[model] + 1) + r)
+        grads.append({pid: g.standard_normal(t.numel, dtype=np.float32) for pid, t in zip(ids, tensors)})
+    return ids, params, grads
+
+
+def run_reference(args) -> int:
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O
+
+    from paper_2004_14020_b200 import gradsets
+
+    tensors = gradsets.gradient_set(args.model)
+    buckets = reference_plan(args.model, world, args.pattern)
+    plan_src = "reference planner (tests/golden/plans.json.gz)"
+    if buckets is None:
+        _, _, plan, _ = build_plan(args.model, world, args.pattern)
+        buckets = [(list(b.param_ids), b.depth) for b in plan.buckets]
+        plan_src = "this package's planner (bit-exact with the reference, tests/test_plan_parity.py)"
+    ids, params, grads = make_host_inputs(tensors, world, args.model)
+    numel = {pid: t.numel for pid, t in zip(ids, tensors)}
+    total = sum(numel.values())
+    nthreads = os.cpu_count() or 1
+    scratch = np.empty((world + 1) * max(sum(numel[p] for p in m) for m, _ in buckets), np.float32)
+    code = {"ring": O.RING, "hd": O.HD, "shuffle": O.SHUFFLE}[args.pattern]
+    steps, warm = max(1, args.steps), max(0, args.warmup)
+    # bounded: keep the whole run to a few minutes
+    t0 = time.perf_counter()
+    cpu_pass(buckets, grads, params, code, nthreads, scratch)
+    one = time.perf_counter() - t0
+    budget = 120.0
+    steps = max(1, min(steps, int(budget / max(one, 1e-6))))
+    warm = min(warm, max(0, int(30.0 / max(one, 1e-6))))
+    for _ in range(warm):
+        cpu_pass(buckets, grads, params, code, nthreads, scratch)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        cpu_pass(buckets, grads, params, code, nthreads, scratch)
+    dt = (time.perf_counter() - t0) / steps
+    nbytes = 4 * total
+    value = world * nbytes / dt / 1e9
+    sample = (f"full {args.model} gradient set ({len(tensors)} tensors, {nbytes / 1e6:.1f} MB per worker, "
+              f"{len(buckets)} buckets, plan from the {plan_src}) x {world} simulated worker(s), "
+              f"{steps} timed pass(es)")
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "impl": "reference", "n_gpus": world,
+        "steps": steps, "warmup": warm, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.model} gradient set, Caramel plan, {args.pattern}, p={world}",
+                   "model": args.model, "pattern": args.pattern, "buckets": len(buckets)},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": nthreads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# caramel arm
+# ---------------------------------------------------------------------------
+def time_kernels_gated(agg, torch, reps=3):
+    """Per-bucket kernel durations, measured with CUDA events around each
+    launch; a _sleep kernel first holds the stream so every launch is queued
+    before the first runs (no host gaps inside the brackets)."""
+    stream = torch.cuda.current_stream()
+    per = [0.0] * len(agg._live)
+    for _ in range(reps):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in agg._live]
+        torch.cuda._sleep(int(50e6))  # ~25 ms at ~2 GHz
+        import ctypes
+
+        from paper_2004_14020_b200 import _native as N
+        N.check(N.lib().caramel_epoch_advance(agg.ctx._ctx, ctypes.c_void_p(stream.cuda_stream)))
+        for lv, (a, b) in zip(agg._live, evs):
+            a.record(stream)
+            agg._launch(lv, stream.cuda_stream)
+            b.record(stream)
+        torch.cuda.synchronize()
+        for i, (a, b) in enumerate(evs):
+            per[i] += a.elapsed_time(b) / reps
+    return per  # ms
+
+
+def nccl_baseline(torch, dist, params, grads_dev, world, steps, warmup, bucket_bytes=25 << 20):
+    """Plain bucketed NCCL all-reduce (DDP-style 25 MiB buckets in reverse
+    parameter order) + SGD update with torch ops: the compared baseline."""
+    ids = list(params)[::-1]
+    buckets, cur, cur_b = [], [], 0
+    for pid in ids:
+        nb = params[pid].numel() * 4
+        if cur and cur_b + nb > bucket_bytes:
+            buckets.append(cur)
+            cur, cur_b = [], 0
+        cur.append(pid)
+        cur_b += nb
+    if cur:
+        buckets.append(cur)
+    flats = [torch.empty(sum(params[p].numel() for p in b), device=grads_dev[ids[0]].device) for b in buckets]
+
+    def one_step():
+        for b, flat in zip(buckets, flats):
+            torch.cat([grads_dev[p].reshape(-1) for p in b], out=flat)
+            dist.all_reduce(flat)
+            off = 0
+            for p in b:
+                n = params[p].numel()
+                params[p].reshape(-1).sub_(flat[off:off + n], alpha=LR / world)
+                off += n
+
+    for _ in range(warmup):
+        one_step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        one_step()
+    e.record()
+    e.synchronize()
+    t = torch.tensor([s.elapsed_time(e) / steps], device=flats[0].device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.item(), len(buckets)
+
+
+def run_caramel(args) -> int:
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_2004_14020_b200 import _native as N
+    from paper_2004_14020_b200.executor import Aggregator
+
+    rank, world, local = env_rank()
+    if world != args.gpus:
+        print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    N.lib()  # fail loudly if the sm_100a library is missing
+
+    tensors, art, plan, plan_s = build_plan(args.model, world, args.pattern)
+    ids, params_h, grads_h = make_host_inputs(tensors, 1, args.model, seed_base=1000)
+    # this rank's gradients: seed 1000*(config)+rank (mode B)
+    g = np.random.default_rng(1000 * (MODEL_INDEX[args.model] + 1) + rank)
+    grads_h = {pid: g.standard_normal(t.numel, dtype=np.float32) for pid, t in zip(ids, tensors)}
+    shapes = {pid: t.shape for pid, t in zip(ids, tensors)}
+    params = {pid: torch.from_numpy(params_h[pid]).to(dev).view(shapes[pid]) for pid in ids}
+    agg = Aggregator(plan, params, rank=rank, lr=LR, epilogue="sgd", param_arena=True)
+    for pid in ids:
+        params[pid].grad.copy_(torch.from_numpy(grads_h[pid]).view(shapes[pid]))
+    nbytes = 4 * plan.total_numel
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    # warm-up, then capture one step in a CUDA graph
+    for _ in range(max(3, args.warmup)):
+        agg.step()
+    torch.cuda.synchronize()
+    agg.status()
+    graph = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    barrier()
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(graph, stream=side):
+            agg.step()
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    for _ in range(max(3, args.warmup)):
+        graph.replay()
+    torch.cuda.synchronize()
+    agg.status()
+
+    # ---- timed region: K graph replays, inputs (grads+params) > L2 --------
+    barrier()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        s.record()
+        for _ in range(args.steps):
+            graph.replay()
+        e.record()
+        e.synchronize()
+    barrier()
+    ms = s.elapsed_time(e) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    agg.status()
+    value = world * nbytes / (ms * 1e-3) / 1e9
+
+    # ---- dominant kernel: per-launch durations (events around each launch)
+    barrier()
+    per_ms = time_kernels_gated(agg, torch)
+    barrier()
+    agg.status()
+    kern_ms = sum(per_ms)
+    if world == 1:
+        alg_bytes = 12 * plan.total_numel  # read grad, read theta, write theta
+        roof = {"bound": "hbm", "unit": "GB/s", "peak": None, "peak_source": None}
+        peaks = ROOT / "MEASURED_PEAKS.json"
+        if peaks.exists():
+            roof["peak"] = json.loads(peaks.read_text()).get("hbm_gbs")
+            roof["peak_source"] = "MEASURED_PEAKS.json hbm_gbs (measured)"
+        if roof["peak"] is None:
+            roof["peak"], roof["peak_source"] = 6650.0, "B200_PROFILING.md fallback"
+    else:
+        alg_bytes = plan.bus_bytes()  # 2(p-1)/p * S per bucket, NVLink per direction
+        roof = {"bound": "nvlink", "unit": "GB/s", "peak": NVLINK_PEAK_GBS,
+                "peak_source": "B200_PROFILING.md measured peer copy per direction (fallback; 900 nominal)"}
+    if dist is not None:
+        t = torch.tensor([kern_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        kern_ms = t.item()
+    achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
+    roof.update({"achieved": round(achieved, 1), "frac": round(achieved / roof["peak"], 4),
+                 "traffic": None, "kernel": "k_collective (caramel.cu)", "launches_per_step": len(per_ms),
+                 "kernel_ms_per_step": round(kern_ms, 4),
+                 "alg_bytes_per_step": alg_bytes,
+                 "alg_bytes_rule": "12 B/elem (grad r, theta r/w)" if world == 1 else "2(p-1)/p x bucket bytes"})
+    tr = ROOT / "profiles" / "traffic.json"
+    if tr.exists():
+        key = f"{args.model}_p{world}_{args.pattern}"
+        roof["traffic"] = json.loads(tr.read_text()).get(key)
+
+    # ---- e2e: through the public API with host buffers --------------------
+    pinned_g = {pid: torch.from_numpy(grads_h[pid]).pin_memory() for pid in ids}
+    pinned_p = {pid: torch.empty(params[pid].numel()).pin_memory() for pid in ids}
+    barrier()
+    torch.cuda.synchronize()
+    e2e_steps = max(3, min(args.steps, 20))
+    s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s2.record()
+    for _ in range(e2e_steps):
+        for pid in ids:
+            params[pid].grad.view(-1).copy_(pinned_g[pid], non_blocking=True)
+        agg.step()
+        for pid in ids:
+            pinned_p[pid].copy_(params[pid].view(-1), non_blocking=True)
+    e2.record()
+    e2.synchronize()
+    e2e_ms = s2.elapsed_time(e2) / e2e_steps
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = t.item()
+    agg.status()
+    e2e = {"value": round(world * nbytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+           "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": round(e2e_ms, 4)}
+
+    # ---- NCCL bucketed baseline (N > 1) -------------------------------------
+    nccl = None
+    if dist is not None and not args.no_nccl:
+        bparams = {pid: params[pid].detach().clone() for pid in ids}
+        bgrads = {pid: params[pid].grad.detach().clone() for pid in ids}
+        nms, nb = nccl_baseline(torch, dist, bparams, bgrads, world, args.steps, max(3, args.warmup))
+        nccl = {"ms_per_step": round(nms, 4), "value": round(world * nbytes / (nms * 1e-3) / 1e9, 3),
+                "bus_gbs": round(plan.bus_bytes() / (nms * 1e-3) / 1e9, 1) if world > 1 else None,
+                "buckets": nb, "bucket_mib": 25}
+
+    # ---- CPU baseline (rank 0, N = 1 only) ----------------------------------
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import oracle as O
+
+        nthreads = os.cpu_count() or 1
+        scratch = np.empty(2 * max(b.numel for b in plan.buckets), np.float32)
+        hp = {pid: params_h[pid].copy() for pid in ids}
+        cb = [(list(b.param_ids), b.depth) for b in plan.buckets]
+        cpu_pass(cb, [grads_h], hp, O.SHUFFLE, nthreads, scratch)
+        reps, t0 = 0, time.perf_counter()
+        while reps < 3 or time.perf_counter() - t0 < 2.0:
+            cpu_pass(cb, [grads_h], hp, O.SHUFFLE, nthreads, scratch)
+            reps += 1
+            if time.perf_counter() - t0 > 20.0:
+                break
+        cdt = (time.perf_counter() - t0) / reps
+        cpu = {"value": round(nbytes / cdt / 1e9, 3), "unit": "GB/s", "cores": nthreads, "kind": "port",
+               "sample": f"full {args.model} set ({nbytes / 1e6:.1f} MB), {len(plan.buckets)} buckets, "
+                         f"{reps} passes of oracle_bucket_step (C, pthreads)"}
+
+    kernels_per_step = agg.kernels_per_step()
+    bus = plan.bus_bytes() / (ms * 1e-3) / 1e9 if world > 1 else None
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.model} fp32 gradient set ({len(tensors)} tensors, {nbytes / 1e6:.1f} MB/GPU): "
+                               f"Caramel plan -> pack + {args.pattern} all-reduce + fused SGD update",
+                   "model": args.model, "pattern": args.pattern, "buckets": len(plan.buckets),
+                   "depths": sorted({b.depth for b in plan.buckets}), "parallelism": f"dp{world}",
+                   "l2": "working set (grads + params) > 126 MB L2; no flush", "graph": "CUDA graph per step",
+                   "network_model": {"latency_us": NVLINK_MODEL[0], "per_byte_us": NVLINK_MODEL[1]},
+                   "threshold_bytes": art.threshold_bytes},
+        "bus_gbs": round(bus, 1) if bus is not None else None,
+        "exposed_comm_ms_per_iter": None,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "nccl_baseline": nccl,
+        "clocks": clocks.summary(),
+        "gpu_launches": kernels_per_step * args.steps,
+        "planner_s": round(plan_s, 3),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    agg.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main() -> int:
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_caramel(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -147,9 +147,15 @@ int caramel_unpack(const caramel_segment* segs, int32_t nseg, uint64_t numel,
  * HBM over NVLink with per-chunk epoch flags, the reduction fused in, summing
  * each element in the pattern's fixed order.  `epoch` must be identical on
  * every rank and strictly increase per bucket (1, 2, 3, ...).  Result lands
- * in every rank's bucket (and members, with CARAMEL_F_UNPACK). */
+ * in every rank's bucket (and members, with CARAMEL_F_UNPACK).
+ * epoch == 0 selects the context's device epoch counter instead (see
+ * caramel_epoch_advance), which makes launches replayable in a CUDA graph. */
 int caramel_allreduce(caramel_ctx* ctx, const caramel_bucket* bucket,
                       uint32_t epoch, void* stream);
+/* Stream-ordered increment of the context's device epoch counter: call once
+ * per iteration before that iteration's epoch==0 launches (every rank the
+ * same number of times). */
+int caramel_epoch_advance(caramel_ctx* ctx, void* stream);
 /* Same collective with the postponed SGD update fused into the all-gather
  * epilogue: the shard owner computes theta - lr*(sum*scale) once and stores
  * it to every rank (transfer.py:156-160). */

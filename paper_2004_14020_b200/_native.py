@@ -89,6 +89,7 @@ SIGNATURES = {
                                     ctypes.c_void_p]),
     "caramel_unpack": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64, ctypes.c_void_p,
                                       ctypes.c_int32, ctypes.c_void_p]),
+    "caramel_epoch_advance": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     "caramel_allreduce": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Bucket), ctypes.c_uint32,
                                          ctypes.c_void_p]),
     "caramel_allreduce_update": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Bucket), ctypes.c_uint32,

@@ -246,7 +246,8 @@ struct KParams {
   caramel_bucket b;
   int world;
   int rank_base;          // first rank hosted by this launch (blockIdx.y adds)
-  uint32_t epoch;
+  uint32_t epoch;          // 0: read *epoch_dev (graph-replayable launches)
+  const uint32_t* epoch_dev;
   uint64_t timeout_ns;
   int* status;
 };
@@ -483,6 +484,8 @@ __device__ void local_path(const KParams& P, int lr_idx) {
        });
 }
 
+__global__ void k_epoch_advance(uint32_t* e) { *e += 1; }
+
 template <int PAT, int NP>
 __global__ void __launch_bounds__(THREADS) k_collective(const __grid_constant__ KParams P) {
   const int lr_idx = blockIdx.y;
@@ -499,7 +502,10 @@ __global__ void __launch_bounds__(THREADS) k_collective(const __grid_constant__ 
   X.j = blockIdx.x;
   X.G = gridDim.x;
   X.ns = nslots(PAT, p);
-  X.epoch = P.epoch;
+  // the device counter is advanced by k_epoch_advance earlier on the same
+  // stream, so every CTA of this launch reads the same value
+  const uint32_t epoch = P.epoch ? P.epoch : *reinterpret_cast<const volatile uint32_t*>(P.epoch_dev);
+  X.epoch = epoch;
   const int me = X.me;
 
   const float* bsrc[MAXR];
@@ -549,7 +555,7 @@ __global__ void __launch_bounds__(THREADS) k_collective(const __grid_constant__ 
   };
 
   // ring / hd: wait until every rank that read my buffers last epoch is done
-  if (PAT != CARAMEL_SHUFFLE && P.epoch > 1) {
+  if (PAT != CARAMEL_SHUFFLE && epoch > 1) {
     int srcs[MAXR];
     int ns = 0;
     if (PAT == CARAMEL_RING) {
@@ -557,7 +563,7 @@ __global__ void __launch_bounds__(THREADS) k_collective(const __grid_constant__ 
     } else {
       for (int d = 1; d < p; d <<= 1) srcs[ns++] = me ^ d;
     }
-    X.wait_from(0, X.ns - 1, srcs, ns, P.epoch - 1);
+    X.wait_from(0, X.ns - 1, srcs, ns, epoch - 1);
   }
 
   // ---- pack (K1, fused) + ready ------------------------------------------
@@ -583,13 +589,13 @@ __global__ void __launch_bounds__(THREADS) k_collective(const __grid_constant__ 
   if (PAT == CARAMEL_SHUFFLE) {
     // ---- two-shot: RS own shard in rank order, epilogue, AG store --------
     for (int c = 0; c < k; ++c) {
-      X.wait_all(c, SLOT_READY, P.epoch);
+      X.wait_all(c, SLOT_READY, epoch);
       uint64_t lo, hi;
       shard(c, me, lo, hi);
       rs_ag_range<NP>(bsrc, odst, theta_flat, tc, lo, hi, epi, B.scale, B.lr, seg_theta);
       X.publish_all(c, SLOT_DONE);
     }
-    for (int c = 0; c < k; ++c) X.wait_all(c, SLOT_DONE, P.epoch);
+    for (int c = 0; c < k; ++c) X.wait_all(c, SLOT_DONE, epoch);
   } else if (PAT == CARAMEL_RING) {
     const int left = (me + p - 1) % p, right = (me + 1) % p;
     for (int c = 0; c < k; ++c) {
@@ -597,7 +603,7 @@ __global__ void __launch_bounds__(THREADS) k_collective(const __grid_constant__ 
       // (r-1-t) mod p into the left neighbour's running sum (the chain of
       // shard s starts at rank s+1 and ends at its owner s).
       for (int t = 1; t <= p - 1; ++t) {
-        X.wait_from(c, t == 1 ? SLOT_READY : t - 1, &left, 1, P.epoch);
+        X.wait_from(c, t == 1 ? SLOT_READY : t - 1, &left, 1, epoch);
         int s = ((me - 1 - t) % p + p) % p;
         const bool last = (t == p - 1);
         uint64_t lo, hi;
@@ -608,7 +614,7 @@ __global__ void __launch_bounds__(THREADS) k_collective(const __grid_constant__ 
       }
       // all-gather: at step t copy shard (r-t) mod p from the left neighbour
       for (int t = 1; t <= p - 1; ++t) {
-        X.wait_from(c, (p - 1) + (t - 1), &left, 1, P.epoch);
+        X.wait_from(c, (p - 1) + (t - 1), &left, 1, epoch);
         int s = ((me - t) % p + p) % p;
         uint64_t lo, hi;
         shard(c, s, lo, hi);
@@ -632,7 +638,7 @@ __global__ void __launch_bounds__(THREADS) k_collective(const __grid_constant__ 
         const int stage = i + 1;
         const int dist = p >> (i + 1);
         const int partner = partner_of(stage);
-        X.wait_from(c, stage - 1, &partner, 1, P.epoch);
+        X.wait_from(c, stage - 1, &partner, 1, epoch);
         const int base = me & ~(2 * dist - 1);
         const int s0 = (me & dist) ? base + dist : base;
         const bool last = (i == L - 1);
@@ -651,7 +657,7 @@ __global__ void __launch_bounds__(THREADS) k_collective(const __grid_constant__ 
         const int stage = L + 1 + i;
         const int dist = 1 << i;
         const int partner = partner_of(stage);
-        X.wait_from(c, stage - 1, &partner, 1, P.epoch);
+        X.wait_from(c, stage - 1, &partner, 1, epoch);
         const int s0 = partner & ~(dist - 1);
         for_shards(c, s0, s0 + dist, [&](uint64_t lo, uint64_t hi) {
           copy_range(odst[partner], odst[me], lo, hi);
@@ -703,6 +709,7 @@ struct caramel_ctx {
   bool imported;
   bool opened[MAXR];
   int* status;
+  uint32_t* epoch_dev;
   uint64_t timeout_ns;
 };
 
@@ -809,8 +816,9 @@ int caramel_init(int rank, int world, int nlocal, uint64_t arena_bytes, uint64_t
     c->arena[r] = (uint64_t)c->arena_local[i];
     c->parena[r] = (uint64_t)c->param_local[i];
   }
-  if ((e = cudaMalloc(&c->status, sizeof(int))) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "cudaMalloc status: %s", cudaGetErrorString(e)); goto fail; }
-  if ((e = cudaMemset(c->status, 0, sizeof(int))) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "memset: %s", cudaGetErrorString(e)); goto fail; }
+  if ((e = cudaMalloc(&c->status, 2 * sizeof(int))) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "cudaMalloc status: %s", cudaGetErrorString(e)); goto fail; }
+  if ((e = cudaMemset(c->status, 0, 2 * sizeof(int))) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "memset: %s", cudaGetErrorString(e)); goto fail; }
+  c->epoch_dev = reinterpret_cast<uint32_t*>(c->status + 1);
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "sync: %s", cudaGetErrorString(e)); goto fail; }
   c->imported = (nlocal == world);
   *out = c;
@@ -963,7 +971,6 @@ static int launch(caramel_ctx* c, const caramel_bucket* b, uint32_t epoch, void*
   if (b->depth < 1 || b->depth > CARAMEL_MAX_DEPTH)
     return set_err(CARAMEL_EINVAL, "depth must be in [1, %d]", CARAMEL_MAX_DEPTH);
   if (b->epilogue < 0 || b->epilogue > 2) return set_err(CARAMEL_EINVAL, "unknown epilogue %d", b->epilogue);
-  if (epoch == 0) return set_err(CARAMEL_EINVAL, "epoch must start at 1");
   if (b->ctas < 1) return set_err(CARAMEL_EINVAL, "ctas must be >= 1 (see caramel_bucket_layout)");
   if (b->bucket_off & 15) return set_err(CARAMEL_EINVAL, "bucket_off must be 16-byte aligned");
   if (b->numel == 0) return 0;
@@ -997,6 +1004,7 @@ static int launch(caramel_ctx* c, const caramel_bucket* b, uint32_t epoch, void*
   P.world = c->world;
   P.rank_base = c->rank;
   P.epoch = epoch;
+  P.epoch_dev = c->epoch_dev;
   P.timeout_ns = c->timeout_ns;
   P.status = c->status;
 
@@ -1020,6 +1028,13 @@ static int launch(caramel_ctx* c, const caramel_bucket* b, uint32_t epoch, void*
     fn<<<grid, block, 0, (cudaStream_t)stream>>>(P);
     CUDA_TRY(cudaGetLastError());
   }
+  return 0;
+}
+
+int caramel_epoch_advance(caramel_ctx* c, void* stream) {
+  if (!c) return set_err(CARAMEL_EINVAL, "null ctx");
+  k_epoch_advance<<<1, 1, 0, (cudaStream_t)stream>>>(c->epoch_dev);
+  CUDA_TRY(cudaGetLastError());
   return 0;
 }
 

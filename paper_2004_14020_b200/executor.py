@@ -1,0 +1,296 @@
+"""From a plan to real launches: lowering, arenas, schedule enforcement.
+
+`lower()` turns the planner's PipelineArtifacts (pipeline.py) into a
+rank-invariant ExecPlan:
+
+* launch order = TransferSchedule.transfers order (transfer.py:193) -- the
+  order every rank enqueues bucket collectives on its comm stream, so cross-
+  rank flag waits can never cross (schedule enforcement);
+* per bucket: members in BatchGroup.param_ids order (batching.py:76,122),
+  depth from the plan (pipeline.py:83-86, adaptive_depth), CTA count and flag
+  block size from caramel_bucket_layout, byte offsets into the symmetric
+  bucket arena and parameter arena (identical on every rank);
+* trigger = the bucket's last member gradient (BatchGroup.ready_time_us is
+  the max member start, batching.py:84-91); placement BP vs FP (postponed
+  update, transfer.py:156-160);
+* a digest all-gathered at init so mismatched plans fail loudly instead of
+  deadlocking.
+
+`Aggregator` owns the CUDA context (comm.Context), moves the parameters into
+the symmetric parameter arena (bucket order, so each bucket's parameters are
+contiguous and the owner's fused SGD epilogue stores them straight into every
+replica), keeps persistent gradient tensors, and launches buckets either all
+at once (`step`, graph-capturable) or as their gradients become ready
+(`attach_hooks`, register_post_accumulate_grad_hook) on a dedicated comm
+stream in the enforced order.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _native as N
+from . import comm
+from .collective import Pattern
+from .pipeline import PipelineArtifacts
+from .transfer import PlacementKind
+
+PATTERN_CODE = {Pattern.RING: N.RING, Pattern.HALVING_DOUBLING: N.HD, Pattern.SHUFFLE: N.SHUFFLE}
+ALIGN = 256
+
+
+def _align(x: int, a: int = ALIGN) -> int:
+    return (x + a - 1) // a * a
+
+
+@dataclass(frozen=True)
+class ExecBucket:
+    index: int                    # launch position
+    group_id: str
+    param_ids: tuple[str, ...]    # member order inside the bucket
+    numels: tuple[int, ...]
+    numel: int
+    depth: int
+    ctas: int
+    bucket_off: int
+    flag_off: int
+    param_off: int
+    placement: str                # PlacementKind value
+    ready_time_us: float
+
+
+@dataclass(frozen=True)
+class ExecPlan:
+    world: int
+    pattern: int
+    buckets: tuple[ExecBucket, ...]
+    arena_bytes: int
+    param_bytes: int
+    total_numel: int
+
+    def digest(self) -> str:
+        doc = {"world": self.world, "pattern": self.pattern, "arena": self.arena_bytes,
+               "param": self.param_bytes,
+               "buckets": [[b.group_id, list(b.param_ids), list(b.numels), b.depth, b.ctas, b.bucket_off,
+                            b.flag_off, b.param_off] for b in self.buckets]}
+        return hashlib.sha256(json.dumps(doc, sort_keys=True).encode()).hexdigest()
+
+    def bus_bytes(self) -> int:
+        """Per-GPU NVLink bytes of one aggregation pass: sum of 2(p-1)/p * S
+        (StagePlan.total_transfer_bytes, collective.py:15-16)."""
+        p = self.world
+        return sum(2 * (p - 1) * 4 * b.numel // p for b in self.buckets) if p > 1 else 0
+
+
+def lower(art: PipelineArtifacts, numels: dict[str, int], world: int, pattern: Pattern = Pattern.SHUFFLE,
+          max_ctas: int | None = None) -> ExecPlan:
+    """Rank-invariant launch plan of a pipeline run (see module docstring)."""
+    code = PATTERN_CODE[pattern]
+    groups = {g.group_id: g for g in art.batch_plan.groups}
+    launch = [t for t in art.transfer_schedule.transfers]
+    if {t.group_id for t in launch} != set(groups):
+        raise ValueError("transfer schedule and batch plan disagree")
+    placement = {t.group_id: t.placement.value for t in launch}
+    buckets = []
+    off = 0
+    poff = 0
+    for idx, t in enumerate(launch):
+        g = groups[t.group_id]
+        ns = tuple(int(numels[p]) for p in g.param_ids)
+        n = sum(ns)
+        if 4 * n != g.total_bytes:
+            raise ValueError(f"{g.group_id}: fp32 member sizes {4 * n} B != planned {g.total_bytes} B")
+        depth = int(art.depths[g.group_id])
+        ctas, bbytes, _ = N.bucket_layout(n, depth, code, world)
+        if max_ctas:
+            ctas = max(1, min(ctas, max_ctas))
+        fbytes = N.flag_bytes_for(depth, ctas, code, world)
+        boff = off
+        foff = _align(boff + bbytes)
+        off = _align(foff + fbytes)
+        buckets.append(ExecBucket(index=idx, group_id=g.group_id, param_ids=tuple(g.param_ids), numels=ns,
+                                  numel=n, depth=depth, ctas=ctas, bucket_off=boff, flag_off=foff,
+                                  param_off=poff, placement=placement[g.group_id],
+                                  ready_time_us=g.ready_time_us))
+        poff = _align(poff + 4 * n)
+    return ExecPlan(world=world, pattern=code, buckets=tuple(buckets), arena_bytes=max(off, ALIGN),
+                    param_bytes=max(poff, ALIGN), total_numel=sum(b.numel for b in buckets))
+
+
+@dataclass
+class _Live:
+    """Per-bucket runtime state."""
+
+    spec: ExecBucket
+    desc: N.Bucket
+    table: torch.Tensor
+    members: list[str]
+    remaining: int = 0
+    done: torch.cuda.Event | None = None
+    gate_modules: list = field(default_factory=list)
+
+
+class Aggregator:
+    """Runs an ExecPlan's bucket collectives on this rank.
+
+    params   : param id -> fp32 CUDA tensor (the model's parameters); with
+               `param_arena=True` their storage is moved into the symmetric
+               parameter arena (values kept) so the fused SGD epilogue writes
+               every replica directly.
+    epilogue : "sgd" (fused postponed update), "mean" or "sum" (gradient
+               all-reduce, result written back into .grad).
+    """
+
+    def __init__(self, plan: ExecPlan, params: dict[str, torch.Tensor], *, rank: int = 0, lr: float = 0.01,
+                 epilogue: str = "sgd", param_arena: bool = True, group=None, bootstrap: bool = True):
+        self.plan = plan
+        self.rank, self.world = rank, plan.world
+        self.lr = float(lr)
+        self.epi = {"sum": N.EPI_SUM, "mean": N.EPI_SCALE, "sgd": N.EPI_SGD}[epilogue]
+        self.param_arena = bool(param_arena) and self.epi == N.EPI_SGD
+        self.params = params
+        dev = next(iter(params.values())).device
+        if dev.type != "cuda":
+            raise ValueError("parameters must live on a CUDA device")
+        self.device = dev
+        self.ctx = comm.Context(rank, self.world, plan.arena_bytes,
+                                plan.param_bytes if self.param_arena else 0)
+        if self.world > 1 and bootstrap:
+            import torch.distributed as dist
+
+            digests: list = [None] * self.world
+            dist.all_gather_object(digests, plan.digest(), group=group)
+            if len(set(digests)) != 1:
+                raise RuntimeError("ranks disagree on the execution plan (digest mismatch)")
+            self.ctx.bootstrap(group)
+        if self.param_arena:
+            self._adopt_params()
+        for p in params.values():
+            if p.grad is None:
+                p.grad = torch.zeros_like(p)
+        self.comm_stream = torch.cuda.Stream(device=dev)
+        self._live = [self._make_live(b) for b in plan.buckets]
+        self._by_param = {}
+        for lv in self._live:
+            for pid in lv.members:
+                self._by_param[pid] = lv
+        self._next = 0
+        self._hooks = []
+        self.epoch = 0
+        self.launches = 0
+
+    # -- setup -----------------------------------------------------------------
+    def _adopt_params(self) -> None:
+        """Move every parameter into the symmetric arena in bucket order."""
+        for b in self.plan.buckets:
+            off = b.param_off
+            for pid, n in zip(b.param_ids, b.numels):
+                p = self.params[pid]
+                view = self.ctx.arena_view(0, off, n, param=True).view(p.shape)
+                view.copy_(p.detach())
+                p.data = view
+                off += 4 * n
+
+    def _make_live(self, b: ExecBucket) -> _Live:
+        segs = comm.segments_for([self.params[p].grad for p in b.param_ids],
+                                 None if self.param_arena else [self.params[p] for p in b.param_ids])
+        table = comm.segment_table([segs], self.device)
+        flags = N.F_PACK | (N.F_PARAM_ARENA if self.param_arena else N.F_UNPACK)
+        scale = 1.0 / self.world
+        desc = comm.make_bucket(b.numel, b.bucket_off, b.flag_off, depth=b.depth, pattern=self.plan.pattern,
+                                epilogue=self.epi, flags=flags, ctas=b.ctas, segs=table, nseg=len(segs),
+                                param_off=b.param_off, lr=self.lr, scale=scale)
+        return _Live(spec=b, desc=desc, table=table, members=list(b.param_ids))
+
+    def refresh_tables(self) -> None:
+        """Rebuild segment tables (after gradients were reallocated)."""
+        self._live = [self._make_live(lv.spec) for lv in self._live]
+        self._by_param = {pid: lv for lv in self._live for pid in lv.members}
+
+    def check_tables(self) -> bool:
+        """True if every gradient still lives where the segment tables point."""
+        for lv in self._live:
+            rows = lv.table.view(-1, 4).cpu()
+            for i, pid in enumerate(lv.members):
+                g = self.params[pid].grad
+                if g is None or int(rows[i, 0]) != g.data_ptr():
+                    return False
+        return True
+
+    # -- launches --------------------------------------------------------------
+    def _launch(self, lv: _Live, stream: int) -> None:
+        self.ctx.allreduce(lv.desc, 0, stream)
+        self.launches += 1
+
+    def step(self, stream: torch.cuda.Stream | None = None) -> None:
+        """Aggregate every bucket now, in launch order, on `stream` (default:
+        the current stream).  Graph-capturable: epochs come from the device
+        counter advanced first on the same stream."""
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        N.check(N.lib().caramel_epoch_advance(self.ctx._ctx, __import__("ctypes").c_void_p(s)))
+        for lv in self._live:
+            self._launch(lv, s)
+
+    def kernels_per_step(self) -> int:
+        return 1 + len(self._live)
+
+    # -- overlapped mode: launch when the last gradient of a bucket is ready ----
+    def attach_hooks(self) -> None:
+        """Launch each bucket on the comm stream as soon as its last member's
+        gradient is accumulated, never out of the planned launch order."""
+        for pid, p in self.params.items():
+            self._hooks.append(p.register_post_accumulate_grad_hook(self._make_hook(pid)))
+        self.begin_iteration()
+
+    def _make_hook(self, pid):
+        def hook(_p):
+            lv = self._by_param[pid]
+            lv.remaining -= 1
+            if lv.remaining == 0:
+                self._drain()
+        return hook
+
+    def begin_iteration(self) -> None:
+        for lv in self._live:
+            lv.remaining = len(lv.members)
+            lv.done = None
+        self._next = 0
+        cur = torch.cuda.current_stream(self.device)
+        self.comm_stream.wait_stream(cur)
+        N.check(N.lib().caramel_epoch_advance(self.ctx._ctx,
+                                              __import__("ctypes").c_void_p(self.comm_stream.cuda_stream)))
+
+    def _drain(self) -> None:
+        """Launch every ready bucket from the head of the launch order."""
+        cur = torch.cuda.current_stream(self.device)
+        while self._next < len(self._live) and self._live[self._next].remaining == 0:
+            lv = self._live[self._next]
+            self.comm_stream.wait_stream(cur)  # its gradients are produced on `cur`
+            self._launch(lv, self.comm_stream.cuda_stream)
+            ev = torch.cuda.Event()
+            ev.record(self.comm_stream)
+            lv.done = ev
+            self._next += 1
+
+    def finish_iteration(self) -> None:
+        """Make the current stream wait for every launched bucket."""
+        if self._next != len(self._live):
+            missing = [lv.spec.group_id for lv in self._live[self._next:]]
+            raise RuntimeError(f"buckets never became ready: {missing[:5]}")
+        torch.cuda.current_stream(self.device).wait_stream(self.comm_stream)
+
+    def detach_hooks(self) -> None:
+        for h in self._hooks:
+            h.remove()
+        self._hooks = []
+
+    def status(self) -> None:
+        self.ctx.status()
+
+    def close(self) -> None:
+        self.detach_hooks()
+        self.ctx.close()
