@@ -162,6 +162,19 @@ int caramel_epoch_advance(caramel_ctx* ctx, void* stream);
 int caramel_allreduce_update(caramel_ctx* ctx, const caramel_bucket* bucket,
                              uint32_t epoch, void* stream);
 
+/* A list of buckets in launch order as ONE launch (the back-to-back pass:
+ * every bucket's gradients already produced).  `host` is the descriptor list
+ * (validated, sizes the grid); `dev_buckets` is a device copy of the same
+ * caramel_bucket[count] and `dev_prefix` a device uint64_t[count+1] of
+ * element prefix sums (prefix[0] = 0).  All buckets share one pattern.  The
+ * two-shot runs phase-major (every pack, then every reduce/all-gather, then
+ * every completion wait); with world == 1 the concatenated element space is
+ * tiled over the whole GPU.  Per bucket the result equals caramel_allreduce /
+ * caramel_allreduce_update on that bucket. */
+int caramel_allreduce_many(caramel_ctx* ctx, const caramel_bucket* host, int32_t count,
+                           uint64_t dev_buckets, uint64_t dev_prefix, uint32_t epoch,
+                           void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -94,6 +94,8 @@ SIGNATURES = {
                                          ctypes.c_void_p]),
     "caramel_allreduce_update": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Bucket), ctypes.c_uint32,
                                                 ctypes.c_void_p]),
+    "caramel_allreduce_many": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Bucket), ctypes.c_int32,
+                                              ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p]),
 }
 
 

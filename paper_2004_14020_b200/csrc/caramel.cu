@@ -238,18 +238,29 @@ __global__ void __launch_bounds__(THREADS) k_unpack(const caramel_segment* segs,
 }
 
 // ---------------------------------------------------------------------------
-// the per-bucket collective kernel
+// the bucket collective: shared by single-bucket and multi-bucket launches
 // ---------------------------------------------------------------------------
-struct KParams {
+struct Env {
   uint64_t arena[MAXR];   // bucket arena base of every rank, mapped on this device
   uint64_t parena[MAXR];  // parameter arena base of every rank (0 if none)
-  caramel_bucket b;
   int world;
   int rank_base;          // first rank hosted by this launch (blockIdx.y adds)
-  uint32_t epoch;          // 0: read *epoch_dev (graph-replayable launches)
+  uint32_t epoch;         // 0: read *epoch_dev (graph-replayable launches)
   const uint32_t* epoch_dev;
   uint64_t timeout_ns;
   int* status;
+};
+
+struct KParams {          // one bucket
+  Env env;
+  caramel_bucket b;
+};
+
+struct MParams {          // a list of buckets, processed in launch order
+  Env env;
+  const caramel_bucket* bs;
+  const uint64_t* prefix; // prefix[i] = elements of buckets [0, i)
+  int nb;
 };
 
 // flag slots
@@ -273,12 +284,19 @@ __host__ __device__ __forceinline__ uint64_t out_region_elems(uint64_t numel) {
   return (numel + 3) & ~3ull;
 }
 
+__device__ __forceinline__ uint32_t launch_epoch(const Env& E) {
+  // the device counter is advanced by k_epoch_advance earlier on the same
+  // stream, so every CTA of a launch reads the same value
+  return E.epoch ? E.epoch : *reinterpret_cast<const volatile uint32_t*>(E.epoch_dev);
+}
+
 struct Ctx {
-  const KParams* P;
+  const Env* E;
+  uint64_t flag_off;
   int me, world, j, G, ns;
   uint32_t epoch;
   __device__ __forceinline__ uint32_t* flag(int rank, int c, int slot, int src) const {
-    uint32_t* base = reinterpret_cast<uint32_t*>(P->arena[rank] + P->b.flag_off);
+    uint32_t* base = reinterpret_cast<uint32_t*>(E->arena[rank] + flag_off);
     return base + ((((uint64_t)c * G + j) * ns + slot) * world + src);
   }
   // every thread calls; thread t < ntargets publishes to targets[t]
@@ -296,38 +314,24 @@ struct Ctx {
       st_release_sys(flag(threadIdx.x, c, slot, me), epoch);
     }
   }
-  // every thread calls; waits until src's flag (in my block) reaches `want`
-  __device__ __forceinline__ void wait_from(int c, int slot, const int* srcs, int nsrc,
-                                            uint32_t want) const {
-    if ((int)threadIdx.x < nsrc) {
-      const uint32_t* f = flag(me, c, slot, srcs[threadIdx.x]);
-      if (ld_acquire_sys(f) < want) {
-        uint64_t t0 = globaltimer();
-        uint32_t spins = 0;
-        while (ld_acquire_sys(f) < want) {
-          if ((++spins & 1023u) == 0 && globaltimer() - t0 > P->timeout_ns) {
-            atomicExch(P->status, CARAMEL_ETIMEOUT);
-            break;
-          }
-        }
+  __device__ __forceinline__ void spin(const uint32_t* f, uint32_t want) const {
+    if (ld_acquire_sys(f) >= want) return;
+    uint64_t t0 = globaltimer();
+    uint32_t spins = 0;
+    while (ld_acquire_sys(f) < want) {
+      if ((++spins & 1023u) == 0 && globaltimer() - t0 > E->timeout_ns) {
+        atomicExch(E->status, CARAMEL_ETIMEOUT);
+        break;
       }
     }
+  }
+  // every thread calls; waits until each src's flag (in my block) reaches `want`
+  __device__ __forceinline__ void wait_from(int c, int slot, const int* srcs, int nsrc, uint32_t want) const {
+    if ((int)threadIdx.x < nsrc) spin(flag(me, c, slot, srcs[threadIdx.x]), want);
     __syncthreads();
   }
   __device__ __forceinline__ void wait_all(int c, int slot, uint32_t want) const {
-    if ((int)threadIdx.x < world) {
-      const uint32_t* f = flag(me, c, slot, threadIdx.x);
-      if (ld_acquire_sys(f) < want) {
-        uint64_t t0 = globaltimer();
-        uint32_t spins = 0;
-        while (ld_acquire_sys(f) < want) {
-          if ((++spins & 1023u) == 0 && globaltimer() - t0 > P->timeout_ns) {
-            atomicExch(P->status, CARAMEL_ETIMEOUT);
-            break;
-          }
-        }
-      }
-    }
+    if ((int)threadIdx.x < world) spin(flag(me, c, slot, threadIdx.x), want);
     __syncthreads();
   }
 };
@@ -337,43 +341,50 @@ struct Ctx {
 // every rank's output buffer.  Two float4 per thread per trip so 2*P 128-bit
 // loads are in flight before the first add.
 template <int P>
-__device__ __forceinline__ void rs_ag_range(const float* const* src, float* const* dst,
-                                            const float* theta_flat, Cursor& tc,
-                                            uint64_t lo, uint64_t hi, int epi,
-                                            float scale, float lr, bool seg_theta) {
+__device__ __forceinline__ void rs_ag_range(const Env& E, const caramel_bucket& B, bool arena, Cursor& tc,
+                                            uint64_t lo, uint64_t hi, int me) {
   if (lo >= hi) return;
+  auto src = [&](int q) { return reinterpret_cast<const float*>(E.arena[q] + B.bucket_off); };
+  auto dst = [&](int q) {
+    return arena ? reinterpret_cast<float*>(E.parena[q] + B.param_off)
+                 : reinterpret_cast<float*>(E.arena[q] + B.bucket_off);
+  };
+  const float* theta_flat = arena ? reinterpret_cast<const float*>(E.parena[me] + B.param_off) : nullptr;
+  const int epi = B.epilogue;
+  const float scale = B.scale, lr = B.lr;
+  const bool need_theta = (epi == CARAMEL_EPI_SGD);
   uint64_t a = (lo + 3) & ~3ull;
   if (a > hi) a = hi;
   uint64_t b = hi & ~3ull;
   if (b < a) b = a;
-  const bool need_theta = (epi == CARAMEL_EPI_SGD);
-  for (uint64_t i = lo + threadIdx.x; i < a; i += blockDim.x) {
-    float s = ld1(src[0] + i);
+  auto scalar = [&](uint64_t i) {
+    float s = ld1(src(0) + i);
 #pragma unroll
-    for (int q = 1; q < P; ++q) s = __fadd_rn(s, ld1(src[q] + i));
+    for (int q = 1; q < P; ++q) s = __fadd_rn(s, ld1(src(q) + i));
     float t = 0.f;
-    if (need_theta) t = seg_theta ? seg_ld1(tc, i, 1) : ld1(theta_flat + i);
+    if (need_theta) t = arena ? ld1(theta_flat + i) : seg_ld1(tc, i, 1);
     float o = epi1(epi, s, t, scale, lr);
 #pragma unroll
-    for (int q = 0; q < P; ++q) st1(dst[q] + i, o);
-  }
+    for (int q = 0; q < P; ++q) st1(dst(q) + i, o);
+  };
+  for (uint64_t i = lo + threadIdx.x; i < a; i += blockDim.x) scalar(i);
   const uint64_t step = 4ull * blockDim.x;
   uint64_t v = a + 4ull * threadIdx.x;
   for (; v + step < b; v += 2 * step) {
     float4 x0[P], x1[P];
 #pragma unroll
     for (int q = 0; q < P; ++q) {
-      x0[q] = ld4(src[q] + v);
-      x1[q] = ld4(src[q] + v + step);
+      x0[q] = ld4(src(q) + v);
+      x1[q] = ld4(src(q) + v + step);
     }
     float4 t0 = make_float4(0.f, 0.f, 0.f, 0.f), t1 = t0;
     if (need_theta) {
-      if (seg_theta) {
-        t0 = seg_ld4(tc, v, 1);
-        t1 = seg_ld4(tc, v + step, 1);
-      } else {
+      if (arena) {
         t0 = ld4(theta_flat + v);
         t1 = ld4(theta_flat + v + step);
+      } else {
+        t0 = seg_ld4(tc, v, 1);
+        t1 = seg_ld4(tc, v + step, 1);
       }
     }
     float4 s0 = x0[0], s1 = x1[0];
@@ -385,47 +396,37 @@ __device__ __forceinline__ void rs_ag_range(const float* const* src, float* cons
     float4 o0 = epi4(epi, s0, t0, scale, lr), o1 = epi4(epi, s1, t1, scale, lr);
 #pragma unroll
     for (int q = 0; q < P; ++q) {
-      st4(dst[q] + v, o0);
-      st4(dst[q] + v + step, o1);
+      st4(dst(q) + v, o0);
+      st4(dst(q) + v + step, o1);
     }
   }
   if (v < b) {
-    float4 s = ld4(src[0] + v);
+    float4 s = ld4(src(0) + v);
 #pragma unroll
-    for (int q = 1; q < P; ++q) s = add4(s, ld4(src[q] + v));
+    for (int q = 1; q < P; ++q) s = add4(s, ld4(src(q) + v));
     float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (need_theta) t = seg_theta ? seg_ld4(tc, v, 1) : ld4(theta_flat + v);
+    if (need_theta) t = arena ? ld4(theta_flat + v) : seg_ld4(tc, v, 1);
     float4 o = epi4(epi, s, t, scale, lr);
 #pragma unroll
-    for (int q = 0; q < P; ++q) st4(dst[q] + v, o);
+    for (int q = 0; q < P; ++q) st4(dst(q) + v, o);
   }
-  for (uint64_t i = b + threadIdx.x; i < hi; i += blockDim.x) {
-    float s = ld1(src[0] + i);
-#pragma unroll
-    for (int q = 1; q < P; ++q) s = __fadd_rn(s, ld1(src[q] + i));
-    float t = 0.f;
-    if (need_theta) t = seg_theta ? seg_ld1(tc, i, 1) : ld1(theta_flat + i);
-    float o = epi1(epi, s, t, scale, lr);
-#pragma unroll
-    for (int q = 0; q < P; ++q) st1(dst[q] + i, o);
-  }
+  for (uint64_t i = b + threadIdx.x; i < hi; i += blockDim.x) scalar(i);
 }
 
 // Pairwise step used by ring and halving-doubling: out = a + b (a first),
 // optionally followed by the epilogue (last reduction of the owner's shard).
 __device__ __forceinline__ void pair_range(const float* a_src, const float* b_src, float* out,
-                                           uint64_t lo, uint64_t hi, bool final_epi, int epi,
-                                           float scale, float lr, const float* theta_flat,
-                                           Cursor& tc, bool seg_theta) {
+                                           uint64_t lo, uint64_t hi, bool final_epi, const caramel_bucket& B,
+                                           const float* theta_flat, Cursor& tc) {
+  const int epi = B.epilogue;
   const bool need_theta = final_epi && epi == CARAMEL_EPI_SGD;
   walk(lo, hi,
        [&](uint64_t v) {
-         float4 x = ld4(a_src + v), y = ld4(b_src + v);
-         float4 s = add4(x, y);
+         float4 s = add4(ld4(a_src + v), ld4(b_src + v));
          if (final_epi) {
            float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-           if (need_theta) t = seg_theta ? seg_ld4(tc, v, 1) : ld4(theta_flat + v);
-           s = epi4(epi, s, t, scale, lr);
+           if (need_theta) t = theta_flat ? ld4(theta_flat + v) : seg_ld4(tc, v, 1);
+           s = epi4(epi, s, t, B.scale, B.lr);
          }
          st4(out + v, s);
        },
@@ -433,8 +434,8 @@ __device__ __forceinline__ void pair_range(const float* a_src, const float* b_sr
          float s = __fadd_rn(ld1(a_src + i), ld1(b_src + i));
          if (final_epi) {
            float t = 0.f;
-           if (need_theta) t = seg_theta ? seg_ld1(tc, i, 1) : ld1(theta_flat + i);
-           s = epi1(epi, s, t, scale, lr);
+           if (need_theta) t = theta_flat ? ld1(theta_flat + i) : seg_ld1(tc, i, 1);
+           s = epi1(epi, s, t, B.scale, B.lr);
          }
          st1(out + i, s);
        });
@@ -446,13 +447,12 @@ __device__ __forceinline__ void copy_range(const float* src, float* dst, uint64_
 }
 
 // Single-rank path (world == 1): no exchange; gather, epilogue and scatter
-// fused in one pass over the bucket.
-__device__ void local_path(const KParams& P, int lr_idx) {
-  const caramel_bucket& B = P.b;
-  const int me = P.rank_base + lr_idx;
-  float* bkt = reinterpret_cast<float*>(P.arena[me] + B.bucket_off);
+// fused in one pass over bucket-local elements [lo, hi).
+__device__ void local_range(const Env& E, const caramel_bucket& B, int lr_idx, uint64_t lo, uint64_t hi) {
+  const int me = E.rank_base + lr_idx;
+  float* bkt = reinterpret_cast<float*>(E.arena[me] + B.bucket_off);
   const bool arena = (B.flags & CARAMEL_F_PARAM_ARENA) && B.epilogue == CARAMEL_EPI_SGD;
-  float* pflat = arena ? reinterpret_cast<float*>(P.parena[me] + B.param_off) : nullptr;
+  float* pflat = arena ? reinterpret_cast<float*>(E.parena[me] + B.param_off) : nullptr;
   const bool pack = B.flags & CARAMEL_F_PACK;
   const bool unpack = (B.flags & CARAMEL_F_UNPACK) && !arena;
   const int out_which = (B.epilogue == CARAMEL_EPI_SGD) ? 1 : 0;
@@ -460,8 +460,6 @@ __device__ void local_path(const KParams& P, int lr_idx) {
   Cursor gc, pc;
   cur_init(gc, segs, B.nseg);
   cur_init(pc, segs, B.nseg);
-  uint64_t lo, hi;
-  tile_of(0, B.numel, gridDim.x, blockIdx.x, lo, hi);
   const int epi = B.epilogue;
   walk(lo, hi,
        [&](uint64_t v) {
@@ -484,78 +482,62 @@ __device__ void local_path(const KParams& P, int lr_idx) {
        });
 }
 
-__global__ void k_epoch_advance(uint32_t* e) { *e += 1; }
-
-template <int PAT, int NP>
-__global__ void __launch_bounds__(THREADS) k_collective(const __grid_constant__ KParams P) {
-  const int lr_idx = blockIdx.y;
-  if (P.world == 1) {
-    local_path(P, lr_idx);
-    return;
-  }
-  const caramel_bucket& B = P.b;
-  const int p = P.world;
+// Per-CTA view of one bucket's collective (world > 1).
+struct BucketRun {
+  const Env* E;
+  const caramel_bucket* B;
   Ctx X;
-  X.P = &P;
-  X.me = P.rank_base + lr_idx;
-  X.world = p;
-  X.j = blockIdx.x;
-  X.G = gridDim.x;
-  X.ns = nslots(PAT, p);
-  // the device counter is advanced by k_epoch_advance earlier on the same
-  // stream, so every CTA of this launch reads the same value
-  const uint32_t epoch = P.epoch ? P.epoch : *reinterpret_cast<const volatile uint32_t*>(P.epoch_dev);
-  X.epoch = epoch;
-  const int me = X.me;
+  int lr_idx;
+  bool arena;
+  uint64_t out_off;
+  const caramel_segment* segs;
 
-  const float* bsrc[MAXR];
-  float* bdst[MAXR];
-  float* odst[MAXR];  // where the final result goes on each rank
-  const bool arena = (B.flags & CARAMEL_F_PARAM_ARENA) && B.epilogue == CARAMEL_EPI_SGD;
+  __device__ __forceinline__ float* bucket(int q) const {
+    return reinterpret_cast<float*>(E->arena[q] + B->bucket_off);
+  }
+  __device__ __forceinline__ float* out(int q) const {
+    return arena ? reinterpret_cast<float*>(E->parena[q] + B->param_off) : bucket(q) + out_off;
+  }
+  __device__ __forceinline__ const float* theta_flat() const {
+    return arena ? reinterpret_cast<const float*>(E->parena[X.me] + B->param_off) : nullptr;
+  }
+  // this CTA's tile of shard s of chunk c
+  __device__ __forceinline__ void shard(int c, int s, uint64_t& lo, uint64_t& hi) const {
+    const uint64_t n = B->numel;
+    const int k = B->depth, p = X.world;
+    uint64_t c0 = split_at(n, k, c), m = split_at(n, k, c + 1) - c0;
+    tile_of(c0 + split_at(m, p, s), c0 + split_at(m, p, s + 1), X.G, X.j, lo, hi);
+  }
+};
+
+__device__ __forceinline__ void make_run(BucketRun& R, const Env& E, const caramel_bucket& B, int pattern,
+                                         int lr_idx, uint32_t epoch) {
+  R.E = &E;
+  R.B = &B;
+  R.lr_idx = lr_idx;
+  R.arena = (B.flags & CARAMEL_F_PARAM_ARENA) && B.epilogue == CARAMEL_EPI_SGD;
   // shuffle all-gathers in place; ring/hd write results to a second region
   // of the bucket so a fast neighbour never overwrites a partial sum that a
   // slower one has yet to pull
-  const uint64_t out_off = (PAT == CARAMEL_SHUFFLE) ? 0 : out_region_elems(B.numel);
-#pragma unroll
-  for (int q = 0; q < MAXR; ++q) {
-    if (q < p) {
-      bdst[q] = reinterpret_cast<float*>(P.arena[q] + B.bucket_off);
-      bsrc[q] = bdst[q];
-      odst[q] = arena ? reinterpret_cast<float*>(P.parena[q] + B.param_off) : bdst[q] + out_off;
-    } else {
-      bdst[q] = nullptr;
-      bsrc[q] = nullptr;
-      odst[q] = nullptr;
-    }
-  }
-  float* mine = bdst[me];
-  const float* theta_flat = arena ? reinterpret_cast<const float*>(P.parena[me] + B.param_off) : nullptr;
-  const bool seg_theta = !arena;
-  const caramel_segment* segs = reinterpret_cast<const caramel_segment*>(B.segs) + (uint64_t)lr_idx * B.nseg;
-  Cursor gc, tc;
-  cur_init(gc, segs, B.nseg);
-  cur_init(tc, segs, B.nseg);
-  const int k = B.depth;
-  const int epi = B.epilogue;
-  const uint64_t n = B.numel;
+  R.out_off = (pattern == CARAMEL_SHUFFLE) ? 0 : out_region_elems(B.numel);
+  R.segs = reinterpret_cast<const caramel_segment*>(B.segs) + (uint64_t)lr_idx * B.nseg;
+  R.X.E = &E;
+  R.X.flag_off = B.flag_off;
+  R.X.me = E.rank_base + lr_idx;
+  R.X.world = E.world;
+  R.X.j = blockIdx.x;
+  R.X.G = B.ctas;
+  R.X.ns = nslots(pattern, E.world);
+  R.X.epoch = epoch;
+}
 
-  auto chunk_lo = [&](int c) { return split_at(n, k, c); };
-  auto shard = [&](int c, int s, uint64_t& lo, uint64_t& hi) {
-    uint64_t c0 = chunk_lo(c), m = chunk_lo(c + 1) - c0;
-    uint64_t a = c0 + split_at(m, p, s), b = c0 + split_at(m, p, s + 1);
-    tile_of(a, b, X.G, X.j, lo, hi);  // this CTA's tile of shard s
-  };
-  // range of shards [s0, s1) of chunk c, tiled for this CTA (shard-wise tiles)
-  auto for_shards = [&](int c, int s0, int s1, auto fn) {
-    for (int s = s0; s < s1; ++s) {
-      uint64_t lo, hi;
-      shard(c, s, lo, hi);
-      fn(lo, hi);
-    }
-  };
-
-  // ring / hd: wait until every rank that read my buffers last epoch is done
+// phase 1 (all patterns): ring/hd buffer-reuse guard, fused pack, ready flags
+template <int PAT>
+__device__ void phase_pack(const BucketRun& R) {
+  const int me = R.X.me, p = R.X.world;
+  const uint32_t epoch = R.X.epoch;
   if (PAT != CARAMEL_SHUFFLE && epoch > 1) {
+    // every rank that read my buffers last epoch must be done with them
     int srcs[MAXR];
     int ns = 0;
     if (PAT == CARAMEL_RING) {
@@ -563,127 +545,153 @@ __global__ void __launch_bounds__(THREADS) k_collective(const __grid_constant__ 
     } else {
       for (int d = 1; d < p; d <<= 1) srcs[ns++] = me ^ d;
     }
-    X.wait_from(0, X.ns - 1, srcs, ns, epoch - 1);
+    R.X.wait_from(0, R.X.ns - 1, srcs, ns, epoch - 1);
   }
-
-  // ---- pack (K1, fused) + ready ------------------------------------------
-  const bool pack = B.flags & CARAMEL_F_PACK;
-  for (int c = 0; c < k; ++c) {
+  const bool pack = R.B->flags & CARAMEL_F_PACK;
+  float* mine = R.bucket(me);
+  Cursor gc;
+  cur_init(gc, R.segs, R.B->nseg);
+  for (int c = 0; c < R.B->depth; ++c) {
     if (pack) {
-      for_shards(c, 0, p, [&](uint64_t lo, uint64_t hi) {
+      for (int s = 0; s < p; ++s) {
+        uint64_t lo, hi;
+        R.shard(c, s, lo, hi);
         walk(lo, hi, [&](uint64_t v) { st4(mine + v, seg_ld4(gc, v, 0)); },
              [&](uint64_t i) { st1(mine + i, seg_ld1(gc, i, 0)); });
-      });
+      }
     }
     if (PAT == CARAMEL_SHUFFLE) {
-      X.publish_all(c, SLOT_READY);
-    } else if (PAT == CARAMEL_RING) {
-      int t = (me + 1) % p;
-      X.publish(c, SLOT_READY, &t, 1);
+      R.X.publish_all(c, SLOT_READY);
     } else {
-      int t = me ^ (p >> 1);
-      X.publish(c, SLOT_READY, &t, 1);
+      int t = (PAT == CARAMEL_RING) ? (me + 1) % p : (me ^ (p >> 1));
+      R.X.publish(c, SLOT_READY, &t, 1);
     }
   }
+}
 
-  if (PAT == CARAMEL_SHUFFLE) {
-    // ---- two-shot: RS own shard in rank order, epilogue, AG store --------
-    for (int c = 0; c < k; ++c) {
-      X.wait_all(c, SLOT_READY, epoch);
+// phase 2, two-shot: reduce own shard in rank order, epilogue, all-gather by store
+template <int NP>
+__device__ void phase_shuffle(const BucketRun& R) {
+  Cursor tc;
+  cur_init(tc, R.segs, R.B->nseg);
+  for (int c = 0; c < R.B->depth; ++c) {
+    R.X.wait_all(c, SLOT_READY, R.X.epoch);
+    uint64_t lo, hi;
+    R.shard(c, R.X.me, lo, hi);
+    rs_ag_range<NP>(*R.E, *R.B, R.arena, tc, lo, hi, R.X.me);
+    R.X.publish_all(c, SLOT_DONE);
+  }
+}
+
+__device__ void phase_ring(const BucketRun& R) {
+  const int me = R.X.me, p = R.X.world;
+  const int left = (me + p - 1) % p, right = (me + 1) % p;
+  float* mine = R.bucket(me);
+  Cursor tc;
+  cur_init(tc, R.segs, R.B->nseg);
+  const float* th = R.theta_flat();
+  for (int c = 0; c < R.B->depth; ++c) {
+    // reduce-scatter: at step t rank r folds its own share of shard
+    // (r-1-t) mod p into the left neighbour's running sum (the chain of
+    // shard s starts at rank s+1 and ends at its owner s)
+    for (int t = 1; t <= p - 1; ++t) {
+      R.X.wait_from(c, t == 1 ? SLOT_READY : t - 1, &left, 1, R.X.epoch);
+      const int s = ((me - 1 - t) % p + p) % p;
+      const bool last = (t == p - 1);
       uint64_t lo, hi;
-      shard(c, me, lo, hi);
-      rs_ag_range<NP>(bsrc, odst, theta_flat, tc, lo, hi, epi, B.scale, B.lr, seg_theta);
-      X.publish_all(c, SLOT_DONE);
+      R.shard(c, s, lo, hi);
+      pair_range(R.bucket(left), mine, last ? R.out(me) : mine, lo, hi, last, *R.B, th, tc);
+      R.X.publish(c, t, &right, 1);
     }
-    for (int c = 0; c < k; ++c) X.wait_all(c, SLOT_DONE, epoch);
-  } else if (PAT == CARAMEL_RING) {
-    const int left = (me + p - 1) % p, right = (me + 1) % p;
-    for (int c = 0; c < k; ++c) {
-      // reduce-scatter: at step t rank r folds its own share of shard
-      // (r-1-t) mod p into the left neighbour's running sum (the chain of
-      // shard s starts at rank s+1 and ends at its owner s).
-      for (int t = 1; t <= p - 1; ++t) {
-        X.wait_from(c, t == 1 ? SLOT_READY : t - 1, &left, 1, epoch);
-        int s = ((me - 1 - t) % p + p) % p;
-        const bool last = (t == p - 1);
-        uint64_t lo, hi;
-        shard(c, s, lo, hi);
-        pair_range(bsrc[left], mine, last ? odst[me] : mine, lo, hi, last, epi, B.scale, B.lr,
-                   theta_flat, tc, seg_theta);
-        X.publish(c, t, &right, 1);
-      }
-      // all-gather: at step t copy shard (r-t) mod p from the left neighbour
-      for (int t = 1; t <= p - 1; ++t) {
-        X.wait_from(c, (p - 1) + (t - 1), &left, 1, epoch);
-        int s = ((me - t) % p + p) % p;
-        uint64_t lo, hi;
-        shard(c, s, lo, hi);
-        copy_range(odst[left], odst[me], lo, hi);
-        X.publish(c, (p - 1) + t, &right, 1);
-      }
+    // all-gather: at step t copy shard (r-t) mod p from the left neighbour
+    for (int t = 1; t <= p - 1; ++t) {
+      R.X.wait_from(c, (p - 1) + (t - 1), &left, 1, R.X.epoch);
+      const int s = ((me - t) % p + p) % p;
+      uint64_t lo, hi;
+      R.shard(c, s, lo, hi);
+      copy_range(R.out(left), R.out(me), lo, hi);
+      R.X.publish(c, (p - 1) + t, &right, 1);
     }
-  } else {  // halving-doubling (p a power of two)
-    // Stages: 0 = pack, 1..L = halving rounds, L+1..2L = doubling rounds.
-    // Stage s reads from partner(s); finishing stage s signals slot s to the
-    // rank that reads from me next, partner(s+1).
-    const int L = ilog2i(p);
-    auto partner_of = [&](int stage) {
-      return stage <= L ? (me ^ (p >> stage)) : (me ^ (1 << (stage - L - 1)));
-    };
-    for (int c = 0; c < k; ++c) {
-      // vector halving, distance halving: round i pairs r with r ^ (p >> (i+1));
-      // r keeps the half of its active block range that contains block r and
-      // sums it as (lower rank's value) + (higher rank's value)
-      for (int i = 0; i < L; ++i) {
-        const int stage = i + 1;
-        const int dist = p >> (i + 1);
-        const int partner = partner_of(stage);
-        X.wait_from(c, stage - 1, &partner, 1, epoch);
-        const int base = me & ~(2 * dist - 1);
-        const int s0 = (me & dist) ? base + dist : base;
-        const bool last = (i == L - 1);
-        const float* lo_src = (me < partner) ? mine : bsrc[partner];
-        const float* hi_src = (me < partner) ? bsrc[partner] : mine;
-        for_shards(c, s0, s0 + dist, [&](uint64_t lo, uint64_t hi) {
-          pair_range(lo_src, hi_src, last ? odst[me] : mine, lo, hi, last, epi, B.scale, B.lr,
-                     theta_flat, tc, seg_theta);
-        });
+  }
+}
+
+__device__ void phase_hd(const BucketRun& R) {
+  // Stages: 0 = pack, 1..L = halving rounds, L+1..2L = doubling rounds.
+  // Stage s reads from partner(s); finishing stage s signals slot s to the
+  // rank that reads from me next, partner(s+1).
+  const int me = R.X.me, p = R.X.world;
+  const int L = ilog2i(p);
+  auto partner_of = [&](int stage) {
+    return stage <= L ? (me ^ (p >> stage)) : (me ^ (1 << (stage - L - 1)));
+  };
+  float* mine = R.bucket(me);
+  Cursor tc;
+  cur_init(tc, R.segs, R.B->nseg);
+  const float* th = R.theta_flat();
+  for (int c = 0; c < R.B->depth; ++c) {
+    // vector halving, distance halving: round i pairs r with r ^ (p >> (i+1));
+    // r keeps the half of its active block range that contains block r and
+    // sums it as (lower rank's value) + (higher rank's value)
+    for (int i = 0; i < L; ++i) {
+      const int stage = i + 1;
+      const int dist = p >> (i + 1);
+      const int partner = partner_of(stage);
+      R.X.wait_from(c, stage - 1, &partner, 1, R.X.epoch);
+      const int base = me & ~(2 * dist - 1);
+      const int s0 = (me & dist) ? base + dist : base;
+      const bool last = (i == L - 1);
+      const float* lo_src = (me < partner) ? mine : R.bucket(partner);
+      const float* hi_src = (me < partner) ? R.bucket(partner) : mine;
+      for (int s = s0; s < s0 + dist; ++s) {
+        uint64_t lo, hi;
+        R.shard(c, s, lo, hi);
+        pair_range(lo_src, hi_src, last ? R.out(me) : mine, lo, hi, last, *R.B, th, tc);
+      }
+      const int nxt = partner_of(stage + 1);
+      R.X.publish(c, stage, &nxt, 1);
+    }
+    // vector doubling: round i pairs r with r ^ (1 << i); copy the partner's
+    // finished blocks into my output
+    for (int i = 0; i < L; ++i) {
+      const int stage = L + 1 + i;
+      const int dist = 1 << i;
+      const int partner = partner_of(stage);
+      R.X.wait_from(c, stage - 1, &partner, 1, R.X.epoch);
+      const int s0 = partner & ~(dist - 1);
+      for (int s = s0; s < s0 + dist; ++s) {
+        uint64_t lo, hi;
+        R.shard(c, s, lo, hi);
+        copy_range(R.out(partner), R.out(me), lo, hi);
+      }
+      if (i + 1 < L) {
         const int nxt = partner_of(stage + 1);
-        X.publish(c, stage, &nxt, 1);
-      }
-      // vector doubling: round i pairs r with r ^ (1 << i); copy the partner's
-      // finished blocks into my output
-      for (int i = 0; i < L; ++i) {
-        const int stage = L + 1 + i;
-        const int dist = 1 << i;
-        const int partner = partner_of(stage);
-        X.wait_from(c, stage - 1, &partner, 1, epoch);
-        const int s0 = partner & ~(dist - 1);
-        for_shards(c, s0, s0 + dist, [&](uint64_t lo, uint64_t hi) {
-          copy_range(odst[partner], odst[me], lo, hi);
-        });
-        if (i + 1 < L) {
-          const int nxt = partner_of(stage + 1);
-          X.publish(c, stage, &nxt, 1);
-        }
+        R.X.publish(c, stage, &nxt, 1);
       }
     }
   }
+}
 
-  // ---- unpack (fused K4 scatter) ------------------------------------------
-  if ((B.flags & CARAMEL_F_UNPACK) && !arena) {
-    const int which = (epi == CARAMEL_EPI_SGD) ? 1 : 0;
+// phase 3: (shuffle) wait for every rank's all-gather; fused unpack; (ring/hd)
+// release the buffers I read from
+template <int PAT>
+__device__ void phase_finish(const BucketRun& R) {
+  const int me = R.X.me, p = R.X.world;
+  if (PAT == CARAMEL_SHUFFLE)
+    for (int c = 0; c < R.B->depth; ++c) R.X.wait_all(c, SLOT_DONE, R.X.epoch);
+  if ((R.B->flags & CARAMEL_F_UNPACK) && !R.arena) {
+    const int which = (R.B->epilogue == CARAMEL_EPI_SGD) ? 1 : 0;
+    const float* res = R.out(me);
     Cursor uc;
-    cur_init(uc, segs, B.nseg);
-    for (int c = 0; c < k; ++c) {
-      for_shards(c, 0, p, [&](uint64_t lo, uint64_t hi) {
-        walk(lo, hi, [&](uint64_t v) { seg_st4(uc, v, which, ld4(odst[me] + v)); },
-             [&](uint64_t i) { seg_st1(uc, i, which, ld1(odst[me] + i)); });
-      });
+    cur_init(uc, R.segs, R.B->nseg);
+    for (int c = 0; c < R.B->depth; ++c) {
+      for (int s = 0; s < p; ++s) {
+        uint64_t lo, hi;
+        R.shard(c, s, lo, hi);
+        walk(lo, hi, [&](uint64_t v) { seg_st4(uc, v, which, ld4(res + v)); },
+             [&](uint64_t i) { seg_st1(uc, i, which, ld1(res + i)); });
+      }
     }
   }
-
-  // ring / hd: tell every rank I read from that I am done with its buffers
   if (PAT != CARAMEL_SHUFFLE) {
     int tg[MAXR];
     int nt = 0;
@@ -692,7 +700,98 @@ __global__ void __launch_bounds__(THREADS) k_collective(const __grid_constant__ 
     } else {
       for (int d = 1; d < p; d <<= 1) tg[nt++] = me ^ d;
     }
-    X.publish(0, X.ns - 1, tg, nt);
+    R.X.publish(0, R.X.ns - 1, tg, nt);
+  }
+}
+
+template <int PAT, int NP>
+__device__ __forceinline__ void run_bucket(const Env& E, const caramel_bucket& B, int lr_idx, uint32_t epoch) {
+  BucketRun R;
+  make_run(R, E, B, PAT, lr_idx, epoch);
+  phase_pack<PAT>(R);
+  if (PAT == CARAMEL_SHUFFLE) phase_shuffle<NP>(R);
+  else if (PAT == CARAMEL_RING) phase_ring(R);
+  else phase_hd(R);
+  phase_finish<PAT>(R);
+}
+
+__global__ void k_epoch_advance(uint32_t* e) { *e += 1; }
+
+template <int PAT, int NP>
+__global__ void __launch_bounds__(THREADS) k_collective(const __grid_constant__ KParams P) {
+  const int lr_idx = blockIdx.y;
+  if (P.env.world == 1) {
+    uint64_t lo, hi;
+    tile_of(0, P.b.numel, gridDim.x, blockIdx.x, lo, hi);
+    local_range(P.env, P.b, lr_idx, lo, hi);
+    return;
+  }
+  // local copies: the phases hold pointers to these, and generic pointers to
+  // kernel parameters are not valid across real device-function calls
+  const Env E = P.env;
+  const caramel_bucket B = P.b;
+  run_bucket<PAT, NP>(E, B, lr_idx, launch_epoch(E));
+}
+
+// Many buckets in one launch (launch order).  world == 1: the concatenated
+// element space is tiled evenly over the grid.  Shuffle: phase-major -- every
+// bucket's pack + ready flags first, then every bucket's reduce/all-gather,
+// then every bucket's completion wait -- so no CTA idles on one bucket's
+// flags while another bucket's work is available.  Ring/hd: bucket by bucket.
+// CTA j takes part in bucket b iff j < b.ctas (same rule on every rank).
+template <int PAT, int NP>
+__global__ void __launch_bounds__(THREADS) k_collective_many(const __grid_constant__ MParams P) {
+  const int lr_idx = blockIdx.y;
+  const Env E = P.env;  // local copy: phases keep pointers to it
+  if (E.world == 1) {
+    uint64_t lo, hi;
+    tile_of(0, P.prefix[P.nb], gridDim.x, blockIdx.x, lo, hi);
+    if (lo >= hi) return;
+    // first bucket overlapping [lo, hi)
+    int a = 0, b = P.nb - 1;
+    while (a < b) {
+      int m = (a + b + 1) >> 1;
+      if (P.prefix[m] <= lo) a = m; else b = m - 1;
+    }
+    for (int i = a; i < P.nb && P.prefix[i] < hi; ++i) {
+      const caramel_bucket B = P.bs[i];
+      const uint64_t b0 = P.prefix[i];
+      const uint64_t l = lo > b0 ? lo - b0 : 0;
+      const uint64_t h = (hi < b0 + B.numel ? hi : b0 + B.numel) - b0;
+      // bucket-local 4-alignment keeps the vector body aligned (buckets start 16B aligned)
+      local_range(E, B, lr_idx, l, h);
+    }
+    return;
+  }
+  const uint32_t epoch = launch_epoch(E);
+  if (PAT == CARAMEL_SHUFFLE) {
+    for (int i = 0; i < P.nb; ++i) {
+      const caramel_bucket B = P.bs[i];
+      if ((int)blockIdx.x >= B.ctas || B.numel == 0) continue;
+      BucketRun R;
+      make_run(R, E, B, PAT, lr_idx, epoch);
+      phase_pack<PAT>(R);
+    }
+    for (int i = 0; i < P.nb; ++i) {
+      const caramel_bucket B = P.bs[i];
+      if ((int)blockIdx.x >= B.ctas || B.numel == 0) continue;
+      BucketRun R;
+      make_run(R, E, B, PAT, lr_idx, epoch);
+      phase_shuffle<NP>(R);
+    }
+    for (int i = 0; i < P.nb; ++i) {
+      const caramel_bucket B = P.bs[i];
+      if ((int)blockIdx.x >= B.ctas || B.numel == 0) continue;
+      BucketRun R;
+      make_run(R, E, B, PAT, lr_idx, epoch);
+      phase_finish<PAT>(R);
+    }
+  } else {
+    for (int i = 0; i < P.nb; ++i) {
+      const caramel_bucket B = P.bs[i];
+      if ((int)blockIdx.x >= B.ctas || B.numel == 0) continue;
+      run_bucket<PAT, NP>(E, B, lr_idx, epoch);
+    }
   }
 }
 
@@ -946,9 +1045,11 @@ int caramel_unpack(const caramel_segment* segs, int32_t nseg, uint64_t numel, co
 }  // extern "C"
 
 typedef void (*kfn_t)(const KParams);
+typedef void (*mfn_t)(const MParams);
 
 template <int PAT>
 static kfn_t pick_np(int p) {
+  if (PAT != CARAMEL_SHUFFLE) return k_collective<PAT, 2>;  // NP only shapes the two-shot reduce
   switch (p) {
     case 1: return k_collective<PAT, 1>;
     case 2: return k_collective<PAT, 2>;
@@ -961,11 +1062,24 @@ static kfn_t pick_np(int p) {
   }
 }
 
+template <int PAT>
+static mfn_t pick_np_many(int p) {
+  if (PAT != CARAMEL_SHUFFLE) return k_collective_many<PAT, 2>;
+  switch (p) {
+    case 1: return k_collective_many<PAT, 1>;
+    case 2: return k_collective_many<PAT, 2>;
+    case 3: return k_collective_many<PAT, 3>;
+    case 4: return k_collective_many<PAT, 4>;
+    case 5: return k_collective_many<PAT, 5>;
+    case 6: return k_collective_many<PAT, 6>;
+    case 7: return k_collective_many<PAT, 7>;
+    default: return k_collective_many<PAT, 8>;
+  }
+}
+
 extern "C" {
 
-static int launch(caramel_ctx* c, const caramel_bucket* b, uint32_t epoch, void* stream) {
-  if (!c || !b) return set_err(CARAMEL_EINVAL, "null argument");
-  if (!c->imported) return set_err(CARAMEL_ESTATE, "peer arenas not mapped (call caramel_import)");
+static int validate_bucket(const caramel_ctx* c, const caramel_bucket* b) {
   int rc = validate_workers(b->pattern, c->world);
   if (rc) return rc;
   if (b->depth < 1 || b->depth > CARAMEL_MAX_DEPTH)
@@ -978,7 +1092,7 @@ static int launch(caramel_ctx* c, const caramel_bucket* b, uint32_t epoch, void*
                                                                          : b->numel);
   if (b->bucket_off + span > c->arena_bytes)
     return set_err(CARAMEL_EINVAL, "bucket [%llu, +%llu B) exceeds the arena", (unsigned long long)b->bucket_off,
-                   (unsigned long long)(b->numel * 4));
+                   (unsigned long long)span);
   const bool arena = (b->flags & CARAMEL_F_PARAM_ARENA) && b->epilogue == CARAMEL_EPI_SGD;
   if (arena) {
     if (!c->param_bytes) return set_err(CARAMEL_EINVAL, "PARAM_ARENA requested but no parameter arena");
@@ -993,41 +1107,55 @@ static int launch(caramel_ctx* c, const caramel_bucket* b, uint32_t epoch, void*
     if (b->flag_off + fb > c->arena_bytes) return set_err(CARAMEL_EINVAL, "flag block exceeds the arena");
     if (b->flag_off & 3) return set_err(CARAMEL_EINVAL, "flag_off must be 4-byte aligned");
   }
+  return 0;
+}
 
-  KParams P;
-  memset(&P, 0, sizeof(P));
+static void fill_env(const caramel_ctx* c, Env& E, uint32_t epoch) {
+  memset(&E, 0, sizeof(E));
   for (int q = 0; q < MAXR; ++q) {
-    P.arena[q] = c->arena[q];
-    P.parena[q] = c->parena[q];
+    E.arena[q] = c->arena[q];
+    E.parena[q] = c->parena[q];
   }
-  P.b = *b;
-  P.world = c->world;
-  P.rank_base = c->rank;
-  P.epoch = epoch;
-  P.epoch_dev = c->epoch_dev;
-  P.timeout_ns = c->timeout_ns;
-  P.status = c->status;
+  E.world = c->world;
+  E.rank_base = c->rank;
+  E.epoch = epoch;
+  E.epoch_dev = c->epoch_dev;
+  E.timeout_ns = c->timeout_ns;
+  E.status = c->status;
+}
 
+// rank emulation: all ranks' CTAs spin on each other, so they must be
+// co-resident -- a cooperative launch guarantees it or fails
+static int coop_launch(const caramel_ctx* c, const void* fn, dim3 grid, void** args, void* stream) {
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, THREADS, 0));
+  if ((uint64_t)per_sm * c->sms < (uint64_t)grid.x * grid.y)
+    return set_err(CARAMEL_EINVAL, "emulated launch of %u x %u CTAs exceeds co-residency (%d per SM)", grid.x,
+                   grid.y, per_sm);
+  CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, dim3(THREADS), args, 0, (cudaStream_t)stream));
+  return 0;
+}
+
+static int launch(caramel_ctx* c, const caramel_bucket* b, uint32_t epoch, void* stream) {
+  if (!c || !b) return set_err(CARAMEL_EINVAL, "null argument");
+  if (!c->imported) return set_err(CARAMEL_ESTATE, "peer arenas not mapped (call caramel_import)");
+  int rc = validate_bucket(c, b);
+  if (rc) return rc;
+  if (b->numel == 0) return 0;
+  KParams P;
+  fill_env(c, P.env, epoch);
+  P.b = *b;
   kfn_t fn;
   if (b->pattern == CARAMEL_SHUFFLE) fn = pick_np<CARAMEL_SHUFFLE>(c->world);
   else if (b->pattern == CARAMEL_RING) fn = pick_np<CARAMEL_RING>(c->world);
   else fn = pick_np<CARAMEL_HD>(c->world);
-
-  dim3 grid(b->ctas, c->nlocal), block(THREADS);
+  dim3 grid(b->ctas, c->nlocal);
   if (c->nlocal > 1) {
-    // rank emulation: all ranks' CTAs spin on each other, so they must be
-    // co-resident -- a cooperative launch guarantees it or fails.
-    int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, THREADS, 0));
-    if ((uint64_t)per_sm * c->sms < (uint64_t)b->ctas * c->nlocal)
-      return set_err(CARAMEL_EINVAL, "emulated launch of %d x %d CTAs exceeds co-residency (%d per SM)", b->ctas,
-                     c->nlocal, per_sm);
     void* args[] = {(void*)&P};
-    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fn, grid, block, args, 0, (cudaStream_t)stream));
-  } else {
-    fn<<<grid, block, 0, (cudaStream_t)stream>>>(P);
-    CUDA_TRY(cudaGetLastError());
+    return coop_launch(c, (const void*)fn, grid, args, stream);
   }
+  fn<<<grid, THREADS, 0, (cudaStream_t)stream>>>(P);
+  CUDA_TRY(cudaGetLastError());
   return 0;
 }
 
@@ -1048,6 +1176,46 @@ int caramel_allreduce_update(caramel_ctx* c, const caramel_bucket* b, uint32_t e
   if (b && b->epilogue != CARAMEL_EPI_SGD)
     return set_err(CARAMEL_EINVAL, "caramel_allreduce_update requires CARAMEL_EPI_SGD");
   return launch(c, b, epoch, stream);
+}
+
+int caramel_allreduce_many(caramel_ctx* c, const caramel_bucket* host, int32_t count, uint64_t dev_buckets,
+                           uint64_t dev_prefix, uint32_t epoch, void* stream) {
+  if (!c || !host || count < 1 || !dev_buckets || !dev_prefix)
+    return set_err(CARAMEL_EINVAL, "allreduce_many: null argument or empty list");
+  if (!c->imported) return set_err(CARAMEL_ESTATE, "peer arenas not mapped (call caramel_import)");
+  const int pattern = host[0].pattern;
+  int gmax = 1;
+  uint64_t total = 0;
+  for (int i = 0; i < count; ++i) {
+    if (host[i].pattern != pattern) return set_err(CARAMEL_EINVAL, "allreduce_many: mixed patterns");
+    int rc = validate_bucket(c, &host[i]);
+    if (rc) return rc;
+    if (host[i].ctas > gmax) gmax = host[i].ctas;
+    total += host[i].numel;
+  }
+  if (total == 0) return 0;
+  if (c->world == 1) {
+    uint64_t g = (total + (uint64_t)THREADS * 16 - 1) / ((uint64_t)THREADS * 16);
+    uint64_t cap = (uint64_t)c->sms * 4;
+    gmax = (int)(g < 1 ? 1 : (g > cap ? cap : g));
+  }
+  MParams P;
+  fill_env(c, P.env, epoch);
+  P.bs = reinterpret_cast<const caramel_bucket*>(dev_buckets);
+  P.prefix = reinterpret_cast<const uint64_t*>(dev_prefix);
+  P.nb = count;
+  mfn_t fn;
+  if (pattern == CARAMEL_SHUFFLE) fn = pick_np_many<CARAMEL_SHUFFLE>(c->world);
+  else if (pattern == CARAMEL_RING) fn = pick_np_many<CARAMEL_RING>(c->world);
+  else fn = pick_np_many<CARAMEL_HD>(c->world);
+  dim3 grid(gmax, c->nlocal);
+  if (c->nlocal > 1) {
+    void* args[] = {(void*)&P};
+    return coop_launch(c, (const void*)fn, grid, args, stream);
+  }
+  fn<<<grid, THREADS, 0, (cudaStream_t)stream>>>(P);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
 }
 
 }  // extern "C"

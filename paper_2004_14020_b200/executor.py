@@ -27,6 +27,7 @@ stream in the enforced order.
 
 from __future__ import annotations
 
+import ctypes
 import hashlib
 import json
 from dataclasses import dataclass, field
@@ -182,6 +183,7 @@ class Aggregator:
         self._hooks = []
         self.epoch = 0
         self.launches = 0
+        self._build_list()
 
     # -- setup -----------------------------------------------------------------
     def _adopt_params(self) -> None:
@@ -206,10 +208,23 @@ class Aggregator:
                                 param_off=b.param_off, lr=self.lr, scale=scale)
         return _Live(spec=b, desc=desc, table=table, members=list(b.param_ids))
 
+    def _build_list(self) -> None:
+        """Host + device copies of every bucket descriptor (launch order) and
+        the element prefix sums, for the one-launch pass (caramel_allreduce_many)."""
+        n = len(self._live)
+        self._host_list = (N.Bucket * n)(*[lv.desc for lv in self._live])
+        raw = bytes(self._host_list)
+        self._dev_list = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(self.device)
+        prefix = [0]
+        for lv in self._live:
+            prefix.append(prefix[-1] + lv.spec.numel)
+        self._dev_prefix = torch.tensor(prefix, dtype=torch.int64, device=self.device)
+
     def refresh_tables(self) -> None:
         """Rebuild segment tables (after gradients were reallocated)."""
         self._live = [self._make_live(lv.spec) for lv in self._live]
         self._by_param = {pid: lv for lv in self._live for pid in lv.members}
+        self._build_list()
 
     def check_tables(self) -> bool:
         """True if every gradient still lives where the segment tables point."""
@@ -226,17 +241,24 @@ class Aggregator:
         self.ctx.allreduce(lv.desc, 0, stream)
         self.launches += 1
 
-    def step(self, stream: torch.cuda.Stream | None = None) -> None:
+    def step(self, stream: torch.cuda.Stream | None = None, fused: bool = True) -> None:
         """Aggregate every bucket now, in launch order, on `stream` (default:
-        the current stream).  Graph-capturable: epochs come from the device
+        the current stream): one launch for the whole list (fused=True) or one
+        launch per bucket.  Graph-capturable: epochs come from the device
         counter advanced first on the same stream."""
         s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
-        N.check(N.lib().caramel_epoch_advance(self.ctx._ctx, __import__("ctypes").c_void_p(s)))
-        for lv in self._live:
-            self._launch(lv, s)
+        N.check(N.lib().caramel_epoch_advance(self.ctx._ctx, ctypes.c_void_p(s)))
+        if fused:
+            N.check(N.lib().caramel_allreduce_many(self.ctx._ctx, self._host_list, len(self._live),
+                                                   self._dev_list.data_ptr(), self._dev_prefix.data_ptr(), 0,
+                                                   ctypes.c_void_p(s)))
+            self.launches += 1
+        else:
+            for lv in self._live:
+                self._launch(lv, s)
 
-    def kernels_per_step(self) -> int:
-        return 1 + len(self._live)
+    def kernels_per_step(self, fused: bool = True) -> int:
+        return 2 if fused else 1 + len(self._live)
 
     # -- overlapped mode: launch when the last gradient of a bucket is ready ----
     def attach_hooks(self) -> None:
@@ -262,7 +284,7 @@ class Aggregator:
         cur = torch.cuda.current_stream(self.device)
         self.comm_stream.wait_stream(cur)
         N.check(N.lib().caramel_epoch_advance(self.ctx._ctx,
-                                              __import__("ctypes").c_void_p(self.comm_stream.cuda_stream)))
+                                              ctypes.c_void_p(self.comm_stream.cuda_stream)))
 
     def _drain(self) -> None:
         """Launch every ready bucket from the head of the launch order."""

@@ -205,3 +205,90 @@ def test_errors_are_reported_not_raised_in_c():
     with pytest.raises(N.CaramelError, match="power-of-two"):
         ctx3.allreduce(b, 1, torch.cuda.current_stream().cuda_stream)
     ctx3.close()
+
+
+def run_emulated_many(pattern, p, bucket_shapes, depths, epi, *, param_arena=False, epochs=2, seed=11):
+    """Several buckets in ONE launch (caramel_allreduce_many), device epoch
+    counter; every bucket checked against the oracle on every rank."""
+    import ctypes
+
+    N, comm = _native()
+    dev = torch.device("cuda:0")
+    rng = np.random.default_rng(seed)
+    lr = 0.25
+    # layout
+    off, poff, specs = 0, 0, []
+    for shapes, depth in zip(bucket_shapes, depths):
+        numel = sum(int(np.prod(s)) for s in shapes)
+        c0, bbytes, _ = N.bucket_layout(numel, depth, pattern, p)
+        ctas = min(c0, max(1, 64 // p))
+        fbytes = N.flag_bytes_for(depth, ctas, pattern, p)
+        boff = off
+        foff = (boff + bbytes + 255) // 256 * 256
+        off = (foff + fbytes + 255) // 256 * 256
+        specs.append((shapes, depth, numel, ctas, boff, foff, poff))
+        poff = (poff + 4 * numel + 255) // 256 * 256
+    ctx = comm.Context(0, p, arena_bytes=off, param_bytes=poff if param_arena else 0, nlocal=p)
+    thetas = [[rng.standard_normal(s).astype(np.float32) for s in sp[0]] for sp in specs]
+    th_dev = [[_members(dev, sp[0], thetas[i], False) for _ in range(p)] for i, sp in enumerate(specs)]
+    if param_arena:
+        for i, sp in enumerate(specs):
+            for r in range(p):
+                ctx.arena_view(r, sp[6], sp[2], param=True).copy_(torch.from_numpy(O.np_pack(thetas[i])).to(dev))
+    stream = torch.cuda.current_stream().cuda_stream
+    flags = N.F_PACK | (N.F_PARAM_ARENA if param_arena else N.F_UNPACK)
+    for e in range(epochs):
+        grads, g_devs, descs, tables = [], [], [], []
+        for i, (shapes, depth, numel, ctas, boff, foff, pof) in enumerate(specs):
+            gr = [[rng.standard_normal(s).astype(np.float32) for s in shapes] for _ in range(p)]
+            gd = [_members(dev, shapes, gr[r], False) for r in range(p)]
+            tab = comm.segment_table([comm.segments_for(gd[r], None if param_arena else th_dev[i][r])
+                                      for r in range(p)], dev)
+            grads.append(gr)
+            g_devs.append(gd)
+            tables.append(tab)
+            descs.append(comm.make_bucket(numel, boff, foff, depth=depth, pattern=pattern, epilogue=epi,
+                                          flags=flags, ctas=ctas, segs=tab, nseg=len(shapes), param_off=pof,
+                                          lr=lr, scale=1.0 / p))
+        host = (N.Bucket * len(descs))(*descs)
+        dev_list = torch.frombuffer(bytearray(bytes(host)), dtype=torch.uint8).to(dev)
+        prefix = torch.tensor(np.concatenate([[0], np.cumsum([sp[2] for sp in specs])]), dtype=torch.int64,
+                              device=dev)
+        N.check(N.lib().caramel_epoch_advance(ctx._ctx, ctypes.c_void_p(stream)))
+        N.check(N.lib().caramel_allreduce_many(ctx._ctx, host, len(descs), dev_list.data_ptr(), prefix.data_ptr(),
+                                               0, ctypes.c_void_p(stream)))
+        ctx.status()
+        torch.cuda.synchronize()
+        for i, (shapes, depth, numel, ctas, boff, foff, pof) in enumerate(specs):
+            want = O.np_allreduce(pattern, [O.np_pack(row) for row in grads[i]], depth, epi, 1.0 / p, lr,
+                                  O.np_pack(thetas[i]))
+            for r in range(p):
+                if epi == N.EPI_SGD and param_arena:
+                    got = ctx.arena_view(r, pof, numel, param=True).cpu().numpy()
+                elif epi == N.EPI_SGD:
+                    got = _flat(th_dev[i][r])
+                else:
+                    got = _flat(g_devs[i][r])
+                assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (i, r, e)
+            if epi == N.EPI_SGD:
+                thetas[i] = O.np_unpack(want, shapes)
+    ctx.close()
+
+
+MANY_BUCKETS = [SHAPES_RAGGED, [(129,)], SHAPES_SMALL, [(1,)], SHAPES_LARGE, [(7, 7), (3,)]]
+MANY_DEPTHS = [3, 1, 2, 1, 8, 2]
+
+
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
+@pytest.mark.parametrize("pattern", ["shuffle", "ring", "hd"])
+def test_many_buckets_one_launch(p, pattern):
+    N, _ = _native()
+    pat = {"ring": N.RING, "hd": N.HD, "shuffle": N.SHUFFLE}[pattern]
+    run_emulated_many(pat, p, MANY_BUCKETS, MANY_DEPTHS, N.EPI_SGD, param_arena=True)
+
+
+@pytest.mark.parametrize("epi", [0, 1, 2])
+def test_many_buckets_unpack_modes(epi):
+    N, _ = _native()
+    run_emulated_many(N.SHUFFLE, 4, MANY_BUCKETS, MANY_DEPTHS, epi, param_arena=False)
+    run_emulated_many(N.SHUFFLE, 1, MANY_BUCKETS, MANY_DEPTHS, epi, param_arena=False)
