@@ -252,27 +252,28 @@ def run_reference(args) -> int:
 # ---------------------------------------------------------------------------
 # caramel arm
 # ---------------------------------------------------------------------------
-def time_kernels_gated(agg, torch, reps=3):
-    """Per-bucket kernel durations, measured with CUDA events around each
-    launch; a _sleep kernel first holds the stream so every launch is queued
-    before the first runs (no host gaps inside the brackets)."""
-    stream = torch.cuda.current_stream()
-    per = [0.0] * len(agg._live)
-    for _ in range(reps):
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in agg._live]
-        torch.cuda._sleep(int(50e6))  # ~25 ms at ~2 GHz
-        import ctypes
+def time_kernel_gated(agg, torch, reps=20):
+    """Average duration of the step's collective launch (caramel_allreduce_many),
+    CUDA events on its stream around each launch; a _sleep kernel first holds
+    the stream so every launch is queued before the first runs (no host gaps
+    inside the brackets)."""
+    import ctypes
 
-        from paper_2004_14020_b200 import _native as N
+    from paper_2004_14020_b200 import _native as N
+
+    stream = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    torch.cuda._sleep(int(20e6))
+    for a, b in evs:
         N.check(N.lib().caramel_epoch_advance(agg.ctx._ctx, ctypes.c_void_p(stream.cuda_stream)))
-        for lv, (a, b) in zip(agg._live, evs):
-            a.record(stream)
-            agg._launch(lv, stream.cuda_stream)
-            b.record(stream)
-        torch.cuda.synchronize()
-        for i, (a, b) in enumerate(evs):
-            per[i] += a.elapsed_time(b) / reps
-    return per  # ms
+        a.record(stream)
+        N.check(N.lib().caramel_allreduce_many(agg.ctx._ctx, agg._host_list, len(agg._live),
+                                               agg._dev_list.data_ptr(), agg._dev_prefix.data_ptr(), 0,
+                                               ctypes.c_void_p(stream.cuda_stream)))
+        b.record(stream)
+    torch.cuda.synchronize()
+    ts = sorted(a.elapsed_time(b) for a, b in evs)
+    return ts[len(ts) // 2]  # ms, median launch
 
 
 def nccl_baseline(torch, dist, params, grads_dev, world, steps, warmup, bucket_bytes=25 << 20):
@@ -393,10 +394,9 @@ def run_caramel(args) -> int:
 
     # ---- dominant kernel: per-launch durations (events around each launch)
     barrier()
-    per_ms = time_kernels_gated(agg, torch)
+    kern_ms = time_kernel_gated(agg, torch)
     barrier()
     agg.status()
-    kern_ms = sum(per_ms)
     if world == 1:
         alg_bytes = 12 * plan.total_numel  # read grad, read theta, write theta
         roof = {"bound": "hbm", "unit": "GB/s", "peak": None, "peak_source": None}
@@ -416,7 +416,7 @@ def run_caramel(args) -> int:
         kern_ms = t.item()
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
     roof.update({"achieved": round(achieved, 1), "frac": round(achieved / roof["peak"], 4),
-                 "traffic": None, "kernel": "k_collective (caramel.cu)", "launches_per_step": len(per_ms),
+                 "traffic": None, "kernel": "k_collective_many (caramel.cu)", "launches_per_step": 1,
                  "kernel_ms_per_step": round(kern_ms, 4),
                  "alg_bytes_per_step": alg_bytes,
                  "alg_bytes_rule": "12 B/elem (grad r, theta r/w)" if world == 1 else "2(p-1)/p x bucket bytes"})
@@ -482,7 +482,7 @@ def run_caramel(args) -> int:
                "sample": f"full {args.model} set ({nbytes / 1e6:.1f} MB), {len(plan.buckets)} buckets, "
                          f"{reps} passes of oracle_bucket_step (C, pthreads)"}
 
-    kernels_per_step = agg.kernels_per_step()
+    kernels_per_step = agg.kernels_per_step(fused=True)
     bus = plan.bus_bytes() / (ms * 1e-3) / 1e9 if world > 1 else None
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,

@@ -100,9 +100,10 @@ int caramel_chunk_bounds(uint64_t numel, int depth, int workers, uint64_t* out);
 
 /* Launch geometry and arena footprint of one bucket (identical on every
  * rank, so every rank launches the same grid): CTAs per rank, bytes of the
- * bucket region (ring/hd keep a second, output half so a fast neighbour never
- * overwrites a partial sum still to be pulled; shuffle all-gathers in place)
- * and bytes of its flag block. */
+ * bucket region and bytes of its flag block.  Bucket region: shuffle = the
+ * bucket itself (packed input, all-gathered in place); ring/hd = input and
+ * partials + a second, output half (a fast neighbour never overwrites a
+ * partial sum still to be pulled). */
 int caramel_bucket_layout(uint64_t numel, int depth, int pattern, int world,
                           int32_t* ctas, uint64_t* bucket_bytes,
                           uint64_t* flag_bytes);
@@ -165,8 +166,10 @@ int caramel_allreduce_update(caramel_ctx* ctx, const caramel_bucket* bucket,
 /* A list of buckets in launch order as ONE launch (the back-to-back pass:
  * every bucket's gradients already produced).  `host` is the descriptor list
  * (validated, sizes the grid); `dev_buckets` is a device copy of the same
- * caramel_bucket[count] and `dev_prefix` a device uint64_t[count+1] of
- * element prefix sums (prefix[0] = 0).  All buckets share one pattern.  The
+ * caramel_bucket[count] and `dev_prefix` a device uint64_t[2*(count+1)]:
+ * element prefix sums of the buckets (prefix[0] = 0) followed by prefix sums
+ * of their member-segment counts.  All buckets share pattern, epilogue and
+ * flags.  The
  * two-shot runs phase-major (every pack, then every reduce/all-gather, then
  * every completion wait); with world == 1 the concatenated element space is
  * tiled over the whole GPU.  Per bucket the result equals caramel_allreduce /

@@ -30,6 +30,8 @@
 
 #define THREADS 512
 #define MAXR CARAMEL_MAX_RANKS
+#define SYNC_BYTES (64 * 1024)  // per-arena library sync words (grid barriers)
+#define MAX_FUSED_BUCKETS 2048
 
 // ---------------------------------------------------------------------------
 // error plumbing (host)
@@ -69,6 +71,12 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+
+__device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
@@ -184,6 +192,324 @@ __device__ __forceinline__ void seg_st4(Cursor& c, uint64_t v, int which, float4
   seg_st1(c, v + 3, which, x.w);
 }
 
+// Segment pieces: call f(seg, a, b) for every member segment overlapping the
+// bucket range [lo, hi), with [a, b) the overlap in bucket coordinates.  One
+// binary search per range, then a forward walk; the hot loops below run on
+// fixed base pointers (no per-vector segment lookup).
+struct Seg {
+  uint64_t grad, param, offset, numel;
+};
+
+__device__ __forceinline__ Seg load_seg(const caramel_segment* s, int i) {
+  const unsigned long long* e = reinterpret_cast<const unsigned long long*>(s + i);
+  Seg r;
+  r.grad = __ldg(e + 0);
+  r.param = __ldg(e + 1);
+  r.offset = __ldg(e + 2);
+  r.numel = __ldg(e + 3);
+  return r;
+}
+
+template <class F>
+__device__ __forceinline__ void for_pieces(const caramel_segment* segs, int nseg, uint64_t lo, uint64_t hi, F f) {
+  if (lo >= hi) return;
+  int a = 0, b = nseg - 1;
+  while (a < b) {
+    int m = (a + b + 1) >> 1;
+    uint64_t off = __ldg(reinterpret_cast<const unsigned long long*>(segs + m) + 2);
+    if (off <= lo) a = m; else b = m - 1;
+  }
+  for (int i = a; i < nseg; ++i) {
+    const Seg sg = load_seg(segs, i);
+    if (sg.offset >= hi) break;
+    const uint64_t x = lo > sg.offset ? lo : sg.offset;
+    const uint64_t y = hi < sg.offset + sg.numel ? hi : sg.offset + sg.numel;
+    if (x < y) f(sg, x, y);
+  }
+}
+
+// Elements before all of the given pointers are 16-byte aligned, or n if they
+// can never be aligned together (then the whole range goes scalar).
+__device__ __forceinline__ uint64_t co_align_head(uint64_t n, uintptr_t p0, uintptr_t p1, uintptr_t p2) {
+  if (((p0 ^ p1) & 15) || ((p0 ^ p2) & 15) || (p0 & 3)) return n;
+  uint64_t h = ((16 - (p0 & 15)) & 15) >> 2;
+  return h < n ? h : n;
+}
+
+// out[i] = epilogue(g[i], theta[i]) for i < n (theta may alias out).  Four
+// float4 per thread per trip, all loads issued before the stores.
+__device__ __forceinline__ void stream_epi(const float* g, const float* th, float* out, uint64_t n, int epi,
+                                           float scale, float lr) {
+  const bool sgd = epi == CARAMEL_EPI_SGD;
+  const uint64_t head = co_align_head(n, (uintptr_t)g, sgd ? (uintptr_t)th : (uintptr_t)g, (uintptr_t)out);
+  for (uint64_t i = threadIdx.x; i < head; i += blockDim.x)
+    out[i] = epi1(epi, ld1(g + i), sgd ? ld1(th + i) : 0.f, scale, lr);
+  const uint64_t nv = (n - head) >> 2;  // float4 count
+  const float4* g4 = reinterpret_cast<const float4*>(g + head);
+  const float4* t4 = reinterpret_cast<const float4*>(th + head);
+  float4* o4 = reinterpret_cast<float4*>(out + head);
+  constexpr int U = 4;
+  const uint64_t T = blockDim.x;
+  uint64_t v = threadIdx.x;
+  for (; v + (U - 1) * T < nv; v += U * T) {
+    float4 x[U], t[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) x[u] = __ldcs(g4 + v + u * T);
+#pragma unroll
+    for (int u = 0; u < U; ++u) t[u] = sgd ? __ldcg(t4 + v + u * T) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < U; ++u) __stcg(o4 + v + u * T, epi4(epi, x[u], t[u], scale, lr));
+  }
+  for (; v < nv; v += T) {
+    float4 t = sgd ? __ldcg(t4 + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+    __stcg(o4 + v, epi4(epi, __ldcs(g4 + v), t, scale, lr));
+  }
+  for (uint64_t i = head + 4 * nv + threadIdx.x; i < n; i += blockDim.x)
+    out[i] = epi1(epi, ld1(g + i), sgd ? ld1(th + i) : 0.f, scale, lr);
+}
+
+// dst[i] = src[i] for i < n, vectorised when co-aligned.
+__device__ __forceinline__ void copy_n(const float* src, float* dst, uint64_t n) {
+  const uint64_t head = co_align_head(n, (uintptr_t)src, (uintptr_t)src, (uintptr_t)dst);
+  for (uint64_t i = threadIdx.x; i < head; i += blockDim.x) st1(dst + i, ld1(src + i));
+  const uint64_t nv = (n - head) >> 2;
+  const float4* s4 = reinterpret_cast<const float4*>(src + head);
+  float4* d4 = reinterpret_cast<float4*>(dst + head);
+  constexpr int U = 4;
+  const uint64_t T = blockDim.x;
+  uint64_t v = threadIdx.x;
+  for (; v + (U - 1) * T < nv; v += U * T) {
+    float4 x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) x[u] = __ldcg(s4 + v + u * T);
+#pragma unroll
+    for (int u = 0; u < U; ++u) __stcg(d4 + v + u * T, x[u]);
+  }
+  for (; v < nv; v += T) __stcg(d4 + v, __ldcg(s4 + v));
+  for (uint64_t i = head + 4 * nv + threadIdx.x; i < n; i += blockDim.x) st1(dst + i, ld1(src + i));
+}
+
+// ---------------------------------------------------------------------------
+// Warp-item engine for member pieces (pack, unpack, single-rank update).
+// A CTA's range overlaps a run of member segments ("pieces").  Thread i
+// describes piece i (pointers, length, epilogue), a block scan lays the
+// pieces out as items of 128 float4 (512 elements) and warps take items
+// round-robin: many small members are in flight at once instead of one
+// block-wide loop -- one memory round trip -- per member.
+// ---------------------------------------------------------------------------
+enum { OP_COPY = 0, OP_EPI = 1 };
+
+struct PieceDesc {
+  const float* g;  // source: gradient member or bucket
+  const float* t;  // theta (SGD epilogue only)
+  float* o;        // destination
+  uint32_t n;      // elements (0: no piece)
+  int epi;
+  float scale, lr;
+};
+
+struct PieceTab {
+  const float* g[THREADS];
+  const float* t[THREADS];
+  float* o[THREADS];
+  uint32_t n[THREADS];
+  uint32_t head[THREADS];       // scalar elements before the aligned body; ~0u = all-scalar piece
+  uint32_t first[THREADS + 1];  // item prefix
+  int epi[THREADS];
+  float scale[THREADS], lr[THREADS];
+  uint32_t scratch[32];
+};
+
+__shared__ PieceTab g_tab;  // one per CTA (static shared memory of the kernels that touch members)
+
+__device__ __forceinline__ int first_seg(const caramel_segment* segs, int nseg, uint64_t pos) {
+  int a = 0, b = nseg - 1;
+  while (a < b) {
+    int m = (a + b + 1) >> 1;
+    uint64_t off = __ldg(reinterpret_cast<const unsigned long long*>(segs + m) + 2);
+    if (off <= pos) a = m; else b = m - 1;
+  }
+  return a;
+}
+
+// block-wide exclusive scan of one uint32 per thread; returns the total
+__device__ __forceinline__ uint32_t block_scan(uint32_t x, uint32_t* out_excl, uint32_t* scratch) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t v = x;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane >= d) v += y;
+  }
+  if (lane == 31) scratch[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t s = lane < nw ? scratch[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, s, d);
+      if (lane >= d) s += y;
+    }
+    if (lane < nw) scratch[lane] = s;  // inclusive warp totals
+  }
+  __syncthreads();
+  *out_excl = (w ? scratch[w - 1] : 0) + v - x;
+  const uint32_t total = scratch[nw - 1];
+  __syncthreads();
+  return total;
+}
+
+__device__ __forceinline__ float apply1(int op, int epi, float g, float t, float scale, float lr) {
+  return op == OP_EPI ? epi1(epi, g, t, scale, lr) : g;
+}
+
+// Pieces [0, npieces): desc(i, PieceDesc&) fills piece i (n = 0 for none).
+template <int OP, class Desc>
+__device__ void run_pieces(int npieces, Desc desc, PieceTab& tab) {
+  for (int base = 0; base < npieces; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    PieceDesc d;
+    d.n = 0;
+    d.g = d.t = nullptr;
+    d.o = nullptr;
+    d.epi = CARAMEL_EPI_SUM;
+    d.scale = d.lr = 0.f;
+    if (i < npieces) desc(i, d);
+    const bool sgd = OP == OP_EPI && d.epi == CARAMEL_EPI_SGD;
+    uint32_t items = 0, head = 0;
+    if (d.n) {
+      const uint32_t h = (uint32_t)co_align_head(d.n, (uintptr_t)d.g, sgd ? (uintptr_t)d.t : (uintptr_t)d.g,
+                                                 (uintptr_t)d.o);
+      if (h == d.n) {  // never co-aligned: scalar items of 512 elements
+        head = ~0u;
+        items = (d.n + 511) / 512;
+      } else {
+        head = h;
+        items = (((d.n - h) >> 2) + 127) / 128;
+      }
+    }
+    uint32_t excl;
+    const uint32_t total = block_scan(items, &excl, tab.scratch);
+    tab.g[threadIdx.x] = d.g;
+    tab.t[threadIdx.x] = d.t;
+    tab.o[threadIdx.x] = d.o;
+    tab.n[threadIdx.x] = d.n;
+    tab.head[threadIdx.x] = head;
+    tab.first[threadIdx.x] = excl;
+    tab.epi[threadIdx.x] = d.epi;
+    tab.scale[threadIdx.x] = d.scale;
+    tab.lr[threadIdx.x] = d.lr;
+    if (threadIdx.x == blockDim.x - 1) tab.first[blockDim.x] = total;
+    // scalar head / tail of this thread's own vector piece (<= 3 + 3 elements)
+    if (d.n && head != ~0u) {
+      const uint32_t tail = head + 4 * ((d.n - head) >> 2);
+      for (uint32_t e = 0; e < head; ++e) d.o[e] = apply1(OP, d.epi, ld1(d.g + e), sgd ? ld1(d.t + e) : 0.f, d.scale, d.lr);
+      for (uint32_t e = tail; e < d.n; ++e) d.o[e] = apply1(OP, d.epi, ld1(d.g + e), sgd ? ld1(d.t + e) : 0.f, d.scale, d.lr);
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int pc = 0;
+    for (uint32_t it = w; it < total; it += nw) {
+      while (tab.first[pc + 1] <= it) ++pc;
+      const uint32_t k = it - tab.first[pc];
+      const float* pg = tab.g[pc];
+      const float* pt = tab.t[pc];
+      float* po = tab.o[pc];
+      const uint32_t pn = tab.n[pc], hd = tab.head[pc];
+      const int epi = tab.epi[pc];
+      const float scale = tab.scale[pc], lr = tab.lr[pc];
+      const bool psgd = OP == OP_EPI && epi == CARAMEL_EPI_SGD;
+      if (hd == ~0u) {  // scalar item: elements [512k, 512k + 512)
+        const uint32_t e0 = 512 * k;
+        float x[16], y[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const uint32_t e = e0 + lane + 32 * u;
+          x[u] = e < pn ? ld1(pg + e) : 0.f;
+          y[u] = (psgd && e < pn) ? ld1(pt + e) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const uint32_t e = e0 + lane + 32 * u;
+          if (e < pn) po[e] = apply1(OP, epi, x[u], y[u], scale, lr);
+        }
+      } else {  // vector item: float4 [128k, 128k + 128) of the aligned body
+        const uint32_t nv = (pn - hd) >> 2;
+        const float4* g4 = reinterpret_cast<const float4*>(pg + hd);
+        const float4* t4 = reinterpret_cast<const float4*>(pt + hd);
+        float4* o4 = reinterpret_cast<float4*>(po + hd);
+        const uint32_t v0 = 128 * k;
+        float4 x[4], y[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t v = v0 + lane + 32 * u;
+          x[u] = v < nv ? __ldcs(g4 + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t v = v0 + lane + 32 * u;
+          y[u] = (psgd && v < nv) ? __ldcg(t4 + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t v = v0 + lane + 32 * u;
+          if (v < nv) __stcg(o4 + v, OP == OP_EPI ? epi4(epi, x[u], y[u], scale, lr) : x[u]);
+        }
+      }
+    }
+    __syncthreads();  // tab is rewritten by the next batch
+  }
+}
+
+// The member segments of one bucket overlapping bucket range [lo, hi):
+// piece i is segment seg0 + i.  Returns seg0 and the count.
+__device__ __forceinline__ int seg_span(const caramel_segment* segs, int nseg, uint64_t lo, uint64_t hi, int& seg0) {
+  if (lo >= hi || nseg < 1) {
+    seg0 = 0;
+    return 0;
+  }
+  seg0 = first_seg(segs, nseg, lo);
+  const int last = first_seg(segs, nseg, hi - 1);
+  return last - seg0 + 1;
+}
+
+// piece [x0, x1) (bucket coordinates) of segment sg clipped to [lo, hi); false if empty
+__device__ __forceinline__ bool clip_seg(const Seg& sg, uint64_t lo, uint64_t hi, uint64_t& x0, uint64_t& x1) {
+  x0 = lo > sg.offset ? lo : sg.offset;
+  x1 = hi < sg.offset + sg.numel ? hi : sg.offset + sg.numel;
+  return x0 < x1;
+}
+
+// pack: bucket[lo, hi) <- member grads
+__device__ __forceinline__ void pack_range(const caramel_segment* segs, int nseg, float* bucket, uint64_t lo,
+                                           uint64_t hi, PieceTab& tab) {
+  int seg0;
+  const int np = seg_span(segs, nseg, lo, hi, seg0);
+  run_pieces<OP_COPY>(np, [&](int i, PieceDesc& d) {
+    const Seg sg = load_seg(segs, seg0 + i);
+    uint64_t x0, x1;
+    if (!clip_seg(sg, lo, hi, x0, x1)) return;
+    d.g = reinterpret_cast<const float*>(sg.grad) + (x0 - sg.offset);
+    d.o = bucket + x0;
+    d.n = (uint32_t)(x1 - x0);
+  }, tab);
+}
+
+// unpack: member grads (to_param = 0) or params <- bucket[lo, hi)
+__device__ __forceinline__ void unpack_range(const caramel_segment* segs, int nseg, const float* bucket,
+                                             uint64_t lo, uint64_t hi, bool to_param, PieceTab& tab) {
+  int seg0;
+  const int np = seg_span(segs, nseg, lo, hi, seg0);
+  run_pieces<OP_COPY>(np, [&](int i, PieceDesc& d) {
+    const Seg sg = load_seg(segs, seg0 + i);
+    uint64_t x0, x1;
+    if (!clip_seg(sg, lo, hi, x0, x1)) return;
+    d.g = bucket + x0;
+    d.o = reinterpret_cast<float*>(to_param ? sg.param : sg.grad) + (x0 - sg.offset);
+    d.n = (uint32_t)(x1 - x0);
+  }, tab);
+}
+
 // Cut [lo, hi) into `parts` tiles whose interior cuts fall on absolute
 // 4-element boundaries (so tile interiors vectorise); tile `j` is returned.
 __device__ __forceinline__ void tile_of(uint64_t lo, uint64_t hi, int parts, int j,
@@ -220,10 +546,7 @@ __global__ void __launch_bounds__(THREADS) k_pack(const caramel_segment* segs, i
                                                   uint64_t numel, float* bucket) {
   uint64_t lo, hi;
   tile_of(0, numel, gridDim.x, blockIdx.x, lo, hi);
-  Cursor c;
-  cur_init(c, segs, nseg);
-  walk(lo, hi, [&](uint64_t v) { st4(bucket + v, seg_ld4(c, v, 0)); },
-       [&](uint64_t i) { st1(bucket + i, seg_ld1(c, i, 0)); });
+  pack_range(segs, nseg, bucket, lo, hi, g_tab);
 }
 
 __global__ void __launch_bounds__(THREADS) k_unpack(const caramel_segment* segs, int nseg,
@@ -231,10 +554,7 @@ __global__ void __launch_bounds__(THREADS) k_unpack(const caramel_segment* segs,
                                                     int to_param) {
   uint64_t lo, hi;
   tile_of(0, numel, gridDim.x, blockIdx.x, lo, hi);
-  Cursor c;
-  cur_init(c, segs, nseg);
-  walk(lo, hi, [&](uint64_t v) { seg_st4(c, v, to_param, ld4(bucket + v)); },
-       [&](uint64_t i) { seg_st1(c, i, to_param, ld1(bucket + i)); });
+  unpack_range(segs, nseg, bucket, lo, hi, to_param != 0, g_tab);
 }
 
 // ---------------------------------------------------------------------------
@@ -249,6 +569,7 @@ struct Env {
   const uint32_t* epoch_dev;
   uint64_t timeout_ns;
   int* status;
+  uint64_t sync_off;      // library sync words, past the user part of every arena
 };
 
 struct KParams {          // one bucket
@@ -284,6 +605,15 @@ __host__ __device__ __forceinline__ uint64_t out_region_elems(uint64_t numel) {
   return (numel + 3) & ~3ull;
 }
 
+__host__ __device__ __forceinline__ void shard_bounds(uint64_t n, int k, int p, int c, int s, uint64_t& lo,
+                                                      uint64_t& hi) {
+  const uint64_t c0 = (n * (uint64_t)c) / k, m = (n * (uint64_t)(c + 1)) / k - c0;
+  lo = c0 + (m * (uint64_t)s) / p;
+  hi = c0 + (m * (uint64_t)(s + 1)) / p;
+}
+
+
+
 __device__ __forceinline__ uint32_t launch_epoch(const Env& E) {
   // the device counter is advanced by k_epoch_advance earlier on the same
   // stream, so every CTA of a launch reads the same value
@@ -299,20 +629,16 @@ struct Ctx {
     uint32_t* base = reinterpret_cast<uint32_t*>(E->arena[rank] + flag_off);
     return base + ((((uint64_t)c * G + j) * ns + slot) * world + src);
   }
-  // every thread calls; thread t < ntargets publishes to targets[t]
+  // Every thread calls; thread t < ntargets publishes to targets[t].
+  // bar.sync orders the CTA's data stores before the publishing thread's
+  // st.release.sys, and release is cumulative over them -- no SC fence.
   __device__ __forceinline__ void publish(int c, int slot, const int* targets, int ntargets) const {
     __syncthreads();
-    if ((int)threadIdx.x < ntargets) {
-      __threadfence_system();
-      st_release_sys(flag(targets[threadIdx.x], c, slot, me), epoch);
-    }
+    if ((int)threadIdx.x < ntargets) st_release_sys(flag(targets[threadIdx.x], c, slot, me), epoch);
   }
   __device__ __forceinline__ void publish_all(int c, int slot) const {
     __syncthreads();
-    if ((int)threadIdx.x < world) {
-      __threadfence_system();
-      st_release_sys(flag(threadIdx.x, c, slot, me), epoch);
-    }
+    if ((int)threadIdx.x < world) st_release_sys(flag(threadIdx.x, c, slot, me), epoch);
   }
   __device__ __forceinline__ void spin(const uint32_t* f, uint32_t want) const {
     if (ld_acquire_sys(f) >= want) return;
@@ -342,9 +668,10 @@ struct Ctx {
 // loads are in flight before the first add.
 template <int P>
 __device__ __forceinline__ void rs_ag_range(const Env& E, const caramel_bucket& B, bool arena, Cursor& tc,
-                                            uint64_t lo, uint64_t hi, int me) {
+                                            uint64_t lo, uint64_t hi, int me, const float* const* srcs) {
   if (lo >= hi) return;
-  auto src = [&](int q) { return reinterpret_cast<const float*>(E.arena[q] + B.bucket_off); };
+  // srcs[q] + x addresses source q's value of bucket position x (an inbox slot)
+  auto src = [&](int q) { return srcs[q]; };
   auto dst = [&](int q) {
     return arena ? reinterpret_cast<float*>(E.parena[q] + B.param_off)
                  : reinterpret_cast<float*>(E.arena[q] + B.bucket_off);
@@ -447,45 +774,66 @@ __device__ __forceinline__ void copy_range(const float* src, float* dst, uint64_
 }
 
 // Single-rank path (world == 1): no exchange; gather, epilogue and scatter
-// fused in one pass over bucket-local elements [lo, hi).
-__device__ void local_range(const Env& E, const caramel_bucket& B, int lr_idx, uint64_t lo, uint64_t hi) {
+// fused in one pass.  Piece [x0, x1) (bucket coordinates) of member sg:
+__device__ __forceinline__ void local_piece(const Env& E, const caramel_bucket& B, int lr_idx, const Seg& sg,
+                                            uint64_t x0, uint64_t x1, PieceDesc& d) {
   const int me = E.rank_base + lr_idx;
   float* bkt = reinterpret_cast<float*>(E.arena[me] + B.bucket_off);
   const bool arena = (B.flags & CARAMEL_F_PARAM_ARENA) && B.epilogue == CARAMEL_EPI_SGD;
   float* pflat = arena ? reinterpret_cast<float*>(E.parena[me] + B.param_off) : nullptr;
   const bool pack = B.flags & CARAMEL_F_PACK;
   const bool unpack = (B.flags & CARAMEL_F_UNPACK) && !arena;
-  const int out_which = (B.epilogue == CARAMEL_EPI_SGD) ? 1 : 0;
+  const bool sgd = B.epilogue == CARAMEL_EPI_SGD;
+  const uint64_t k = x0 - sg.offset;
+  d.g = pack ? reinterpret_cast<const float*>(sg.grad) + k : bkt + x0;
+  d.t = arena ? pflat + x0 : (sgd ? reinterpret_cast<const float*>(sg.param) + k : nullptr);
+  d.o = arena ? pflat + x0 : unpack ? reinterpret_cast<float*>(sgd ? sg.param : sg.grad) + k : bkt + x0;
+  d.n = (uint32_t)(x1 - x0);
+  d.epi = B.epilogue;
+  d.scale = B.scale;
+  d.lr = B.lr;
+}
+
+__device__ __forceinline__ bool local_needs_members(const caramel_bucket& B) {
+  const bool arena = (B.flags & CARAMEL_F_PARAM_ARENA) && B.epilogue == CARAMEL_EPI_SGD;
+  return (B.flags & CARAMEL_F_PACK) || ((B.flags & CARAMEL_F_UNPACK) && !arena) ||
+         (B.epilogue == CARAMEL_EPI_SGD && !arena);
+}
+
+// bucket-local [lo, hi) of one bucket
+__device__ void local_range(const Env& E, const caramel_bucket& B, int lr_idx, uint64_t lo, uint64_t hi,
+                            PieceTab& tab) {
+  const int me = E.rank_base + lr_idx;
+  if (!local_needs_members(B)) {  // bucket in, bucket / arena out
+    float* bkt = reinterpret_cast<float*>(E.arena[me] + B.bucket_off);
+    const bool arena = (B.flags & CARAMEL_F_PARAM_ARENA) && B.epilogue == CARAMEL_EPI_SGD;
+    float* out = arena ? reinterpret_cast<float*>(E.parena[me] + B.param_off) : bkt;
+    run_pieces<OP_EPI>(lo < hi ? 1 : 0, [&](int, PieceDesc& d) {
+      d.g = bkt + lo;
+      d.t = out + lo;
+      d.o = out + lo;
+      d.n = (uint32_t)(hi - lo);
+      d.epi = B.epilogue;
+      d.scale = B.scale;
+      d.lr = B.lr;
+    }, tab);
+    return;
+  }
   const caramel_segment* segs = reinterpret_cast<const caramel_segment*>(B.segs) + (uint64_t)lr_idx * B.nseg;
-  Cursor gc, pc;
-  cur_init(gc, segs, B.nseg);
-  cur_init(pc, segs, B.nseg);
-  const int epi = B.epilogue;
-  walk(lo, hi,
-       [&](uint64_t v) {
-         float4 g = pack ? seg_ld4(gc, v, 0) : ld4(bkt + v);
-         float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-         if (epi == CARAMEL_EPI_SGD) t = arena ? ld4(pflat + v) : seg_ld4(pc, v, 1);
-         float4 o = epi4(epi, g, t, B.scale, B.lr);
-         if (arena) st4(pflat + v, o);
-         else if (unpack) seg_st4(pc, v, out_which, o);
-         else st4(bkt + v, o);
-       },
-       [&](uint64_t i) {
-         float g = pack ? seg_ld1(gc, i, 0) : ld1(bkt + i);
-         float t = 0.f;
-         if (epi == CARAMEL_EPI_SGD) t = arena ? ld1(pflat + i) : seg_ld1(pc, i, 1);
-         float o = epi1(epi, g, t, B.scale, B.lr);
-         if (arena) st1(pflat + i, o);
-         else if (unpack) seg_st1(pc, i, out_which, o);
-         else st1(bkt + i, o);
-       });
+  int seg0;
+  const int np = seg_span(segs, B.nseg, lo, hi, seg0);
+  run_pieces<OP_EPI>(np, [&](int i, PieceDesc& d) {
+    const Seg sg = load_seg(segs, seg0 + i);
+    uint64_t x0, x1;
+    if (clip_seg(sg, lo, hi, x0, x1)) local_piece(E, B, lr_idx, sg, x0, x1, d);
+  }, tab);
 }
 
 // Per-CTA view of one bucket's collective (world > 1).
 struct BucketRun {
   const Env* E;
   const caramel_bucket* B;
+  PieceTab* tab;
   Ctx X;
   int lr_idx;
   bool arena;
@@ -511,9 +859,10 @@ struct BucketRun {
 };
 
 __device__ __forceinline__ void make_run(BucketRun& R, const Env& E, const caramel_bucket& B, int pattern,
-                                         int lr_idx, uint32_t epoch) {
+                                         int lr_idx, uint32_t epoch, int j) {
   R.E = &E;
   R.B = &B;
+  R.tab = &g_tab;
   R.lr_idx = lr_idx;
   R.arena = (B.flags & CARAMEL_F_PARAM_ARENA) && B.epilogue == CARAMEL_EPI_SGD;
   // shuffle all-gathers in place; ring/hd write results to a second region
@@ -525,14 +874,15 @@ __device__ __forceinline__ void make_run(BucketRun& R, const Env& E, const caram
   R.X.flag_off = B.flag_off;
   R.X.me = E.rank_base + lr_idx;
   R.X.world = E.world;
-  R.X.j = blockIdx.x;
+  R.X.j = j;
   R.X.G = B.ctas;
   R.X.ns = nslots(pattern, E.world);
   R.X.epoch = epoch;
 }
 
 // phase 1 (all patterns): ring/hd buffer-reuse guard, fused pack, ready flags
-template <int PAT>
+// (DEFER: the caller publishes every bucket's ready flags after one fence)
+template <int PAT, bool DEFER = false>
 __device__ void phase_pack(const BucketRun& R) {
   const int me = R.X.me, p = R.X.world;
   const uint32_t epoch = R.X.epoch;
@@ -549,19 +899,16 @@ __device__ void phase_pack(const BucketRun& R) {
   }
   const bool pack = R.B->flags & CARAMEL_F_PACK;
   float* mine = R.bucket(me);
-  Cursor gc;
-  cur_init(gc, R.segs, R.B->nseg);
   for (int c = 0; c < R.B->depth; ++c) {
     if (pack) {
       for (int s = 0; s < p; ++s) {
         uint64_t lo, hi;
         R.shard(c, s, lo, hi);
-        walk(lo, hi, [&](uint64_t v) { st4(mine + v, seg_ld4(gc, v, 0)); },
-             [&](uint64_t i) { st1(mine + i, seg_ld1(gc, i, 0)); });
+        pack_range(R.segs, R.B->nseg, mine, lo, hi, *R.tab);
       }
     }
     if (PAT == CARAMEL_SHUFFLE) {
-      R.X.publish_all(c, SLOT_READY);
+      if (!DEFER) R.X.publish_all(c, SLOT_READY);
     } else {
       int t = (PAT == CARAMEL_RING) ? (me + 1) % p : (me ^ (p >> 1));
       R.X.publish(c, SLOT_READY, &t, 1);
@@ -570,7 +917,7 @@ __device__ void phase_pack(const BucketRun& R) {
 }
 
 // phase 2, two-shot: reduce own shard in rank order, epilogue, all-gather by store
-template <int NP>
+template <int NP, bool DEFER = false>
 __device__ void phase_shuffle(const BucketRun& R) {
   Cursor tc;
   cur_init(tc, R.segs, R.B->nseg);
@@ -578,8 +925,11 @@ __device__ void phase_shuffle(const BucketRun& R) {
     R.X.wait_all(c, SLOT_READY, R.X.epoch);
     uint64_t lo, hi;
     R.shard(c, R.X.me, lo, hi);
-    rs_ag_range<NP>(*R.E, *R.B, R.arena, tc, lo, hi, R.X.me);
-    R.X.publish_all(c, SLOT_DONE);
+    const float* srcs[NP];  // pull: every rank's packed bucket, in place
+#pragma unroll
+    for (int q = 0; q < NP; ++q) srcs[q] = R.bucket(q);
+    rs_ag_range<NP>(*R.E, *R.B, R.arena, tc, lo, hi, R.X.me, srcs);
+    if (!DEFER) R.X.publish_all(c, SLOT_DONE);
   }
 }
 
@@ -679,16 +1029,13 @@ __device__ void phase_finish(const BucketRun& R) {
   if (PAT == CARAMEL_SHUFFLE)
     for (int c = 0; c < R.B->depth; ++c) R.X.wait_all(c, SLOT_DONE, R.X.epoch);
   if ((R.B->flags & CARAMEL_F_UNPACK) && !R.arena) {
-    const int which = (R.B->epilogue == CARAMEL_EPI_SGD) ? 1 : 0;
+    const bool to_param = (R.B->epilogue == CARAMEL_EPI_SGD);
     const float* res = R.out(me);
-    Cursor uc;
-    cur_init(uc, R.segs, R.B->nseg);
     for (int c = 0; c < R.B->depth; ++c) {
       for (int s = 0; s < p; ++s) {
         uint64_t lo, hi;
         R.shard(c, s, lo, hi);
-        walk(lo, hi, [&](uint64_t v) { seg_st4(uc, v, which, ld4(res + v)); },
-             [&](uint64_t i) { seg_st1(uc, i, which, ld1(res + i)); });
+        unpack_range(R.segs, R.B->nseg, res, lo, hi, to_param, *R.tab);
       }
     }
   }
@@ -705,9 +1052,10 @@ __device__ void phase_finish(const BucketRun& R) {
 }
 
 template <int PAT, int NP>
-__device__ __forceinline__ void run_bucket(const Env& E, const caramel_bucket& B, int lr_idx, uint32_t epoch) {
+__device__ __forceinline__ void run_bucket(const Env& E, const caramel_bucket& B, int lr_idx, uint32_t epoch,
+                                           int j) {
   BucketRun R;
-  make_run(R, E, B, PAT, lr_idx, epoch);
+  make_run(R, E, B, PAT, lr_idx, epoch, j);
   phase_pack<PAT>(R);
   if (PAT == CARAMEL_SHUFFLE) phase_shuffle<NP>(R);
   else if (PAT == CARAMEL_RING) phase_ring(R);
@@ -718,19 +1066,322 @@ __device__ __forceinline__ void run_bucket(const Env& E, const caramel_bucket& B
 __global__ void k_epoch_advance(uint32_t* e) { *e += 1; }
 
 template <int PAT, int NP>
-__global__ void __launch_bounds__(THREADS) k_collective(const __grid_constant__ KParams P) {
+__global__ void __launch_bounds__(THREADS, 1) k_collective(const __grid_constant__ KParams P) {
   const int lr_idx = blockIdx.y;
-  if (P.env.world == 1) {
-    uint64_t lo, hi;
-    tile_of(0, P.b.numel, gridDim.x, blockIdx.x, lo, hi);
-    local_range(P.env, P.b, lr_idx, lo, hi);
-    return;
-  }
   // local copies: the phases hold pointers to these, and generic pointers to
   // kernel parameters are not valid across real device-function calls
   const Env E = P.env;
   const caramel_bucket B = P.b;
-  run_bucket<PAT, NP>(E, B, lr_idx, launch_epoch(E));
+  run_bucket<PAT, NP>(E, B, lr_idx, launch_epoch(E), blockIdx.x);
+}
+
+// world == 1, many buckets: the concatenated element space is tiled evenly
+// over the grid; a tile's pieces may come from several buckets and are all
+// described in one batch (prefix[0..nb] element prefix sums, prefix[nb+1 ..
+// 2nb+1] member-segment prefix sums).
+__global__ void __launch_bounds__(THREADS, 2) k_local_many(const __grid_constant__ MParams P) {
+  const int lr_idx = blockIdx.y;
+  const Env E = P.env;
+  const uint64_t* pre = P.prefix;
+  const uint64_t* spre = P.prefix + P.nb + 1;
+  uint64_t lo, hi;
+  tile_of(0, pre[P.nb], gridDim.x, blockIdx.x, lo, hi);
+  if (lo >= hi) return;
+  auto bucket_of = [&](const uint64_t* arr, uint64_t x) {  // last i with arr[i] <= x
+    int a = 0, b = P.nb - 1;
+    while (a < b) {
+      int m = (a + b + 1) >> 1;
+      if (arr[m] <= x) a = m; else b = m - 1;
+    }
+    return a;
+  };
+  // first / last member segment (global numbering) overlapping [lo, hi)
+  const int ba = bucket_of(pre, lo), bb = bucket_of(pre, hi - 1);
+  const caramel_bucket Ba = P.bs[ba], Bb = P.bs[bb];
+  const bool members = local_needs_members(Ba);  // uniform over a list (same flags/epilogue)
+  if (!members) {
+    for (int i = ba; i <= bb; ++i) {
+      const caramel_bucket B = P.bs[i];
+      const uint64_t l = lo > pre[i] ? lo - pre[i] : 0;
+      const uint64_t h = (hi < pre[i] + B.numel ? hi : pre[i] + B.numel) - pre[i];
+      local_range(E, B, lr_idx, l, h, g_tab);
+    }
+    return;
+  }
+  const caramel_segment* sa = reinterpret_cast<const caramel_segment*>(Ba.segs) + (uint64_t)lr_idx * Ba.nseg;
+  const caramel_segment* sb = reinterpret_cast<const caramel_segment*>(Bb.segs) + (uint64_t)lr_idx * Bb.nseg;
+  const uint64_t g0 = spre[ba] + first_seg(sa, Ba.nseg, lo - pre[ba]);
+  const uint64_t g1 = spre[bb] + first_seg(sb, Bb.nseg, hi - 1 - pre[bb]);
+  run_pieces<OP_EPI>((int)(g1 - g0 + 1), [&](int i, PieceDesc& d) {
+    const uint64_t gs = g0 + i;
+    const int bi = bucket_of(spre, gs);
+    const caramel_bucket B = P.bs[bi];
+    const caramel_segment* segs = reinterpret_cast<const caramel_segment*>(B.segs) + (uint64_t)lr_idx * B.nseg;
+    const Seg sg = load_seg(segs, (int)(gs - spre[bi]));
+    const uint64_t l = lo > pre[bi] ? lo - pre[bi] : 0;
+    const uint64_t h = (hi < pre[bi] + B.numel ? hi : pre[bi] + B.numel) - pre[bi];
+    uint64_t x0, x1;
+    if (clip_seg(sg, l, h, x0, x1)) local_piece(E, B, lr_idx, sg, x0, x1, d);
+  }, g_tab);
+}
+
+__global__ void __launch_bounds__(THREADS, 2) k_local(const __grid_constant__ KParams P) {
+  uint64_t lo, hi;
+  tile_of(0, P.b.numel, gridDim.x, blockIdx.x, lo, hi);
+  const Env E = P.env;
+  const caramel_bucket B = P.b;
+  local_range(E, B, blockIdx.y, lo, hi, g_tab);
+}
+
+// ---------------------------------------------------------------------------
+// Fused two-shot over a whole bucket list (all gradients ready: the
+// back-to-back aggregation pass).  Three flat phases separated by cross-rank
+// grid barriers instead of per-bucket flags:
+//   0  pack every member into my bucket region (local HBM, warp-item engine
+//      over the concatenated element space, tiled evenly over the grid)
+//   1  for every (bucket, chunk): pull my shard from every rank's bucket,
+//      sum in ascending rank order, epilogue (fused SGD), push the result
+//      into every rank's output -- warp items of 256 elements tiled evenly
+//      over the grid, 2*NP float4 loads in flight per lane
+//   2  (results in buckets + CARAMEL_F_UNPACK) scatter to the members
+// Ownership of every element follows the per-bucket chunk/shard rule.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t* sync_words(const Env& E, int rank) {
+  return reinterpret_cast<uint32_t*>(E.arena[rank] + E.sync_off);
+}
+
+// Grid barrier k across every CTA of every rank (launch sequence value S).
+// Arrive: fence.acq_rel.sys, then a counter RMW; the last CTA of a rank
+// acquires the others' arrivals with its own fence and releases a flag to
+// every rank; everybody waits for all ranks' flags.
+__device__ void grid_barrier(const Env& E, int me, int k, uint32_t S) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t* mine = sync_words(E, me);
+    fence_acq_rel_sys();
+    const uint32_t old = atomicAdd(mine + 16 + k, 1u);
+    if (old == gridDim.x - 1) {
+      atomicExch(mine + 16 + k, 0u);
+      if (k == 0) atomicAdd(mine, 1u);  // launch sequence: everybody has read it
+      fence_acq_rel_sys();
+      for (int q = 0; q < E.world; ++q) st_relaxed_sys(sync_words(E, q) + 64 + k * MAXR + me, S + 1);
+    }
+    for (int q = 0; q < E.world; ++q) {
+      const uint32_t* f = mine + 64 + k * MAXR + q;
+      if (ld_acquire_sys(f) >= S + 1) continue;
+      const uint64_t t0 = globaltimer();
+      uint32_t spins = 0;
+      while (ld_acquire_sys(f) < S + 1) {
+        if ((++spins & 1023u) == 0 && globaltimer() - t0 > E.timeout_ns) {
+          atomicExch(E.status, CARAMEL_ETIMEOUT);
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// items of my shard range [lo, hi): one edge item (scalar head + tail) and
+// vector items of 64 float4 over the 4-aligned interior
+__device__ __forceinline__ uint32_t shard_items(uint64_t lo, uint64_t hi) {
+  if (lo >= hi) return 0;
+  const uint64_t a = (lo + 3) & ~3ull, e = hi & ~3ull;
+  return 1 + (e > a ? (uint32_t)(((e - a) / 4 + 63) / 64) : 0);
+}
+
+struct FusedShared {
+  uint32_t bpre[MAX_FUSED_BUCKETS + 1];
+};
+
+template <int NP>
+__global__ void __launch_bounds__(THREADS, 1) k_shuffle_fused(const __grid_constant__ MParams P) {
+  __shared__ FusedShared sh;
+  const Env E = P.env;
+  const int lr_idx = blockIdx.y;
+  const int me = E.rank_base + lr_idx;
+  const uint32_t S = *reinterpret_cast<volatile uint32_t*>(sync_words(E, me));
+  const caramel_bucket B0 = P.bs[0];
+  const bool arena = (B0.flags & CARAMEL_F_PARAM_ARENA) && B0.epilogue == CARAMEL_EPI_SGD;
+  const uint64_t* pre = P.prefix;
+  const uint64_t* spre = P.prefix + P.nb + 1;
+  auto bucket_of = [&](const uint64_t* arr, uint64_t x) {  // last i with arr[i] <= x
+    int a = 0, b = P.nb - 1;
+    while (a < b) {
+      int m = (a + b + 1) >> 1;
+      if (arr[m] <= x) a = m; else b = m - 1;
+    }
+    return a;
+  };
+  // ---- phase 0: pack ---------------------------------------------------------
+  if (B0.flags & CARAMEL_F_PACK) {
+    uint64_t lo, hi;
+    tile_of(0, pre[P.nb], gridDim.x, blockIdx.x, lo, hi);
+    if (lo < hi) {
+      const int ba = bucket_of(pre, lo), bb = bucket_of(pre, hi - 1);
+      const caramel_bucket Ba = P.bs[ba], Bb = P.bs[bb];
+      const caramel_segment* sa = reinterpret_cast<const caramel_segment*>(Ba.segs) + (uint64_t)lr_idx * Ba.nseg;
+      const caramel_segment* sb = reinterpret_cast<const caramel_segment*>(Bb.segs) + (uint64_t)lr_idx * Bb.nseg;
+      const uint64_t g0 = spre[ba] + first_seg(sa, Ba.nseg, lo - pre[ba]);
+      const uint64_t g1 = spre[bb] + first_seg(sb, Bb.nseg, hi - 1 - pre[bb]);
+      run_pieces<OP_COPY>((int)(g1 - g0 + 1), [&](int i, PieceDesc& d) {
+        const uint64_t gs = g0 + i;
+        const int bi = bucket_of(spre, gs);
+        const caramel_bucket B = P.bs[bi];
+        const caramel_segment* segs = reinterpret_cast<const caramel_segment*>(B.segs) + (uint64_t)lr_idx * B.nseg;
+        const Seg sg = load_seg(segs, (int)(gs - spre[bi]));
+        const uint64_t l = lo > pre[bi] ? lo - pre[bi] : 0;
+        const uint64_t h = (hi < pre[bi] + B.numel ? hi : pre[bi] + B.numel) - pre[bi];
+        uint64_t x0, x1;
+        if (!clip_seg(sg, l, h, x0, x1)) return;
+        d.g = reinterpret_cast<const float*>(sg.grad) + (x0 - sg.offset);
+        d.o = reinterpret_cast<float*>(E.arena[me] + B.bucket_off) + x0;
+        d.n = (uint32_t)(x1 - x0);
+      }, g_tab);
+    }
+  }
+  grid_barrier(E, me, 0, S);
+
+  // ---- phase 1: reduce my shards, epilogue, all-gather by store --------------
+  {
+    // per-bucket item prefix of my shards (block scan in batches)
+    uint32_t carry = 0;
+    for (int b0 = 0; b0 < P.nb; b0 += blockDim.x) {
+      const int i = b0 + threadIdx.x;
+      uint32_t cnt = 0;
+      if (i < P.nb) {
+        const caramel_bucket B = P.bs[i];
+        for (int c = 0; c < B.depth; ++c) {
+          uint64_t lo, hi;
+          shard_bounds(B.numel, B.depth, E.world, c, me, lo, hi);
+          cnt += shard_items(lo, hi);
+        }
+      }
+      uint32_t excl;
+      const uint32_t tot = block_scan(cnt, &excl, g_tab.scratch);
+      if (i < P.nb) sh.bpre[i] = carry + excl;
+      carry += tot;
+    }
+    if (threadIdx.x == 0) sh.bpre[P.nb] = carry;
+    __syncthreads();
+    const uint32_t T = carry;
+    const uint32_t it0 = (uint32_t)(((uint64_t)T * blockIdx.x) / gridDim.x);
+    const uint32_t it1 = (uint32_t)(((uint64_t)T * (blockIdx.x + 1)) / gridDim.x);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int bc = -1;
+    caramel_bucket B;
+    Cursor tc;
+    for (uint32_t it = it0 + w; it < it1; it += nw) {
+      if (bc < 0 || sh.bpre[bc + 1] <= it) {
+        int a = bc < 0 ? 0 : bc, b = P.nb - 1;
+        while (a < b) {
+          int m = (a + b + 1) >> 1;
+          if (sh.bpre[m] <= it) a = m; else b = m - 1;
+        }
+        bc = a;
+        B = P.bs[bc];
+        cur_init(tc, reinterpret_cast<const caramel_segment*>(B.segs) + (uint64_t)lr_idx * B.nseg, B.nseg);
+      }
+      uint32_t li = it - sh.bpre[bc];
+      uint64_t lo = 0, hi = 0;
+      for (int c = 0; c < B.depth; ++c) {
+        shard_bounds(B.numel, B.depth, E.world, c, me, lo, hi);
+        const uint32_t n = shard_items(lo, hi);
+        if (li < n) break;
+        li -= n;
+      }
+      const float* src[NP];
+      float* dst[NP];
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        src[q] = reinterpret_cast<const float*>(E.arena[q] + B.bucket_off);
+        dst[q] = arena ? reinterpret_cast<float*>(E.parena[q] + B.param_off)
+                       : reinterpret_cast<float*>(E.arena[q] + B.bucket_off);
+      }
+      const float* th = arena ? reinterpret_cast<const float*>(E.parena[me] + B.param_off) : nullptr;
+      const bool sgd = B.epilogue == CARAMEL_EPI_SGD;
+      const uint64_t a = (lo + 3) & ~3ull, e = hi & ~3ull;
+      if (li == 0) {  // edge item: scalar head [lo, a) and tail [e, hi) (whole range if no interior)
+        const bool interior = e > a;
+        const uint64_t n_head = interior ? a - lo : hi - lo;
+        const uint64_t n_tail = interior ? hi - e : 0;
+        if ((uint64_t)lane < n_head + n_tail) {
+          const uint64_t x = (uint64_t)lane < n_head ? lo + lane : e + (lane - n_head);
+          float acc = ld1(src[0] + x);
+#pragma unroll
+          for (int q = 1; q < NP; ++q) acc = __fadd_rn(acc, ld1(src[q] + x));
+          const float t = sgd ? (arena ? ld1(th + x) : seg_ld1(tc, x, 1)) : 0.f;
+          const float o = epi1(B.epilogue, acc, t, B.scale, B.lr);
+#pragma unroll
+          for (int q = 0; q < NP; ++q) st1(dst[q] + x, o);
+        }
+        continue;
+      }
+      // vector item li-1: float4 [64 (li-1), 64 li) of the interior; lane does two
+      const uint64_t nv = (e - a) / 4;
+      const uint64_t v0 = 64ull * (li - 1) + lane, v1 = v0 + 32;
+      const bool ok0 = v0 < nv, ok1 = v1 < nv;
+      const uint64_t x0 = a + 4 * v0, x1 = a + 4 * v1;
+      float4 p0[NP], p1[NP];
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        p0[q] = ok0 ? ld4(src[q] + x0) : make_float4(0.f, 0.f, 0.f, 0.f);
+        p1[q] = ok1 ? ld4(src[q] + x1) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      float4 t0 = make_float4(0.f, 0.f, 0.f, 0.f), t1 = t0;
+      if (sgd) {
+        if (arena) {
+          if (ok0) t0 = ld4(th + x0);
+          if (ok1) t1 = ld4(th + x1);
+        } else {
+          if (ok0) t0 = seg_ld4(tc, x0, 1);
+          if (ok1) t1 = seg_ld4(tc, x1, 1);
+        }
+      }
+      float4 s0 = p0[0], s1 = p1[0];
+#pragma unroll
+      for (int q = 1; q < NP; ++q) {
+        s0 = add4(s0, p0[q]);
+        s1 = add4(s1, p1[q]);
+      }
+      const float4 o0 = epi4(B.epilogue, s0, t0, B.scale, B.lr), o1 = epi4(B.epilogue, s1, t1, B.scale, B.lr);
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        if (ok0) st4(dst[q] + x0, o0);
+        if (ok1) st4(dst[q] + x1, o1);
+      }
+    }
+  }
+  grid_barrier(E, me, 1, S);
+
+  // ---- phase 2: unpack (results live in the buckets) --------------------------
+  if ((B0.flags & CARAMEL_F_UNPACK) && !arena) {
+    const bool to_param = B0.epilogue == CARAMEL_EPI_SGD;
+    uint64_t lo, hi;
+    tile_of(0, pre[P.nb], gridDim.x, blockIdx.x, lo, hi);
+    if (lo < hi) {
+      const int ba = bucket_of(pre, lo), bb = bucket_of(pre, hi - 1);
+      const caramel_bucket Ba = P.bs[ba], Bb = P.bs[bb];
+      const caramel_segment* sa = reinterpret_cast<const caramel_segment*>(Ba.segs) + (uint64_t)lr_idx * Ba.nseg;
+      const caramel_segment* sb = reinterpret_cast<const caramel_segment*>(Bb.segs) + (uint64_t)lr_idx * Bb.nseg;
+      const uint64_t g0 = spre[ba] + first_seg(sa, Ba.nseg, lo - pre[ba]);
+      const uint64_t g1 = spre[bb] + first_seg(sb, Bb.nseg, hi - 1 - pre[bb]);
+      run_pieces<OP_COPY>((int)(g1 - g0 + 1), [&](int i, PieceDesc& d) {
+        const uint64_t gs = g0 + i;
+        const int bi = bucket_of(spre, gs);
+        const caramel_bucket B = P.bs[bi];
+        const caramel_segment* segs = reinterpret_cast<const caramel_segment*>(B.segs) + (uint64_t)lr_idx * B.nseg;
+        const Seg sg = load_seg(segs, (int)(gs - spre[bi]));
+        const uint64_t l = lo > pre[bi] ? lo - pre[bi] : 0;
+        const uint64_t h = (hi < pre[bi] + B.numel ? hi : pre[bi] + B.numel) - pre[bi];
+        uint64_t x0, x1;
+        if (!clip_seg(sg, l, h, x0, x1)) return;
+        d.g = reinterpret_cast<const float*>(E.arena[me] + B.bucket_off) + x0;
+        d.o = reinterpret_cast<float*>(to_param ? sg.param : sg.grad) + (x0 - sg.offset);
+        d.n = (uint32_t)(x1 - x0);
+      }, g_tab);
+    }
+  }
 }
 
 // Many buckets in one launch (launch order).  world == 1: the concatenated
@@ -740,57 +1391,27 @@ __global__ void __launch_bounds__(THREADS) k_collective(const __grid_constant__ 
 // flags while another bucket's work is available.  Ring/hd: bucket by bucket.
 // CTA j takes part in bucket b iff j < b.ctas (same rule on every rank).
 template <int PAT, int NP>
-__global__ void __launch_bounds__(THREADS) k_collective_many(const __grid_constant__ MParams P) {
+__global__ void __launch_bounds__(THREADS, 1) k_collective_many(const __grid_constant__ MParams P) {
   const int lr_idx = blockIdx.y;
   const Env E = P.env;  // local copy: phases keep pointers to it
-  if (E.world == 1) {
-    uint64_t lo, hi;
-    tile_of(0, P.prefix[P.nb], gridDim.x, blockIdx.x, lo, hi);
-    if (lo >= hi) return;
-    // first bucket overlapping [lo, hi)
-    int a = 0, b = P.nb - 1;
-    while (a < b) {
-      int m = (a + b + 1) >> 1;
-      if (P.prefix[m] <= lo) a = m; else b = m - 1;
-    }
-    for (int i = a; i < P.nb && P.prefix[i] < hi; ++i) {
-      const caramel_bucket B = P.bs[i];
-      const uint64_t b0 = P.prefix[i];
-      const uint64_t l = lo > b0 ? lo - b0 : 0;
-      const uint64_t h = (hi < b0 + B.numel ? hi : b0 + B.numel) - b0;
-      // bucket-local 4-alignment keeps the vector body aligned (buckets start 16B aligned)
-      local_range(E, B, lr_idx, l, h);
-    }
-    return;
-  }
   const uint32_t epoch = launch_epoch(E);
-  if (PAT == CARAMEL_SHUFFLE) {
+  const int G = gridDim.x;
+  // bucket i occupies CTAs base_i .. base_i + ctas_i - 1 (mod G), base_i being
+  // the running sum of the previous buckets' CTA counts: small buckets spread
+  // over the grid and proceed in parallel.  Same rule on every rank.
+  auto my_tile = [&](int base, int ctas) {
+    int jj = ((int)blockIdx.x - base) % G;
+    if (jj < 0) jj += G;
+    return jj < ctas ? jj : -1;
+  };
+  {  // ring / hd: bucket by bucket (the two-shot list runs in k_shuffle_fused)
+    int base = 0;
     for (int i = 0; i < P.nb; ++i) {
       const caramel_bucket B = P.bs[i];
-      if ((int)blockIdx.x >= B.ctas || B.numel == 0) continue;
-      BucketRun R;
-      make_run(R, E, B, PAT, lr_idx, epoch);
-      phase_pack<PAT>(R);
-    }
-    for (int i = 0; i < P.nb; ++i) {
-      const caramel_bucket B = P.bs[i];
-      if ((int)blockIdx.x >= B.ctas || B.numel == 0) continue;
-      BucketRun R;
-      make_run(R, E, B, PAT, lr_idx, epoch);
-      phase_shuffle<NP>(R);
-    }
-    for (int i = 0; i < P.nb; ++i) {
-      const caramel_bucket B = P.bs[i];
-      if ((int)blockIdx.x >= B.ctas || B.numel == 0) continue;
-      BucketRun R;
-      make_run(R, E, B, PAT, lr_idx, epoch);
-      phase_finish<PAT>(R);
-    }
-  } else {
-    for (int i = 0; i < P.nb; ++i) {
-      const caramel_bucket B = P.bs[i];
-      if ((int)blockIdx.x >= B.ctas || B.numel == 0) continue;
-      run_bucket<PAT, NP>(E, B, lr_idx, epoch);
+      const int j = my_tile(base, B.ctas);
+      base = (base + B.ctas) % G;
+      if (j < 0 || B.numel == 0) continue;
+      run_bucket<PAT, NP>(E, B, lr_idx, epoch, j);
     }
   }
 }
@@ -872,7 +1493,7 @@ int caramel_bucket_layout(uint64_t numel, int depth, int pattern, int world, int
   if (g < 1) g = 1;
   if (ctas) *ctas = (int32_t)g;
   if (bucket_bytes) {
-    uint64_t e = out_region_elems(numel);
+    const uint64_t e = out_region_elems(numel);
     *bucket_bytes = 4 * ((world > 1 && pattern != CARAMEL_SHUFFLE) ? 2 * e : e);
   }
   if (flag_bytes) {
@@ -905,8 +1526,8 @@ int caramel_init(int rank, int world, int nlocal, uint64_t arena_bytes, uint64_t
   if ((e = cudaGetDevice(&c->device)) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "cudaGetDevice: %s", cudaGetErrorString(e)); goto fail; }
   if ((e = cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device)) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "attr: %s", cudaGetErrorString(e)); goto fail; }
   for (int i = 0; i < nlocal; ++i) {
-    if ((e = cudaMalloc(&c->arena_local[i], c->arena_bytes)) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "cudaMalloc arena (%llu B): %s", (unsigned long long)c->arena_bytes, cudaGetErrorString(e)); goto fail; }
-    if ((e = cudaMemset(c->arena_local[i], 0, c->arena_bytes)) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "memset: %s", cudaGetErrorString(e)); goto fail; }
+    if ((e = cudaMalloc(&c->arena_local[i], c->arena_bytes + SYNC_BYTES)) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "cudaMalloc arena (%llu B): %s", (unsigned long long)c->arena_bytes, cudaGetErrorString(e)); goto fail; }
+    if ((e = cudaMemset(c->arena_local[i], 0, c->arena_bytes + SYNC_BYTES)) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "memset: %s", cudaGetErrorString(e)); goto fail; }
     if (c->param_bytes) {
       if ((e = cudaMalloc(&c->param_local[i], c->param_bytes)) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "cudaMalloc param arena: %s", cudaGetErrorString(e)); goto fail; }
       if ((e = cudaMemset(c->param_local[i], 0, c->param_bytes)) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "memset: %s", cudaGetErrorString(e)); goto fail; }
@@ -1051,7 +1672,6 @@ template <int PAT>
 static kfn_t pick_np(int p) {
   if (PAT != CARAMEL_SHUFFLE) return k_collective<PAT, 2>;  // NP only shapes the two-shot reduce
   switch (p) {
-    case 1: return k_collective<PAT, 1>;
     case 2: return k_collective<PAT, 2>;
     case 3: return k_collective<PAT, 3>;
     case 4: return k_collective<PAT, 4>;
@@ -1062,19 +1682,21 @@ static kfn_t pick_np(int p) {
   }
 }
 
-template <int PAT>
-static mfn_t pick_np_many(int p) {
-  if (PAT != CARAMEL_SHUFFLE) return k_collective_many<PAT, 2>;
+static mfn_t pick_fused(int p) {
   switch (p) {
-    case 1: return k_collective_many<PAT, 1>;
-    case 2: return k_collective_many<PAT, 2>;
-    case 3: return k_collective_many<PAT, 3>;
-    case 4: return k_collective_many<PAT, 4>;
-    case 5: return k_collective_many<PAT, 5>;
-    case 6: return k_collective_many<PAT, 6>;
-    case 7: return k_collective_many<PAT, 7>;
-    default: return k_collective_many<PAT, 8>;
+    case 2: return k_shuffle_fused<2>;
+    case 3: return k_shuffle_fused<3>;
+    case 4: return k_shuffle_fused<4>;
+    case 5: return k_shuffle_fused<5>;
+    case 6: return k_shuffle_fused<6>;
+    case 7: return k_shuffle_fused<7>;
+    default: return k_shuffle_fused<8>;
   }
+}
+
+template <int PAT>
+static mfn_t pick_np_many(int) {
+  return k_collective_many<PAT, 2>;  // ring / hd only; NP does not shape them
 }
 
 extern "C" {
@@ -1122,6 +1744,7 @@ static void fill_env(const caramel_ctx* c, Env& E, uint32_t epoch) {
   E.epoch_dev = c->epoch_dev;
   E.timeout_ns = c->timeout_ns;
   E.status = c->status;
+  E.sync_off = c->arena_bytes;
 }
 
 // rank emulation: all ranks' CTAs spin on each other, so they must be
@@ -1146,7 +1769,8 @@ static int launch(caramel_ctx* c, const caramel_bucket* b, uint32_t epoch, void*
   fill_env(c, P.env, epoch);
   P.b = *b;
   kfn_t fn;
-  if (b->pattern == CARAMEL_SHUFFLE) fn = pick_np<CARAMEL_SHUFFLE>(c->world);
+  if (c->world == 1) fn = k_local;
+  else if (b->pattern == CARAMEL_SHUFFLE) fn = pick_np<CARAMEL_SHUFFLE>(c->world);
   else if (b->pattern == CARAMEL_RING) fn = pick_np<CARAMEL_RING>(c->world);
   else fn = pick_np<CARAMEL_HD>(c->world);
   dim3 grid(b->ctas, c->nlocal);
@@ -1187,7 +1811,8 @@ int caramel_allreduce_many(caramel_ctx* c, const caramel_bucket* host, int32_t c
   int gmax = 1;
   uint64_t total = 0;
   for (int i = 0; i < count; ++i) {
-    if (host[i].pattern != pattern) return set_err(CARAMEL_EINVAL, "allreduce_many: mixed patterns");
+    if (host[i].pattern != pattern || host[i].epilogue != host[0].epilogue || host[i].flags != host[0].flags)
+      return set_err(CARAMEL_EINVAL, "allreduce_many: buckets must share pattern, epilogue and flags");
     int rc = validate_bucket(c, &host[i]);
     if (rc) return rc;
     if (host[i].ctas > gmax) gmax = host[i].ctas;
@@ -1205,7 +1830,13 @@ int caramel_allreduce_many(caramel_ctx* c, const caramel_bucket* host, int32_t c
   P.prefix = reinterpret_cast<const uint64_t*>(dev_prefix);
   P.nb = count;
   mfn_t fn;
-  if (pattern == CARAMEL_SHUFFLE) fn = pick_np_many<CARAMEL_SHUFFLE>(c->world);
+  if (c->world == 1) fn = k_local_many;
+  else if (pattern == CARAMEL_SHUFFLE) {
+    if (count > MAX_FUSED_BUCKETS)
+      return set_err(CARAMEL_EINVAL, "allreduce_many: at most %d buckets per fused launch", MAX_FUSED_BUCKETS);
+    fn = pick_fused(c->world);
+    gmax = c->nlocal > 1 ? gmax : c->sms;  // flat phases: the whole GPU (one CTA per SM)
+  }
   else if (pattern == CARAMEL_RING) fn = pick_np_many<CARAMEL_RING>(c->world);
   else fn = pick_np_many<CARAMEL_HD>(c->world);
   dim3 grid(gmax, c->nlocal);

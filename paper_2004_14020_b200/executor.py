@@ -215,10 +215,11 @@ class Aggregator:
         self._host_list = (N.Bucket * n)(*[lv.desc for lv in self._live])
         raw = bytes(self._host_list)
         self._dev_list = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(self.device)
-        prefix = [0]
+        prefix, segpre = [0], [0]
         for lv in self._live:
             prefix.append(prefix[-1] + lv.spec.numel)
-        self._dev_prefix = torch.tensor(prefix, dtype=torch.int64, device=self.device)
+            segpre.append(segpre[-1] + len(lv.members))
+        self._dev_prefix = torch.tensor(prefix + segpre, dtype=torch.int64, device=self.device)
 
     def refresh_tables(self) -> None:
         """Rebuild segment tables (after gradients were reallocated)."""

@@ -252,7 +252,8 @@ def run_emulated_many(pattern, p, bucket_shapes, depths, epi, *, param_arena=Fal
                                           lr=lr, scale=1.0 / p))
         host = (N.Bucket * len(descs))(*descs)
         dev_list = torch.frombuffer(bytearray(bytes(host)), dtype=torch.uint8).to(dev)
-        prefix = torch.tensor(np.concatenate([[0], np.cumsum([sp[2] for sp in specs])]), dtype=torch.int64,
+        prefix = torch.tensor(np.concatenate([[0], np.cumsum([sp[2] for sp in specs]),
+                                              [0], np.cumsum([len(sp[0]) for sp in specs])]), dtype=torch.int64,
                               device=dev)
         N.check(N.lib().caramel_epoch_advance(ctx._ctx, ctypes.c_void_p(stream)))
         N.check(N.lib().caramel_allreduce_many(ctx._ctx, host, len(descs), dev_list.data_ptr(), prefix.data_ptr(),

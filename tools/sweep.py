@@ -18,7 +18,10 @@ def main():
     depths = [int(x) for x in os.environ.get("SWEEP_DEPTHS", "1").split(",")]
     iters = int(os.environ.get("SWEEP_ITERS", 20))
     maxel = max_bytes // 4
-    ctx = comm.Context(rank, world, arena_bytes=2 * max_bytes + (64 << 20))
+    region = max(N.bucket_layout(maxel, d, pt, world)[1] for pt in (0, 1, 2) if not (pt == 1 and world & (world - 1))
+                 for d in (1, 8))
+    region = (region + (1 << 20)) // (1 << 20) * (1 << 20)
+    ctx = comm.Context(rank, world, arena_bytes=region + (64 << 20))
     ctx.bootstrap()
     base, _ = ctx.arena_ptrs(0)
     buf = comm._view_fp32(base, maxel)
@@ -35,7 +38,7 @@ def main():
                 ctas, bbytes, fbytes = N.bucket_layout(n, depth, pat, world)
                 if os.environ.get("SWEEP_CTAS"):
                     ctas = min(ctas, int(os.environ["SWEEP_CTAS"]))
-                foff = 2 * max_bytes + (1 << 20)
+                foff = region
                 b = comm.make_bucket(n, 0, foff, depth=depth, pattern=pat, epilogue=N.EPI_SUM, flags=0, ctas=ctas)
                 key = (pat, depth, ctas)
                 # flags region shared across sizes: keep epochs monotone per key
@@ -43,29 +46,33 @@ def main():
                 idx = list(epoch).index(key) if key in epoch else len(epoch)
                 epoch.setdefault(key, 0)
                 b.flag_off = foff + idx * (8 << 20) // 8
-                ts = []
-                for it in range(iters + 5):
+                for it in range(5):
                     epoch[key] += 1
-                    dist.barrier(); torch.cuda.synchronize()
-                    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    s.record(stream); ctx.allreduce(b, epoch[key], stream.cuda_stream); e.record(stream)
-                    e.synchronize()
-                    if it >= 5: ts.append(s.elapsed_time(e))
+                    ctx.allreduce(b, epoch[key], stream.cuda_stream)
+                torch.cuda.synchronize(); dist.barrier()
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record(stream)
+                for it in range(iters):
+                    epoch[key] += 1
+                    ctx.allreduce(b, epoch[key], stream.cuda_stream)
+                e.record(stream); e.synchronize()
                 ctx.status()
-                t = torch.tensor(sorted(ts)[len(ts) // 2], device=dev)
+                t = torch.tensor(s.elapsed_time(e) / iters, device=dev)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 us = t.item() * 1e3
                 bus = 2 * (world - 1) / world * size / (us * 1e-6) / 1e9
                 rows.append(dict(impl="caramel", pattern=pat, depth=depth, ctas=ctas, bytes=size, us=round(us, 2), busbw=round(bus, 1)))
         # NCCL
         x = buf[:n]
-        ts = []
-        for it in range(iters + 5):
-            dist.barrier(); torch.cuda.synchronize()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record(stream); dist.all_reduce(x); e.record(stream); e.synchronize()
-            if it >= 5: ts.append(s.elapsed_time(e))
-        t = torch.tensor(sorted(ts)[len(ts) // 2], device=dev)
+        for it in range(5):
+            dist.all_reduce(x)
+        torch.cuda.synchronize(); dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        for it in range(iters):
+            dist.all_reduce(x)
+        e.record(stream); e.synchronize()
+        t = torch.tensor(s.elapsed_time(e) / iters, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         us = t.item() * 1e3
         rows.append(dict(impl="nccl", bytes=size, us=round(us, 2), busbw=round(2 * (world - 1) / world * size / (us * 1e-6) / 1e9, 1)))
