@@ -416,7 +416,10 @@ def run_caramel(args) -> int:
         kern_ms = t.item()
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
     roof.update({"achieved": round(achieved, 1), "frac": round(achieved / roof["peak"], 4),
-                 "traffic": None, "kernel": "k_collective_many (caramel.cu)", "launches_per_step": 1,
+                 "traffic": None,
+                 "kernel": ("k_local_many" if world == 1 else
+                            "k_shuffle_fused" if args.pattern == "shuffle" else "k_collective_many") + " (caramel.cu)",
+                 "launches_per_step": 1,
                  "kernel_ms_per_step": round(kern_ms, 4),
                  "alg_bytes_per_step": alg_bytes,
                  "alg_bytes_rule": "12 B/elem (grad r, theta r/w)" if world == 1 else "2(p-1)/p x bucket bytes"})

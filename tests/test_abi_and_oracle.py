@@ -1,0 +1,176 @@
+"""CPU-side checks: the C ABI library loads and exports exactly what
+include/caramel.h declares (no GPU call), host arithmetic of the ABI, the
+oracle against the reference's stage arithmetic (golden vectors from the
+reference, tests/golden/plans.json.gz), and plan lowering."""
+
+from __future__ import annotations
+
+import ctypes
+import gzip
+import json
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+ROOT = Path(__file__).resolve().parents[1]
+HEADER = ROOT / "include" / "caramel.h"
+
+
+def _lib():
+    from paper_2004_14020_b200 import _native as N
+
+    if not N.LIB_PATH.exists():
+        import __graft_entry__
+
+        __graft_entry__.build()
+    return N
+
+
+def declared_functions() -> list[str]:
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(caramel_[a-z_]+)\s*\(", text)))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for required in ("caramel_init", "caramel_pack", "caramel_allreduce", "caramel_allreduce_update",
+                     "caramel_finalize", "caramel_last_error", "caramel_allreduce_many", "caramel_unpack"):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol():
+    N = _lib()
+    handle = ctypes.CDLL(str(N.LIB_PATH))
+    missing = [n for n in declared_functions() if not hasattr(handle, n)]
+    assert not missing, f"declared in caramel.h but not exported: {missing}"
+    assert set(N.SIGNATURES) == set(declared_functions()), "ctypes binding out of sync with caramel.h"
+    assert N.lib().caramel_abi_version() == 1
+
+
+def test_chunk_bounds_match_oracle_rule():
+    N = _lib()
+    for n in (0, 1, 7, 4_000_012, 25_557_032):
+        for k in (1, 3, 8):
+            for p in (1, 2, 3, 8):
+                assert N.chunk_bounds(n, k, p) == O.chunk_bounds(n, k, p)
+
+
+def test_chunk_rule_agrees_with_reference_float_bytes():
+    """Integer bounds equal the reference's float chunk bytes (c*d/k,
+    collective.py:124) when 4*k*p divides d, and differ by < 1 element otherwise."""
+    for n in (4096, 1 << 20, 1_000_003, 4_000_012 // 4):
+        for k in (1, 2, 8):
+            for p in (2, 4, 8):
+                d = 4 * n
+                for c, row in enumerate(O.chunk_bounds(n, k, p)):
+                    exact = c * d / k / 4
+                    assert abs(row[0] - exact) < 1.0
+                    if d % (4 * k * p) == 0:
+                        assert row[0] == exact
+                        for s in range(p):
+                            assert row[s] == exact + s * (d / k / p) / 4
+
+
+def test_bucket_layout_and_errors():
+    N = _lib()
+    ctas, bb, fb = N.bucket_layout(1 << 20, 2, N.SHUFFLE, 8)
+    assert 1 <= ctas <= 64 and bb == 4 << 20 and fb > 0
+    _, bb_ring, _ = N.bucket_layout(1 << 20, 2, N.RING, 8)
+    assert bb_ring == 8 << 20  # input + output halves
+    with pytest.raises(N.CaramelError, match="power-of-two"):
+        N.bucket_layout(1024, 1, N.HD, 6)
+    with pytest.raises(N.CaramelError, match="depth"):
+        N.bucket_layout(1024, 9, N.SHUFFLE, 2)
+    assert N.flag_bytes_for(3, 5, N.SHUFFLE, 4) == (3 * 5 * 2 * 4 * 4 + 255) & ~255
+
+
+def _golden():
+    with gzip.open(ROOT / "tests" / "golden" / "plans.json.gz", "rt") as fh:
+        return json.load(fh)
+
+
+def test_oracle_data_movement_matches_reference_stage_plan():
+    """The oracle executes each pattern on p simulated workers and counts the
+    bytes worker 0 pulls and reduces per stage; they must equal the reference's
+    stage_plan (golden vectors) for divisible payloads."""
+    pat = {"ring": O.RING, "hd": O.HD, "shuffle": O.SHUFFLE}
+    checked = 0
+    for u in _golden()["units"]["stage_plan"]:
+        p, d = u["workers"], u["bytes"]
+        if d % (4 * p) or d > 4 * 2**20 or p > 8:
+            continue
+        n = d // 4
+        bufs = [np.ones(n, np.float32) for _ in range(p)]
+        _, xfer, red = O.c_allreduce(pat[u["pattern"]], bufs, 1)
+        assert [[4 * x, 4 * r] for x, r in zip(xfer, red)] == u["stages"], u
+        checked += 1
+    assert checked >= 20
+
+
+def test_oracle_numpy_and_c_agree_bit_exact():
+    rng = np.random.default_rng(0)
+    for pattern in (O.RING, O.HD, O.SHUFFLE):
+        for p in (2, 4, 8):
+            for k in (1, 3):
+                bufs = [rng.standard_normal(1003).astype(np.float32) for _ in range(p)]
+                th = rng.standard_normal(1003).astype(np.float32)
+                want = O.np_allreduce(pattern, bufs, k, O.EPI_SGD, 1.0 / p, 0.1, th)
+                outs, _, _ = O.c_allreduce(pattern, bufs, k, O.EPI_SGD, 1.0 / p, 0.1, th)
+                for o in outs:
+                    assert np.array_equal(o.view(np.uint32), want.view(np.uint32))
+
+
+def test_oracle_fixed_order_is_rank_order_for_shuffle():
+    x = [np.float32(1e8), np.float32(1.0), np.float32(-1e8), np.float32(1.0)]
+    bufs = [np.array([v], np.float32) for v in x]
+    got = O.np_allreduce(O.SHUFFLE, bufs, 1)[0]
+    assert got == np.float32(np.float32(np.float32(x[0] + x[1]) + x[2]) + x[3])
+
+
+def test_oracle_bucket_step_threads_invariant():
+    rng = np.random.default_rng(1)
+    shapes = [(33,), (1000,), (7, 9), (4096,)]
+    grads = [[rng.standard_normal(s).astype(np.float32).ravel() for s in shapes] for _ in range(4)]
+    base = [rng.standard_normal(s).astype(np.float32).ravel() for s in shapes]
+    outs = []
+    for nt in (1, 3, 8):
+        params = [b.copy() for b in base]
+        O.c_bucket_step(O.SHUFFLE, 2, grads, params, O.EPI_SGD, 0.25, 0.1, nthreads=nt)
+        outs.append(np.concatenate(params))
+    assert all(np.array_equal(outs[0], o) for o in outs[1:])
+    want = O.np_allreduce(O.SHUFFLE, [O.np_pack(g) for g in grads], 2, O.EPI_SGD, 0.25, 0.1, O.np_pack(base))
+    assert np.array_equal(outs[0], want)
+
+
+def test_lowering_is_rank_invariant_and_covers_the_plan():
+    _lib()
+    from paper_2004_14020_b200 import gradsets
+    from paper_2004_14020_b200.collective import Pattern, ReduceModel
+    from paper_2004_14020_b200.costmodel import NetworkModel
+    from paper_2004_14020_b200.executor import lower
+    from paper_2004_14020_b200.pipeline import run_pipeline
+    from paper_2004_14020_b200.sim import SimConfig
+
+    for model in ("resnet50", "inception_v3"):
+        ts = gradsets.gradient_set(model)
+        numels = {gradsets.param_id(i, len(ts)): t.numel for i, t in enumerate(ts)}
+        art = run_pipeline(gradsets.layered_chain_dag(model),
+                           SimConfig(workers=8, network=NetworkModel(10.0, 1 / 460e3), reduce=ReduceModel(400, 10)))
+        plan = lower(art, numels, 8, Pattern.SHUFFLE)
+        assert plan.digest() == lower(art, numels, 8, Pattern.SHUFFLE).digest()
+        # launch order = transfer schedule order; members = batch plan members
+        assert [b.group_id for b in plan.buckets] == [t.group_id for t in art.transfer_schedule.transfers]
+        groups = {g.group_id: g for g in art.batch_plan.groups}
+        for b in plan.buckets:
+            assert b.param_ids == groups[b.group_id].param_ids
+            assert b.depth == art.depths[b.group_id]
+            assert b.bucket_off % 256 == 0 and b.flag_off % 256 == 0 and b.param_off % 256 == 0
+        assert plan.total_numel == sum(t.numel for t in ts)
+        # regions never overlap
+        spans = sorted((b.bucket_off, b.flag_off) for b in plan.buckets)
+        assert all(a[1] <= b[0] for a, b in zip(spans, spans[1:]))
