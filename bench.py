@@ -49,6 +49,9 @@ def parse_args():
     ap.add_argument("--pattern", default="shuffle", choices=["shuffle", "ring", "hd"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--no-exposed", action="store_true", help="skip the model fwd/bwd exposed-comm measurement")
+    ap.add_argument("--batch", type=int, default=64, help="per-GPU batch for the exposed-comm measurement")
+    ap.add_argument("--exposed-iters", type=int, default=10)
     return ap.parse_args()
 
 
@@ -317,6 +320,114 @@ def nccl_baseline(torch, dist, params, grads_dev, world, steps, warmup, bucket_b
     return t.item(), len(buckets)
 
 
+def measure_exposed(args, plan, ids, world, rank, dev, dist):
+    """Exposed communication per iteration, T - C (sim.py:155-157), measured on
+    the real model: torchvision `args.model` (random init, synthetic batch,
+    bf16 autocast, fp32 parameters and gradients), forward + backward on every
+    GPU.  C = compute only (no aggregation, no update).  Caramel: the Aggregator
+    launches each bucket from gradient hooks in the enforced order during
+    backward, SGD fused.  NCCL: DistributedDataParallel (25 MiB buckets) +
+    torch.optim.SGD.  CUDA events around `exposed_iters` iterations, max over ranks."""
+    import torch
+    import torchvision
+
+    from paper_2004_14020_b200.executor import Aggregator
+
+    size = 299 if args.model == "inception_v3" else 224
+    B, K = args.batch, args.exposed_iters
+
+    def make():
+        torch.manual_seed(7)
+        kw = {"aux_logits": True, "init_weights": False} if args.model == "inception_v3" else {}
+        return getattr(torchvision.models, args.model)(**kw).to(dev)
+
+    gen = torch.Generator(device=dev).manual_seed(1000 * (MODEL_INDEX[args.model] + 1) + rank)
+    x = torch.randn(B, 3, size, size, device=dev, generator=gen)
+    y = torch.randint(0, 1000, (B,), device=dev, generator=gen)
+    loss_fn = torch.nn.CrossEntropyLoss()
+
+    def fwd_bwd(m):
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            out = m(x)
+            if isinstance(out, tuple) or hasattr(out, "logits"):
+                out = out[0] if isinstance(out, tuple) else out.logits
+            loss = loss_fn(out.float(), y)
+        loss.backward()
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(K):
+            fn()
+        e.record()
+        e.synchronize()
+        ms = s.elapsed_time(e) / K
+        if dist is not None:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        return ms
+
+    model = make()
+    named = list(model.named_parameters())
+    from paper_2004_14020_b200 import gradsets
+
+    if [tuple(p.shape) for _, p in named] != [t.shape for t in gradsets.gradient_set(args.model)]:
+        raise RuntimeError("model parameters do not match the recorded gradient set")
+    for p in model.parameters():
+        p.grad = torch.zeros_like(p)
+
+    def compute_only():
+        model.zero_grad(set_to_none=False)
+        fwd_bwd(model)
+
+    c_ms = timed(compute_only)
+
+    agg = Aggregator(plan, dict(zip(ids, model.parameters())), rank=rank, lr=LR, epilogue="sgd")
+    agg.attach_hooks()
+
+    def caramel_step():
+        model.zero_grad(set_to_none=False)
+        agg.begin_iteration()
+        fwd_bwd(model)
+        agg.finish_iteration()
+
+    k_ms = timed(caramel_step)
+    agg.status()
+    agg.close()
+    del model, agg
+    torch.cuda.empty_cache()
+
+    nccl_ms = None
+    if dist is not None:
+        from torch.nn.parallel import DistributedDataParallel as DDP
+
+        m2 = make()
+        ddp = DDP(m2, device_ids=[dev.index], bucket_cap_mb=25, gradient_as_bucket_view=True)
+        opt = torch.optim.SGD(m2.parameters(), lr=LR)
+
+        def ddp_step():
+            opt.zero_grad(set_to_none=False)
+            fwd_bwd(ddp)
+            opt.step()
+
+        nccl_ms = timed(ddp_step)
+        del ddp, m2, opt
+        torch.cuda.empty_cache()
+    out = {"compute_ms": round(c_ms, 4), "caramel_ms": round(k_ms, 4),
+           "caramel_exposed_ms": round(k_ms - c_ms, 4),
+           "model": f"torchvision {args.model}, batch {B}/GPU, {size}x{size}, bf16 autocast, fp32 grads",
+           "iters": K}
+    if nccl_ms is not None:
+        out.update({"nccl_ddp_ms": round(nccl_ms, 4), "nccl_ddp_exposed_ms": round(nccl_ms - c_ms, 4)})
+    return out
+
+
 def run_caramel(args) -> int:
     import ctypes
 
@@ -463,6 +574,15 @@ def run_caramel(args) -> int:
                 "bus_gbs": round(plan.bus_bytes() / (nms * 1e-3) / 1e9, 1) if world > 1 else None,
                 "buckets": nb, "bucket_mib": 25}
 
+    # ---- exposed communication on the real model (T - C) --------------------
+    exposed = None
+    if not args.no_exposed:
+        agg.close()
+        for pid in ids:  # free the step's tensors before the model runs
+            params[pid] = None
+        torch.cuda.empty_cache()
+        exposed = measure_exposed(args, plan, ids, world, rank, dev, dist)
+
     # ---- CPU baseline (rank 0, N = 1 only) ----------------------------------
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -499,7 +619,8 @@ def run_caramel(args) -> int:
                    "network_model": {"latency_us": NVLINK_MODEL[0], "per_byte_us": NVLINK_MODEL[1]},
                    "threshold_bytes": art.threshold_bytes},
         "bus_gbs": round(bus, 1) if bus is not None else None,
-        "exposed_comm_ms_per_iter": None,
+        "exposed_comm_ms_per_iter": exposed["caramel_exposed_ms"] if exposed else None,
+        "exposed_comm": exposed,
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -510,7 +631,8 @@ def run_caramel(args) -> int:
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
-    agg.close()
+    if exposed is None:
+        agg.close()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()

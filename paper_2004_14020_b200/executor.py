@@ -264,10 +264,10 @@ class Aggregator:
     # -- overlapped mode: launch when the last gradient of a bucket is ready ----
     def attach_hooks(self) -> None:
         """Launch each bucket on the comm stream as soon as its last member's
-        gradient is accumulated, never out of the planned launch order."""
+        gradient is accumulated, never out of the planned launch order.  Call
+        begin_iteration() before every backward and finish_iteration() after."""
         for pid, p in self.params.items():
             self._hooks.append(p.register_post_accumulate_grad_hook(self._make_hook(pid)))
-        self.begin_iteration()
 
     def _make_hook(self, pid):
         def hook(_p):
@@ -278,6 +278,8 @@ class Aggregator:
         return hook
 
     def begin_iteration(self) -> None:
+        """Arm every bucket for one backward pass (gradients must be zeroed in
+        place, e.g. zero_grad(set_to_none=False), so the segment tables stay valid)."""
         for lv in self._live:
             lv.remaining = len(lv.members)
             lv.done = None

@@ -85,13 +85,73 @@ def main() -> int:
                     bad = np.nonzero(got.view(np.uint32) != want.view(np.uint32))[0]
                     print(f"rank {rank}: MISMATCH pattern={pat} depth={depth} epi={epi} arena={arena} "
                           f"epoch={epoch}: {bad.size} elems, first {bad[:5]}", flush=True)
+    ctx.close()
+    failures += overlapped_hooks_check(rank, world, dev)
     t = torch.tensor([failures], device=dev)
     dist.all_reduce(t)
     if rank == 0:
-        print(f"multigpu parity: world={world} cases={len(layout) * 6} failures={int(t.item())}", flush=True)
-    ctx.close()
+        print(f"multigpu parity: world={world} cases={len(layout) * 6 + 3} failures={int(t.item())}", flush=True)
     dist.destroy_process_group()
     return 0 if int(t.item()) == 0 else 1
+
+
+def overlapped_hooks_check(rank: int, world: int, dev) -> int:
+    """Real backward on every rank, buckets launched from gradient hooks in the
+    enforced order, SGD fused into the all-gather; every replica must equal
+    theta - lr * ((sum of all ranks' grads in rank order) * (1/p))."""
+    from paper_2004_14020_b200 import gradsets
+    from paper_2004_14020_b200.collective import Pattern, ReduceModel
+    from paper_2004_14020_b200.costmodel import NetworkModel
+    from paper_2004_14020_b200.executor import Aggregator, lower
+    from paper_2004_14020_b200.pipeline import run_pipeline
+    from paper_2004_14020_b200.sim import SimConfig
+
+    def tiny():
+        torch.manual_seed(0)
+        return torch.nn.Sequential(torch.nn.Linear(37, 64), torch.nn.ReLU(), torch.nn.Linear(64, 129),
+                                   torch.nn.ReLU(), torch.nn.Linear(129, 10)).to(dev)
+
+    lr = 0.05
+    model, ref = tiny(), tiny()
+    tensors = tuple(gradsets.Tensor(n, tuple(p.shape)) for n, p in model.named_parameters())
+    art = run_pipeline(gradsets.layered_chain_dag(tensors),
+                       SimConfig(workers=world, network=NetworkModel(10.0, 1e-4), reduce=ReduceModel(400.0, 10.0)))
+    ids = [gradsets.param_id(i, len(tensors)) for i in range(len(tensors))]
+    plan = lower(art, {pid: t.numel for pid, t in zip(ids, tensors)}, world, Pattern.SHUFFLE)
+    agg = Aggregator(plan, dict(zip(ids, model.parameters())), rank=rank, lr=lr, epilogue="sgd")
+    agg.attach_hooks()
+    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
+    fails = 0
+    for it in range(3):
+        x = torch.randn(16, 37, device=dev, generator=gen)
+        ref.zero_grad(set_to_none=False)
+        ref(x).square().mean().backward()
+        flat = torch.cat([p.grad.reshape(-1) for p in ref.parameters()])
+        allg = [torch.empty_like(flat) for _ in range(world)]
+        dist.all_gather(allg, flat)
+        s = allg[0].clone()
+        for q in range(1, world):
+            s = s + allg[q]
+        step = lr * (s * (1.0 / world))
+        off = 0
+        with torch.no_grad():
+            for p in ref.parameters():
+                n = p.numel()
+                p.copy_(p - step[off:off + n].view_as(p))
+                off += n
+        model.zero_grad(set_to_none=False)
+        agg.begin_iteration()
+        model(x).square().mean().backward()
+        agg.finish_iteration()
+        torch.cuda.synchronize()
+        agg.status()
+        for a, b in zip(model.parameters(), ref.parameters()):
+            if not torch.equal(a, b):
+                fails += 1
+                print(f"rank {rank}: overlapped hooks mismatch at iteration {it}", flush=True)
+                break
+    agg.close()
+    return fails
 
 
 if __name__ == "__main__":
