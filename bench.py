@@ -270,9 +270,7 @@ def time_kernel_gated(agg, torch, reps=20):
     for a, b in evs:
         N.check(N.lib().caramel_epoch_advance(agg.ctx._ctx, ctypes.c_void_p(stream.cuda_stream)))
         a.record(stream)
-        N.check(N.lib().caramel_allreduce_many(agg.ctx._ctx, agg._host_list, len(agg._live),
-                                               agg._dev_list.data_ptr(), agg._dev_prefix.data_ptr(), 0,
-                                               ctypes.c_void_p(stream.cuda_stream)))
+        agg._launch_range(0, len(agg._live), stream.cuda_stream, N.MANY_FUSED, 0)
         b.record(stream)
     torch.cuda.synchronize()
     ts = sorted(a.elapsed_time(b) for a, b in evs)

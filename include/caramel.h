@@ -163,20 +163,30 @@ int caramel_epoch_advance(caramel_ctx* ctx, void* stream);
 int caramel_allreduce_update(caramel_ctx* ctx, const caramel_bucket* bucket,
                              uint32_t epoch, void* stream);
 
-/* A list of buckets in launch order as ONE launch (the back-to-back pass:
- * every bucket's gradients already produced).  `host` is the descriptor list
- * (validated, sizes the grid); `dev_buckets` is a device copy of the same
- * caramel_bucket[count] and `dev_prefix` a device uint64_t[2*(count+1)]:
- * element prefix sums of the buckets (prefix[0] = 0) followed by prefix sums
- * of their member-segment counts.  All buckets share pattern, epilogue and
- * flags.  The
- * two-shot runs phase-major (every pack, then every reduce/all-gather, then
- * every completion wait); with world == 1 the concatenated element space is
- * tiled over the whole GPU.  Per bucket the result equals caramel_allreduce /
- * caramel_allreduce_update on that bucket. */
+/* caramel_allreduce_many modes. */
+#define CARAMEL_MANY_FUSED 0  /* flat phases + cross-rank grid barriers: fastest;
+                                 every rank must issue the identical list */
+#define CARAMEL_MANY_FLAGS 1  /* per-(bucket, chunk, tile) flags, the same words
+                                 single-bucket launches use: ranks may group the
+                                 same launch order into different lists */
+
+/* A list of buckets in launch order as ONE launch (every listed bucket's
+ * gradients already produced).  `host` is the descriptor list (validated);
+ * `dev_buckets` a device copy of the same caramel_bucket[count];
+ * `dev_prefix` / `dev_segprefix` device uint64_t[count+1] prefix sums of the
+ * buckets' element counts / member-segment counts (absolute values are fine,
+ * so a sub-range of a longer list is passed by offsetting all three
+ * pointers).  All buckets share pattern, epilogue and flags.  `ctas`: CTAs per
+ * rank, 0 = library default (the whole GPU).  `mode`: CARAMEL_MANY_*.  In
+ * FUSED mode the two-shot runs as three flat
+ * phases (pack / pull-reduce-epilogue-push / unpack) separated by cross-rank
+ * grid barriers, every element owned per the bucket's chunk/shard rule; with
+ * world == 1 the concatenated element space is tiled over the grid.  Per
+ * bucket the result equals caramel_allreduce[_update] on that bucket. */
 int caramel_allreduce_many(caramel_ctx* ctx, const caramel_bucket* host, int32_t count,
-                           uint64_t dev_buckets, uint64_t dev_prefix, uint32_t epoch,
-                           void* stream);
+                           uint64_t dev_buckets, uint64_t dev_prefix,
+                           uint64_t dev_segprefix, int32_t ctas, int32_t mode,
+                           uint32_t epoch, void* stream);
 
 #ifdef __cplusplus
 }

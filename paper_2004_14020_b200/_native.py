@@ -18,6 +18,7 @@ HEADER = HERE.parent / "include" / "caramel.h"
 RING, HD, SHUFFLE = 0, 1, 2
 EPI_SUM, EPI_SCALE, EPI_SGD = 0, 1, 2
 F_PACK, F_UNPACK, F_PARAM_ARENA = 1, 2, 4
+MANY_FUSED, MANY_FLAGS = 0, 1
 MAX_RANKS = 8
 MAX_DEPTH = 8
 
@@ -95,7 +96,8 @@ SIGNATURES = {
     "caramel_allreduce_update": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Bucket), ctypes.c_uint32,
                                                 ctypes.c_void_p]),
     "caramel_allreduce_many": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Bucket), ctypes.c_int32,
-                                              ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p]),
+                                              ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int32,
+                                              ctypes.c_int32, ctypes.c_uint32, ctypes.c_void_p]),
 }
 
 

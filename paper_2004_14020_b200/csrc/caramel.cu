@@ -580,7 +580,8 @@ struct KParams {          // one bucket
 struct MParams {          // a list of buckets, processed in launch order
   Env env;
   const caramel_bucket* bs;
-  const uint64_t* prefix; // prefix[i] = elements of buckets [0, i)
+  const uint64_t* prefix;    // element prefix sums, prefix[i+1] - prefix[i] = bs[i].numel (absolute)
+  const uint64_t* segprefix; // member-segment prefix sums (absolute)
   int nb;
 };
 
@@ -1083,9 +1084,9 @@ __global__ void __launch_bounds__(THREADS, 2) k_local_many(const __grid_constant
   const int lr_idx = blockIdx.y;
   const Env E = P.env;
   const uint64_t* pre = P.prefix;
-  const uint64_t* spre = P.prefix + P.nb + 1;
+  const uint64_t* spre = P.segprefix;
   uint64_t lo, hi;
-  tile_of(0, pre[P.nb], gridDim.x, blockIdx.x, lo, hi);
+  tile_of(pre[0], pre[P.nb], gridDim.x, blockIdx.x, lo, hi);
   if (lo >= hi) return;
   auto bucket_of = [&](const uint64_t* arr, uint64_t x) {  // last i with arr[i] <= x
     int a = 0, b = P.nb - 1;
@@ -1204,7 +1205,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_shuffle_fused(const __grid_const
   const caramel_bucket B0 = P.bs[0];
   const bool arena = (B0.flags & CARAMEL_F_PARAM_ARENA) && B0.epilogue == CARAMEL_EPI_SGD;
   const uint64_t* pre = P.prefix;
-  const uint64_t* spre = P.prefix + P.nb + 1;
+  const uint64_t* spre = P.segprefix;
   auto bucket_of = [&](const uint64_t* arr, uint64_t x) {  // last i with arr[i] <= x
     int a = 0, b = P.nb - 1;
     while (a < b) {
@@ -1216,7 +1217,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_shuffle_fused(const __grid_const
   // ---- phase 0: pack ---------------------------------------------------------
   if (B0.flags & CARAMEL_F_PACK) {
     uint64_t lo, hi;
-    tile_of(0, pre[P.nb], gridDim.x, blockIdx.x, lo, hi);
+    tile_of(pre[0], pre[P.nb], gridDim.x, blockIdx.x, lo, hi);
     if (lo < hi) {
       const int ba = bucket_of(pre, lo), bb = bucket_of(pre, hi - 1);
       const caramel_bucket Ba = P.bs[ba], Bb = P.bs[bb];
@@ -1358,7 +1359,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_shuffle_fused(const __grid_const
   if ((B0.flags & CARAMEL_F_UNPACK) && !arena) {
     const bool to_param = B0.epilogue == CARAMEL_EPI_SGD;
     uint64_t lo, hi;
-    tile_of(0, pre[P.nb], gridDim.x, blockIdx.x, lo, hi);
+    tile_of(pre[0], pre[P.nb], gridDim.x, blockIdx.x, lo, hi);
     if (lo < hi) {
       const int ba = bucket_of(pre, lo), bb = bucket_of(pre, hi - 1);
       const caramel_bucket Ba = P.bs[ba], Bb = P.bs[bb];
@@ -1404,7 +1405,53 @@ __global__ void __launch_bounds__(THREADS, 1) k_collective_many(const __grid_con
     if (jj < 0) jj += G;
     return jj < ctas ? jj : -1;
   };
-  {  // ring / hd: bucket by bucket (the two-shot list runs in k_shuffle_fused)
+  if (PAT == CARAMEL_SHUFFLE) {
+    // Per-bucket-flag list (CARAMEL_MANY_FLAGS): phase-major.  A .sys release
+    // waits for every outstanding remote store of the CTA (about one NVLink
+    // round trip), so all packs go out, then ONE fence.acq_rel.sys and every
+    // READY flag as a relaxed store (READY depends on local work only).  DONE
+    // is published per bucket: deferring it would make bucket b's completion
+    // wait for bucket b+1's READY, which a rank that launches bucket by bucket
+    // only sends after b completes -- a deadlock.  Flags are the same
+    // (bucket, chunk, tile) words a single-bucket launch uses, so ranks may
+    // group the same launch order into different lists.
+    auto publish_deferred = [&](int slot) {
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        fence_acq_rel_sys();
+        const int me = E.rank_base + lr_idx, p = E.world;
+        int base = 0;
+        for (int i = 0; i < P.nb; ++i) {
+          const caramel_bucket B = P.bs[i];
+          const int j = my_tile(base, B.ctas);
+          base = (base + B.ctas) % G;
+          if (j < 0 || B.numel == 0) continue;
+          const int ns = nslots(PAT, p);
+          for (int idx = threadIdx.x; idx < B.depth * p; idx += 32) {
+            const int c = idx / p, q = idx % p;
+            uint32_t* f = reinterpret_cast<uint32_t*>(E.arena[q] + B.flag_off) +
+                          ((((uint64_t)c * B.ctas + j) * ns + slot) * p + me);
+            st_relaxed_sys(f, epoch);
+          }
+        }
+      }
+    };
+    for (int phase = 0; phase < 3; ++phase) {
+      int base = 0;
+      for (int i = 0; i < P.nb; ++i) {
+        const caramel_bucket B = P.bs[i];
+        const int j = my_tile(base, B.ctas);
+        base = (base + B.ctas) % G;
+        if (j < 0 || B.numel == 0) continue;
+        BucketRun R;
+        make_run(R, E, B, PAT, lr_idx, epoch, j);
+        if (phase == 0) phase_pack<PAT, true>(R);
+        else if (phase == 1) phase_shuffle<NP, false>(R);
+        else phase_finish<PAT>(R);
+      }
+      if (phase == 0) publish_deferred(SLOT_READY);
+    }
+  } else {  // ring / hd: bucket by bucket
     int base = 0;
     for (int i = 0; i < P.nb; ++i) {
       const caramel_bucket B = P.bs[i];
@@ -1695,8 +1742,17 @@ static mfn_t pick_fused(int p) {
 }
 
 template <int PAT>
-static mfn_t pick_np_many(int) {
-  return k_collective_many<PAT, 2>;  // ring / hd only; NP does not shape them
+static mfn_t pick_np_many(int p) {
+  if (PAT != CARAMEL_SHUFFLE) return k_collective_many<PAT, 2>;  // NP does not shape ring / hd
+  switch (p) {
+    case 2: return k_collective_many<PAT, 2>;
+    case 3: return k_collective_many<PAT, 3>;
+    case 4: return k_collective_many<PAT, 4>;
+    case 5: return k_collective_many<PAT, 5>;
+    case 6: return k_collective_many<PAT, 6>;
+    case 7: return k_collective_many<PAT, 7>;
+    default: return k_collective_many<PAT, 8>;
+  }
 }
 
 extern "C" {
@@ -1803,8 +1859,11 @@ int caramel_allreduce_update(caramel_ctx* c, const caramel_bucket* b, uint32_t e
 }
 
 int caramel_allreduce_many(caramel_ctx* c, const caramel_bucket* host, int32_t count, uint64_t dev_buckets,
-                           uint64_t dev_prefix, uint32_t epoch, void* stream) {
-  if (!c || !host || count < 1 || !dev_buckets || !dev_prefix)
+                           uint64_t dev_prefix, uint64_t dev_segprefix, int32_t ctas, int32_t mode,
+                           uint32_t epoch, void* stream) {
+  if (mode != CARAMEL_MANY_FUSED && mode != CARAMEL_MANY_FLAGS)
+    return set_err(CARAMEL_EINVAL, "allreduce_many: unknown mode %d", mode);
+  if (!c || !host || count < 1 || !dev_buckets || !dev_prefix || !dev_segprefix)
     return set_err(CARAMEL_EINVAL, "allreduce_many: null argument or empty list");
   if (!c->imported) return set_err(CARAMEL_ESTATE, "peer arenas not mapped (call caramel_import)");
   const int pattern = host[0].pattern;
@@ -1828,17 +1887,29 @@ int caramel_allreduce_many(caramel_ctx* c, const caramel_bucket* host, int32_t c
   fill_env(c, P.env, epoch);
   P.bs = reinterpret_cast<const caramel_bucket*>(dev_buckets);
   P.prefix = reinterpret_cast<const uint64_t*>(dev_prefix);
+  P.segprefix = reinterpret_cast<const uint64_t*>(dev_segprefix);
   P.nb = count;
   mfn_t fn;
   if (c->world == 1) fn = k_local_many;
-  else if (pattern == CARAMEL_SHUFFLE) {
+  else if (pattern == CARAMEL_SHUFFLE && mode == CARAMEL_MANY_FLAGS) {
+    fn = pick_np_many<CARAMEL_SHUFFLE>(c->world);
+  } else if (pattern == CARAMEL_SHUFFLE) {
     if (count > MAX_FUSED_BUCKETS)
       return set_err(CARAMEL_EINVAL, "allreduce_many: at most %d buckets per fused launch", MAX_FUSED_BUCKETS);
     fn = pick_fused(c->world);
-    gmax = c->nlocal > 1 ? gmax : c->sms;  // flat phases: the whole GPU (one CTA per SM)
+    if (c->nlocal == 1) gmax = c->sms;  // flat phases: by default the whole GPU (one CTA per SM)
+  } else if (pattern == CARAMEL_RING) {
+    fn = pick_np_many<CARAMEL_RING>(c->world);
+  } else {
+    fn = pick_np_many<CARAMEL_HD>(c->world);
   }
-  else if (pattern == CARAMEL_RING) fn = pick_np_many<CARAMEL_RING>(c->world);
-  else fn = pick_np_many<CARAMEL_HD>(c->world);
+  if (ctas > 0) {
+    // caller's grid; per-bucket-flag and ring/hd lists need every bucket's tiles
+    int need = 1;
+    for (int i = 0; i < count; ++i) need = host[i].ctas > need ? host[i].ctas : need;
+    const bool tiled = c->world > 1 && (mode == CARAMEL_MANY_FLAGS || pattern != CARAMEL_SHUFFLE);
+    gmax = tiled && ctas < need ? need : ctas;
+  }
   dim3 grid(gmax, c->nlocal);
   if (c->nlocal > 1) {
     void* args[] = {(void*)&P};

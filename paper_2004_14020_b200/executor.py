@@ -183,6 +183,7 @@ class Aggregator:
         self._hooks = []
         self.epoch = 0
         self.launches = 0
+        self._last_done = None
         self._build_list()
 
     # -- setup -----------------------------------------------------------------
@@ -219,7 +220,9 @@ class Aggregator:
         for lv in self._live:
             prefix.append(prefix[-1] + lv.spec.numel)
             segpre.append(segpre[-1] + len(lv.members))
-        self._dev_prefix = torch.tensor(prefix + segpre, dtype=torch.int64, device=self.device)
+        self._prefix = prefix
+        self._dev_prefix = torch.tensor(prefix, dtype=torch.int64, device=self.device)
+        self._dev_segprefix = torch.tensor(segpre, dtype=torch.int64, device=self.device)
 
     def refresh_tables(self) -> None:
         """Rebuild segment tables (after gradients were reallocated)."""
@@ -250,13 +253,20 @@ class Aggregator:
         s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
         N.check(N.lib().caramel_epoch_advance(self.ctx._ctx, ctypes.c_void_p(s)))
         if fused:
-            N.check(N.lib().caramel_allreduce_many(self.ctx._ctx, self._host_list, len(self._live),
-                                                   self._dev_list.data_ptr(), self._dev_prefix.data_ptr(), 0,
-                                                   ctypes.c_void_p(s)))
-            self.launches += 1
+            self._launch_range(0, len(self._live), s, N.MANY_FUSED, 0)
         else:
             for lv in self._live:
                 self._launch(lv, s)
+
+    def _launch_range(self, i: int, j: int, stream: int, mode: int, ctas: int) -> None:
+        """Buckets [i, j) of the launch order as one caramel_allreduce_many launch."""
+        bsz = ctypes.sizeof(N.Bucket)
+        host = ctypes.cast(ctypes.byref(self._host_list, i * bsz), ctypes.POINTER(N.Bucket))
+        N.check(N.lib().caramel_allreduce_many(self.ctx._ctx, host, j - i, self._dev_list.data_ptr() + i * bsz,
+                                               self._dev_prefix.data_ptr() + 8 * i,
+                                               self._dev_segprefix.data_ptr() + 8 * i, ctas, mode, 0,
+                                               ctypes.c_void_p(stream)))
+        self.launches += 1
 
     def kernels_per_step(self, fused: bool = True) -> int:
         return 2 if fused else 1 + len(self._live)
@@ -284,25 +294,53 @@ class Aggregator:
             lv.remaining = len(lv.members)
             lv.done = None
         self._next = 0
+        self._last_done = None
         cur = torch.cuda.current_stream(self.device)
         self.comm_stream.wait_stream(cur)
         N.check(N.lib().caramel_epoch_advance(self.ctx._ctx,
                                               ctypes.c_void_p(self.comm_stream.cuda_stream)))
 
-    def _drain(self) -> None:
-        """Launch every ready bucket from the head of the launch order."""
+    #: overlapped mode: while the comm stream is busy, ready buckets are held
+    #: back and coalesced into one list launch (per-bucket flags, so ranks may
+    #: group differently) until this many are pending or this many bytes
+    coalesce_buckets = 16
+    coalesce_bytes = 8 << 20
+    coalesce_ctas = 32  # grid of a coalesced launch: leave SMs to the backward pass
+
+    def _comm_busy(self) -> bool:
+        return self._last_done is not None and not self._last_done.query()
+
+    def _drain(self, force: bool = False) -> None:
+        """Launch ready buckets from the head of the launch order: one at a
+        time when the comm stream is idle, coalesced while it is busy."""
+        j = self._next
+        while j < len(self._live) and self._live[j].remaining == 0:
+            j += 1
+        if j == self._next:
+            return
+        pending_bytes = 4 * (self._prefix[j] - self._prefix[self._next])
+        if not force and self._comm_busy() and j - self._next < self.coalesce_buckets \
+                and pending_bytes < self.coalesce_bytes:
+            return
         cur = torch.cuda.current_stream(self.device)
-        while self._next < len(self._live) and self._live[self._next].remaining == 0:
-            lv = self._live[self._next]
-            self.comm_stream.wait_stream(cur)  # its gradients are produced on `cur`
-            self._launch(lv, self.comm_stream.cuda_stream)
-            ev = torch.cuda.Event()
-            ev.record(self.comm_stream)
+        self.comm_stream.wait_stream(cur)  # the gradients are produced on `cur`
+        s = self.comm_stream.cuda_stream
+        if j - self._next == 1:
+            self._launch(self._live[self._next], s)
+        else:
+            ctas = min(self.coalesce_ctas, max(lv.spec.ctas for lv in self._live[self._next:j]) * 4)
+            self._launch_range(self._next, j, s, N.MANY_FLAGS, ctas)
+        ev = torch.cuda.Event()
+        ev.record(self.comm_stream)
+        for lv in self._live[self._next:j]:
             lv.done = ev
-            self._next += 1
+        self._last_done = ev
+        self._next = j
 
     def finish_iteration(self) -> None:
-        """Make the current stream wait for every launched bucket."""
+        """Launch whatever is still held back, then make the current stream
+        wait for every bucket."""
+        self._drain(force=True)
         if self._next != len(self._live):
             missing = [lv.spec.group_id for lv in self._live[self._next:]]
             raise RuntimeError(f"buckets never became ready: {missing[:5]}")

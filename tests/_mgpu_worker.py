@@ -86,6 +86,7 @@ def main() -> int:
                     print(f"rank {rank}: MISMATCH pattern={pat} depth={depth} epi={epi} arena={arena} "
                           f"epoch={epoch}: {bad.size} elems, first {bad[:5]}", flush=True)
     ctx.close()
+    failures += mixed_grouping_check(rank, world, dev)
     failures += overlapped_hooks_check(rank, world, dev)
     t = torch.tensor([failures], device=dev)
     dist.all_reduce(t)
@@ -93,6 +94,75 @@ def main() -> int:
         print(f"multigpu parity: world={world} cases={len(layout) * 6 + 3} failures={int(t.item())}", flush=True)
     dist.destroy_process_group()
     return 0 if int(t.item()) == 0 else 1
+
+
+def mixed_grouping_check(rank: int, world: int, dev) -> int:
+    """Same launch order, different grouping per rank: rank 0 issues the five
+    buckets as ONE per-bucket-flag list (CARAMEL_MANY_FLAGS), odd ranks one
+    launch per bucket, the rest as two lists.  Every rank must match the oracle."""
+    import ctypes
+
+    rng = np.random.default_rng(300 + rank)
+    bucket_shapes = [[(5,), (300,)], [(7, 7)], [(1,)], [(4096,), (3,)], [(64, 65)]]
+    depths = [1, 2, 1, 3, 2]
+    specs, off = [], 0
+    for shapes, depth in zip(bucket_shapes, depths):
+        numel = sum(int(np.prod(s)) for s in shapes)
+        ctas, bbytes, fbytes = N.bucket_layout(numel, depth, N.SHUFFLE, world)
+        boff = off
+        foff = (boff + bbytes + 255) // 256 * 256
+        off = (foff + fbytes + 255) // 256 * 256
+        specs.append((shapes, depth, numel, ctas, boff, foff))
+    ctx = comm.Context(rank, world, arena_bytes=off)
+    ctx.bootstrap()
+    stream = torch.cuda.current_stream().cuda_stream
+    fails = 0
+    for epoch in (1, 2, 3):
+        grads, gdev, descs, tables = [], [], [], []
+        for shapes, depth, numel, ctas, boff, foff in specs:
+            g = [rng.standard_normal(s).astype(np.float32) for s in shapes]
+            gd = [torch.from_numpy(a).to(dev) for a in g]
+            t = comm.segment_table([comm.segments_for(gd)], dev)
+            grads.append(g)
+            gdev.append(gd)
+            tables.append(t)
+            descs.append(comm.make_bucket(numel, boff, foff, depth=depth, pattern=N.SHUFFLE, epilogue=N.EPI_SUM,
+                                          flags=N.F_PACK | N.F_UNPACK, ctas=ctas, segs=t, nseg=len(shapes)))
+        host = (N.Bucket * len(descs))(*descs)
+        dlist = torch.frombuffer(bytearray(bytes(host)), dtype=torch.uint8).to(dev)
+        pre = torch.tensor(np.concatenate([[0], np.cumsum([sp[2] for sp in specs])]), dtype=torch.int64, device=dev)
+        spre = torch.tensor(np.concatenate([[0], np.cumsum([len(sp[0]) for sp in specs])]), dtype=torch.int64,
+                            device=dev)
+        bsz = ctypes.sizeof(N.Bucket)
+
+        def launch_list(i, j):
+            h = ctypes.cast(ctypes.byref(host, i * bsz), ctypes.POINTER(N.Bucket))
+            N.check(N.lib().caramel_allreduce_many(ctx._ctx, h, j - i, dlist.data_ptr() + i * bsz,
+                                                   pre.data_ptr() + 8 * i, spre.data_ptr() + 8 * i, 0,
+                                                   N.MANY_FLAGS, epoch, ctypes.c_void_p(stream)))
+
+        torch.cuda.synchronize()
+        dist.barrier()
+        if rank == 0:
+            launch_list(0, len(descs))
+        elif rank % 2 == 1:
+            for d in descs:
+                ctx.allreduce(d, epoch, stream)
+        else:
+            launch_list(0, 2)
+            launch_list(2, len(descs))
+        ctx.status()
+        for i, (shapes, depth, numel, ctas, boff, foff) in enumerate(specs):
+            flat = torch.from_numpy(O.np_pack(grads[i])).to(dev)
+            allg = [torch.empty_like(flat) for _ in range(world)]
+            dist.all_gather(allg, flat)
+            want = O.np_allreduce(N.SHUFFLE, [a.cpu().numpy() for a in allg], depth)
+            got = torch.cat([t.flatten() for t in gdev[i]]).cpu().numpy()
+            if not np.array_equal(got.view(np.uint32), want.view(np.uint32)):
+                fails += 1
+                print(f"rank {rank}: mixed grouping mismatch bucket {i} epoch {epoch}", flush=True)
+    ctx.close()
+    return fails
 
 
 def overlapped_hooks_check(rank: int, world: int, dev) -> int:

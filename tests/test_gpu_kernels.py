@@ -207,7 +207,7 @@ def test_errors_are_reported_not_raised_in_c():
     ctx3.close()
 
 
-def run_emulated_many(pattern, p, bucket_shapes, depths, epi, *, param_arena=False, epochs=2, seed=11):
+def run_emulated_many(pattern, p, bucket_shapes, depths, epi, *, param_arena=False, epochs=2, seed=11, mode=0):
     """Several buckets in ONE launch (caramel_allreduce_many), device epoch
     counter; every bucket checked against the oracle on every rank."""
     import ctypes
@@ -252,12 +252,13 @@ def run_emulated_many(pattern, p, bucket_shapes, depths, epi, *, param_arena=Fal
                                           lr=lr, scale=1.0 / p))
         host = (N.Bucket * len(descs))(*descs)
         dev_list = torch.frombuffer(bytearray(bytes(host)), dtype=torch.uint8).to(dev)
-        prefix = torch.tensor(np.concatenate([[0], np.cumsum([sp[2] for sp in specs]),
-                                              [0], np.cumsum([len(sp[0]) for sp in specs])]), dtype=torch.int64,
+        prefix = torch.tensor(np.concatenate([[0], np.cumsum([sp[2] for sp in specs])]), dtype=torch.int64,
                               device=dev)
+        segprefix = torch.tensor(np.concatenate([[0], np.cumsum([len(sp[0]) for sp in specs])]),
+                                 dtype=torch.int64, device=dev)
         N.check(N.lib().caramel_epoch_advance(ctx._ctx, ctypes.c_void_p(stream)))
         N.check(N.lib().caramel_allreduce_many(ctx._ctx, host, len(descs), dev_list.data_ptr(), prefix.data_ptr(),
-                                               0, ctypes.c_void_p(stream)))
+                                               segprefix.data_ptr(), 0, mode, 0, ctypes.c_void_p(stream)))
         ctx.status()
         torch.cuda.synchronize()
         for i, (shapes, depth, numel, ctas, boff, foff, pof) in enumerate(specs):
@@ -286,6 +287,13 @@ def test_many_buckets_one_launch(p, pattern):
     N, _ = _native()
     pat = {"ring": N.RING, "hd": N.HD, "shuffle": N.SHUFFLE}[pattern]
     run_emulated_many(pat, p, MANY_BUCKETS, MANY_DEPTHS, N.EPI_SGD, param_arena=True)
+
+
+@pytest.mark.parametrize("p", [2, 3, 8])
+def test_many_buckets_flags_mode(p):
+    N, _ = _native()
+    run_emulated_many(N.SHUFFLE, p, MANY_BUCKETS, MANY_DEPTHS, N.EPI_SGD, param_arena=True, mode=N.MANY_FLAGS)
+    run_emulated_many(N.SHUFFLE, p, MANY_BUCKETS, MANY_DEPTHS, N.EPI_SUM, mode=N.MANY_FLAGS)
 
 
 @pytest.mark.parametrize("epi", [0, 1, 2])
