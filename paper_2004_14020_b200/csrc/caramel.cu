@@ -78,6 +78,16 @@ __device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
 
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
+__device__ __forceinline__ void st_u64_relaxed_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_u64_relaxed_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -606,6 +616,23 @@ __host__ __device__ __forceinline__ uint64_t out_region_elems(uint64_t numel) {
   return (numel + 3) & ~3ull;
 }
 
+// Small two-shot buckets use the LL ("low latency") protocol: every element
+// travels as ONE 64-bit relaxed store {epoch:32 | value:32} straight into its
+// owner's inbox, so arrival of the data is its own flag -- no fence, no flag
+// word, two one-way NVLink hops per bucket.  Region: [float bucket | LL out
+// (numel x 8 B) | LL in (p slots x numel x 8 B)].  Chosen from numel alone, so
+// every rank and every launch kind agrees.
+#define LL_MAX_ELEMS 16384
+__host__ __device__ __forceinline__ bool use_ll(int pattern, int world, uint64_t numel) {
+  return pattern == CARAMEL_SHUFFLE && world > 1 && numel > 0 && numel <= LL_MAX_ELEMS;
+}
+__host__ __device__ __forceinline__ uint64_t ll_out_off(uint64_t numel) {  // bytes from bucket start
+  return 4 * ((numel + 3) & ~3ull);
+}
+__host__ __device__ __forceinline__ uint64_t ll_region_bytes(uint64_t numel, int world) {
+  return ll_out_off(numel) + 8 * numel * (1 + (uint64_t)world);
+}
+
 __host__ __device__ __forceinline__ void shard_bounds(uint64_t n, int k, int p, int c, int s, uint64_t& lo,
                                                       uint64_t& hi) {
   const uint64_t c0 = (n * (uint64_t)c) / k, m = (n * (uint64_t)(c + 1)) / k - c0;
@@ -1022,6 +1049,130 @@ __device__ void phase_hd(const BucketRun& R) {
   }
 }
 
+// ---- LL protocol phases (small two-shot buckets) ------------------------------
+__device__ __forceinline__ uint64_t ll_pack(uint32_t epoch, float v) {
+  return ((uint64_t)epoch << 32) | (uint64_t)__float_as_uint(v);
+}
+
+// spin until the LL word carries `epoch`; returns its value
+__device__ __forceinline__ float ll_wait(const uint64_t* p, uint32_t epoch, const Env& E) {
+  uint64_t w = ld_u64_relaxed_sys(p);
+  if ((uint32_t)(w >> 32) != epoch) {
+    const uint64_t t0 = globaltimer();
+    uint32_t spins = 0;
+    do {
+      w = ld_u64_relaxed_sys(p);
+      if ((++spins & 1023u) == 0 && globaltimer() - t0 > E.timeout_ns) {
+        atomicExch(E.status, CARAMEL_ETIMEOUT);
+        break;
+      }
+    } while ((uint32_t)(w >> 32) != epoch);
+  }
+  return __uint_as_float((uint32_t)w);
+}
+
+__device__ __forceinline__ uint64_t* ll_out(const BucketRun& R, int rank) {
+  return reinterpret_cast<uint64_t*>(R.E->arena[rank] + R.B->bucket_off + ll_out_off(R.B->numel));
+}
+__device__ __forceinline__ uint64_t* ll_in(const BucketRun& R, int rank, int slot) {
+  return ll_out(R, rank) + R.B->numel * (1 + (uint64_t)slot);
+}
+
+// A: every element of my tile of every shard, pushed into its owner's inbox slot `me`
+__device__ void phase_ll_scatter(const BucketRun& R) {
+  const int me = R.X.me, p = R.X.world;
+  const bool pack = R.B->flags & CARAMEL_F_PACK;
+  const float* bkt = R.bucket(me);
+  Cursor gc;
+  cur_init(gc, R.segs, R.B->nseg);
+  for (int c = 0; c < R.B->depth; ++c)
+    for (int s = 0; s < p; ++s) {
+      uint64_t lo, hi;
+      R.shard(c, s, lo, hi);
+      uint64_t* dst = ll_in(R, s, me);
+      for (uint64_t x = lo + threadIdx.x; x < hi; x += blockDim.x) {
+        const float v = pack ? seg_ld1(gc, x, 0) : ld1(bkt + x);
+        st_u64_relaxed_sys(dst + x, ll_pack(R.X.epoch, v));
+      }
+    }
+}
+
+// B: my shard -- wait for every source in rank order, sum, epilogue, push to
+// all.  Loads for LL_U elements x every source are issued together; only the
+// words that have not arrived yet are polled again.
+#define LL_U 4
+template <int NP>
+__device__ void phase_ll_reduce(const BucketRun& R) {
+  const int me = R.X.me;
+  Cursor tc;
+  cur_init(tc, R.segs, R.B->nseg);
+  const float* th = R.theta_flat();
+  const bool sgd = R.B->epilogue == CARAMEL_EPI_SGD;
+  const uint32_t ep = R.X.epoch;
+  for (int c = 0; c < R.B->depth; ++c) {
+    uint64_t lo, hi;
+    R.shard(c, me, lo, hi);
+    const uint64_t T = blockDim.x;
+    for (uint64_t x0 = lo + threadIdx.x; x0 < hi; x0 += LL_U * T) {
+      uint64_t w[LL_U][NP];
+#pragma unroll
+      for (int u = 0; u < LL_U; ++u)
+#pragma unroll
+        for (int q = 0; q < NP; ++q)
+          w[u][q] = (x0 + u * T < hi) ? ld_u64_relaxed_sys(ll_in(R, me, q) + x0 + u * T) : 0;
+#pragma unroll
+      for (int u = 0; u < LL_U; ++u) {
+        const uint64_t x = x0 + u * T;
+        if (x >= hi) break;
+        float acc = 0.f;
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          float v = __uint_as_float((uint32_t)w[u][q]);
+          if ((uint32_t)(w[u][q] >> 32) != ep) v = ll_wait(ll_in(R, me, q) + x, ep, *R.E);
+          acc = q == 0 ? v : __fadd_rn(acc, v);
+        }
+        const float t = sgd ? (th ? ld1(th + x) : seg_ld1(tc, x, 1)) : 0.f;
+        const uint64_t o = ll_pack(ep, epi1(R.B->epilogue, acc, t, R.B->scale, R.B->lr));
+#pragma unroll
+        for (int q = 0; q < NP; ++q) st_u64_relaxed_sys(ll_out(R, q) + x, o);
+      }
+    }
+  }
+}
+
+// C: collect my tile of every shard's result; write to the parameter arena,
+// the members, or the float bucket (loads batched as in B)
+__device__ void phase_ll_finish(const BucketRun& R) {
+  const int me = R.X.me, p = R.X.world;
+  const bool unpack = (R.B->flags & CARAMEL_F_UNPACK) && !R.arena;
+  const int which = R.B->epilogue == CARAMEL_EPI_SGD ? 1 : 0;
+  float* res = R.arena ? R.out(me) : R.bucket(me);
+  Cursor uc;
+  cur_init(uc, R.segs, R.B->nseg);
+  const uint64_t* in = ll_out(R, me);
+  const uint32_t ep = R.X.epoch;
+  const uint64_t T = blockDim.x;
+  for (int c = 0; c < R.B->depth; ++c)
+    for (int s = 0; s < p; ++s) {
+      uint64_t lo, hi;
+      R.shard(c, s, lo, hi);
+      for (uint64_t x0 = lo + threadIdx.x; x0 < hi; x0 += 4 * LL_U * T) {
+        uint64_t w[4 * LL_U];
+#pragma unroll
+        for (int u = 0; u < 4 * LL_U; ++u) w[u] = (x0 + u * T < hi) ? ld_u64_relaxed_sys(in + x0 + u * T) : 0;
+#pragma unroll
+        for (int u = 0; u < 4 * LL_U; ++u) {
+          const uint64_t x = x0 + u * T;
+          if (x >= hi) break;
+          float v = __uint_as_float((uint32_t)w[u]);
+          if ((uint32_t)(w[u] >> 32) != ep) v = ll_wait(in + x, ep, *R.E);
+          if (unpack) seg_st1(uc, x, which, v);
+          else st1(res + x, v);
+        }
+      }
+    }
+}
+
 // phase 3: (shuffle) wait for every rank's all-gather; fused unpack; (ring/hd)
 // release the buffers I read from
 template <int PAT>
@@ -1052,15 +1203,42 @@ __device__ void phase_finish(const BucketRun& R) {
   }
 }
 
+// Publish `slot` for every chunk of this CTA's tile to every rank after ONE
+// fence (a .sys release costs about an NVLink round trip once remote stores
+// are outstanding; one per chunk made depth > 1 slower, not faster).
+__device__ __forceinline__ void publish_chunks(const BucketRun& R, int slot) {
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    fence_acq_rel_sys();
+    const int p = R.X.world;
+    for (int idx = threadIdx.x; idx < R.B->depth * p; idx += 32)
+      st_relaxed_sys(R.X.flag(idx % p, idx / p, slot, R.X.me), R.X.epoch);
+  }
+}
+
 template <int PAT, int NP>
 __device__ __forceinline__ void run_bucket(const Env& E, const caramel_bucket& B, int lr_idx, uint32_t epoch,
                                            int j) {
   BucketRun R;
   make_run(R, E, B, PAT, lr_idx, epoch, j);
-  phase_pack<PAT>(R);
-  if (PAT == CARAMEL_SHUFFLE) phase_shuffle<NP>(R);
-  else if (PAT == CARAMEL_RING) phase_ring(R);
-  else phase_hd(R);
+  if (use_ll(PAT, E.world, B.numel)) {
+    phase_ll_scatter(R);
+    phase_ll_reduce<NP>(R);
+    phase_ll_finish(R);
+    return;
+  }
+  if (PAT == CARAMEL_SHUFFLE) {
+    // all chunks packed, one publication; all chunks reduced and gathered,
+    // one publication (consumers still wait per chunk)
+    phase_pack<PAT, true>(R);
+    publish_chunks(R, SLOT_READY);
+    phase_shuffle<NP, true>(R);
+    publish_chunks(R, SLOT_DONE);
+  } else {
+    phase_pack<PAT>(R);
+    if (PAT == CARAMEL_RING) phase_ring(R);
+    else phase_hd(R);
+  }
   phase_finish<PAT>(R);
 }
 
@@ -1425,7 +1603,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_collective_many(const __grid_con
           const caramel_bucket B = P.bs[i];
           const int j = my_tile(base, B.ctas);
           base = (base + B.ctas) % G;
-          if (j < 0 || B.numel == 0) continue;
+          if (j < 0 || B.numel == 0 || use_ll(PAT, p, B.numel)) continue;
           const int ns = nslots(PAT, p);
           for (int idx = threadIdx.x; idx < B.depth * p; idx += 32) {
             const int c = idx / p, q = idx % p;
@@ -1445,6 +1623,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_collective_many(const __grid_con
         if (j < 0 || B.numel == 0) continue;
         BucketRun R;
         make_run(R, E, B, PAT, lr_idx, epoch, j);
+        if (use_ll(PAT, E.world, B.numel)) {
+          if (phase == 0) phase_ll_scatter(R);
+          else if (phase == 1) phase_ll_reduce<NP>(R);
+          else phase_ll_finish(R);
+          continue;
+        }
         if (phase == 0) phase_pack<PAT, true>(R);
         else if (phase == 1) phase_shuffle<NP, false>(R);
         else phase_finish<PAT>(R);
@@ -1532,6 +1716,9 @@ int caramel_bucket_layout(uint64_t numel, int depth, int pattern, int world, int
   if (world == 1) {
     g = (numel + 4 * tile - 1) / (4 * tile);
     if (g > 148 * 4) g = 148 * 4;
+  } else if (use_ll(pattern, world, numel)) {
+    g = (per + 511) / 512;  // latency-bound: spread the few elements wide
+    if (g > 32) g = 32;
   } else {
     g = (per + tile - 1) / tile;
     uint64_t cap = (uint64_t)default_max_ctas();
@@ -1541,7 +1728,8 @@ int caramel_bucket_layout(uint64_t numel, int depth, int pattern, int world, int
   if (ctas) *ctas = (int32_t)g;
   if (bucket_bytes) {
     const uint64_t e = out_region_elems(numel);
-    *bucket_bytes = 4 * ((world > 1 && pattern != CARAMEL_SHUFFLE) ? 2 * e : e);
+    *bucket_bytes = use_ll(pattern, world, numel) ? (ll_region_bytes(numel, world) + 15) & ~15ull
+                                                  : 4 * ((world > 1 && pattern != CARAMEL_SHUFFLE) ? 2 * e : e);
   }
   if (flag_bytes) {
     uint64_t fb = world == 1 ? 0 : (uint64_t)depth * g * nslots(pattern, world) * world * 4;
@@ -1766,8 +1954,10 @@ static int validate_bucket(const caramel_ctx* c, const caramel_bucket* b) {
   if (b->ctas < 1) return set_err(CARAMEL_EINVAL, "ctas must be >= 1 (see caramel_bucket_layout)");
   if (b->bucket_off & 15) return set_err(CARAMEL_EINVAL, "bucket_off must be 16-byte aligned");
   if (b->numel == 0) return 0;
-  const uint64_t span = 4 * ((c->world > 1 && b->pattern != CARAMEL_SHUFFLE) ? 2 * out_region_elems(b->numel)
-                                                                         : b->numel);
+  const uint64_t span = use_ll(b->pattern, c->world, b->numel)
+                            ? ll_region_bytes(b->numel, c->world)
+                            : 4 * ((c->world > 1 && b->pattern != CARAMEL_SHUFFLE) ? 2 * out_region_elems(b->numel)
+                                                                                   : b->numel);
   if (b->bucket_off + span > c->arena_bytes)
     return set_err(CARAMEL_EINVAL, "bucket [%llu, +%llu B) exceeds the arena", (unsigned long long)b->bucket_off,
                    (unsigned long long)span);

@@ -1,6 +1,6 @@
 """Bucket-size sweep (config 5): caramel two-shot / ring / hd bus GB/s vs
 NCCL all_reduce, one process per GPU.  Launch with torch.distributed.run."""
-import json, os, sys
+import ctypes, json, os, sys
 from pathlib import Path
 import torch, torch.distributed as dist
 ROOT = Path(__file__).resolve().parents[1]
@@ -15,13 +15,14 @@ def main():
     max_bytes = int(os.environ.get("SWEEP_MAX", 1 << 30))
     sizes = [4096 * 4 ** i for i in range(12) if 4096 * 4 ** i <= max_bytes]
     pats = [int(x) for x in os.environ.get("SWEEP_PATTERNS", "2").split(",")]
+    engines = os.environ.get("SWEEP_ENGINES", "single").split(",")
     depths = [int(x) for x in os.environ.get("SWEEP_DEPTHS", "1").split(",")]
     iters = int(os.environ.get("SWEEP_ITERS", 20))
     maxel = max_bytes // 4
     region = max(N.bucket_layout(maxel, d, pt, world)[1] for pt in (0, 1, 2) if not (pt == 1 and world & (world - 1))
                  for d in (1, 8))
     region = (region + (1 << 20)) // (1 << 20) * (1 << 20)
-    ctx = comm.Context(rank, world, arena_bytes=region + (64 << 20))
+    ctx = comm.Context(rank, world, arena_bytes=region + (256 << 20))
     ctx.bootstrap()
     base, _ = ctx.arena_ptrs(0)
     buf = comm._view_fp32(base, maxel)
@@ -31,8 +32,11 @@ def main():
     epoch = {}
     for size in sizes:
         n = size // 4
-        for pat in pats:
+        for engine in engines:
+          for pat in pats:
             if pat == N.HD and world & (world - 1):
+                continue
+            if engine == "fused" and pat != N.SHUFFLE:
                 continue
             for depth in depths:
                 ctas, bbytes, fbytes = N.bucket_layout(n, depth, pat, world)
@@ -40,28 +44,41 @@ def main():
                     ctas = min(ctas, int(os.environ["SWEEP_CTAS"]))
                 foff = region
                 b = comm.make_bucket(n, 0, foff, depth=depth, pattern=pat, epilogue=N.EPI_SUM, flags=0, ctas=ctas)
-                key = (pat, depth, ctas)
-                # flags region shared across sizes: keep epochs monotone per key
-                # by giving each key its own flag region
+                key = (engine, pat, depth, ctas)
                 idx = list(epoch).index(key) if key in epoch else len(epoch)
                 epoch.setdefault(key, 0)
-                b.flag_off = foff + idx * (8 << 20) // 8
+                b.flag_off = foff + idx * (1 << 20)
+                if engine == "fused":
+                    host = (N.Bucket * 1)(b)
+                    dlist = torch.frombuffer(bytearray(bytes(host)), dtype=torch.uint8).to(dev)
+                    pre = torch.tensor([0, n], dtype=torch.int64, device=dev)
+                    spre = torch.tensor([0, 0], dtype=torch.int64, device=dev)
+
+                def launch(ep):
+                    if engine == "fused":
+                        N.check(N.lib().caramel_allreduce_many(ctx._ctx, host, 1, dlist.data_ptr(), pre.data_ptr(),
+                                                               spre.data_ptr(), 0, N.MANY_FUSED, ep,
+                                                               ctypes.c_void_p(stream.cuda_stream)))
+                    else:
+                        ctx.allreduce(b, ep, stream.cuda_stream)
+
                 for it in range(5):
                     epoch[key] += 1
-                    ctx.allreduce(b, epoch[key], stream.cuda_stream)
+                    launch(epoch[key])
                 torch.cuda.synchronize(); dist.barrier()
                 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 s.record(stream)
                 for it in range(iters):
                     epoch[key] += 1
-                    ctx.allreduce(b, epoch[key], stream.cuda_stream)
+                    launch(epoch[key])
                 e.record(stream); e.synchronize()
                 ctx.status()
                 t = torch.tensor(s.elapsed_time(e) / iters, device=dev)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 us = t.item() * 1e3
                 bus = 2 * (world - 1) / world * size / (us * 1e-6) / 1e9
-                rows.append(dict(impl="caramel", pattern=pat, depth=depth, ctas=ctas, bytes=size, us=round(us, 2), busbw=round(bus, 1)))
+                rows.append(dict(impl="caramel-" + engine, pattern=pat, depth=depth, ctas=ctas, bytes=size,
+                                 us=round(us, 2), busbw=round(bus, 1)))
         # NCCL
         x = buf[:n]
         for it in range(5):
