@@ -52,6 +52,7 @@ def parse_args():
     ap.add_argument("--no-exposed", action="store_true", help="skip the model fwd/bwd exposed-comm measurement")
     ap.add_argument("--batch", type=int, default=64, help="per-GPU batch for the exposed-comm measurement")
     ap.add_argument("--exposed-iters", type=int, default=10)
+    ap.add_argument("--no-sweep", action="store_true", help="skip the bucket-size sweep (N > 1)")
     return ap.parse_args()
 
 
@@ -426,6 +427,71 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist):
     return out
 
 
+SWEEP_SIZES = (4096, 65536, 1 << 20, 4 << 20, 16 << 20, 64 << 20, 256 << 20)
+
+
+def bucket_sweep(torch, dist, world, rank, dev, iters=20):
+    """Config 5: one bucket of S bytes, adaptive depth from the NVLink model,
+    two-shot over NVLink (caramel_allreduce, packed input, result in place)
+    vs torch.distributed.all_reduce (NCCL) on the same bytes.  Back-to-back
+    launches between two CUDA events, max over ranks; bus GB/s = 2(p-1)/p*S/t."""
+    import ctypes
+
+    from paper_2004_14020_b200 import _native as N
+    from paper_2004_14020_b200 import comm
+    from paper_2004_14020_b200.collective import adaptive_depth
+    from paper_2004_14020_b200.costmodel import NetworkModel, batching_threshold
+
+    thr = batching_threshold(NetworkModel(*NVLINK_MODEL))
+    big = max(SWEEP_SIZES)
+    region = max(N.bucket_layout(big // 4, d, N.SHUFFLE, world)[1] for d in (1, 8))
+    region = (region + (1 << 20)) // (1 << 20) * (1 << 20)
+    ctx = comm.Context(rank, world, arena_bytes=region + (32 << 20))
+    ctx.bootstrap()
+    base, _ = ctx.arena_ptrs(0)
+    comm._view_fp32(base, big // 4).normal_()
+    stream = torch.cuda.current_stream()
+    rows = []
+    for k, size in enumerate(SWEEP_SIZES):
+        n = size // 4
+        depth = adaptive_depth(size, thr)
+        ctas, _, _ = N.bucket_layout(n, depth, N.SHUFFLE, world)
+        b = comm.make_bucket(n, 0, region + k * (1 << 20), depth=depth, pattern=N.SHUFFLE, epilogue=N.EPI_SUM,
+                             flags=0, ctas=ctas)
+
+        def timed(fn):
+            for _ in range(5):
+                fn()
+            torch.cuda.synchronize()
+            dist.barrier()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            for _ in range(iters):
+                fn()
+            e.record(stream)
+            e.synchronize()
+            t = torch.tensor([s.elapsed_time(e) / iters], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return t.item() * 1e3  # us
+
+        ep = [0]
+
+        def caramel():
+            ep[0] += 1
+            ctx.allreduce(b, ep[0], stream.cuda_stream)
+
+        x = torch.empty(n, device=dev).normal_()
+        us_c = timed(caramel)
+        us_n = timed(lambda: dist.all_reduce(x))
+        bus = 2 * (world - 1) / world * size / 1e3
+        rows.append({"bytes": size, "depth": depth, "caramel_us": round(us_c, 2),
+                     "caramel_bus_gbs": round(bus / us_c, 1), "nccl_us": round(us_n, 2),
+                     "nccl_bus_gbs": round(bus / us_n, 1)})
+    ctx.status()
+    ctx.close()
+    return rows
+
+
 def run_caramel(args) -> int:
     import ctypes
 
@@ -572,6 +638,30 @@ def run_caramel(args) -> int:
                 "bus_gbs": round(plan.bus_bytes() / (nms * 1e-3) / 1e9, 1) if world > 1 else None,
                 "buckets": nb, "bucket_mib": 25}
 
+    # ---- calibrated network model (SURVEY §8f row 1, N > 1) --------------------
+    calibrated = None
+    if dist is not None:
+        from paper_2004_14020_b200.costmodel import batching_threshold
+        from paper_2004_14020_b200.executor import calibrate_network_model
+
+        model, meas = calibrate_network_model(world, rank)
+        from paper_2004_14020_b200 import gradsets as _gs
+        from paper_2004_14020_b200.collective import Pattern as _P, ReduceModel as _RM
+        from paper_2004_14020_b200.pipeline import run_pipeline as _rp
+        from paper_2004_14020_b200.sim import SimConfig as _SC
+
+        cal_art = _rp(_gs.layered_chain_dag(args.model),
+                      _SC(workers=world, network=model, reduce=_RM(*REDUCE_MODEL), pattern=_P(args.pattern)))
+        calibrated = {"latency_us": round(model.latency_us, 3), "per_byte_us": model.per_byte_us,
+                      "threshold_bytes": batching_threshold(model), "buckets": len(cal_art.batch_plan.groups),
+                      "samples": [[m.size_bytes, round(m.observed_time_us, 2)] for m in meas],
+                      "fit": "fit_network_model (costmodel.py:84-108) on caramel_allreduce 64 B / 4 MB, max over ranks"}
+
+    # ---- config 5: bucket-size sweep vs NCCL (N > 1) --------------------------
+    sweep = None
+    if dist is not None and not args.no_sweep:
+        sweep = bucket_sweep(torch, dist, world, rank, dev)
+
     # ---- exposed communication on the real model (T - C) --------------------
     exposed = None
     if not args.no_exposed:
@@ -619,6 +709,8 @@ def run_caramel(args) -> int:
         "bus_gbs": round(bus, 1) if bus is not None else None,
         "exposed_comm_ms_per_iter": exposed["caramel_exposed_ms"] if exposed else None,
         "exposed_comm": exposed,
+        "bucket_sweep": sweep,
+        "calibrated_network_model": calibrated,
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,

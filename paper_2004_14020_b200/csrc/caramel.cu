@@ -877,12 +877,32 @@ struct BucketRun {
   __device__ __forceinline__ const float* theta_flat() const {
     return arena ? reinterpret_cast<const float*>(E->parena[X.me] + B->param_off) : nullptr;
   }
-  // this CTA's tile of shard s of chunk c
+  // Chunk-parallel tiling: the bucket's G CTAs are split into `depth` groups,
+  // group c = CTAs [s_c, e_c) works on chunk c only (several chunks share a
+  // CTA when G < depth).  mine(c): does this CTA take part in chunk c, and as
+  // which tile of how many.
+  __device__ __forceinline__ bool mine(int c, int& jj, int& gg) const {
+    const int G = X.G, k = B->depth;
+    const int s0 = (int)(((int64_t)c * G) / k);
+    int e0 = (int)(((int64_t)(c + 1) * G) / k);
+    if (e0 <= s0) e0 = s0 + 1;
+    if (X.j < s0 || X.j >= e0) return false;
+    jj = X.j - s0;
+    gg = e0 - s0;
+    return true;
+  }
+  __device__ __forceinline__ bool mine(int c) const {
+    int a, b;
+    return mine(c, a, b);
+  }
+  // this CTA's tile of shard s of chunk c (only meaningful when mine(c))
   __device__ __forceinline__ void shard(int c, int s, uint64_t& lo, uint64_t& hi) const {
     const uint64_t n = B->numel;
     const int k = B->depth, p = X.world;
+    int jj = 0, gg = 1;
+    mine(c, jj, gg);
     uint64_t c0 = split_at(n, k, c), m = split_at(n, k, c + 1) - c0;
-    tile_of(c0 + split_at(m, p, s), c0 + split_at(m, p, s + 1), X.G, X.j, lo, hi);
+    tile_of(c0 + split_at(m, p, s), c0 + split_at(m, p, s + 1), gg, jj, lo, hi);
   }
 };
 
@@ -928,6 +948,7 @@ __device__ void phase_pack(const BucketRun& R) {
   const bool pack = R.B->flags & CARAMEL_F_PACK;
   float* mine = R.bucket(me);
   for (int c = 0; c < R.B->depth; ++c) {
+    if (!R.mine(c)) continue;
     if (pack) {
       for (int s = 0; s < p; ++s) {
         uint64_t lo, hi;
@@ -944,20 +965,117 @@ __device__ void phase_pack(const BucketRun& R) {
   }
 }
 
-// phase 2, two-shot: reduce own shard in rank order, epilogue, all-gather by store
+// Reduce + epilogue + all-gather of several ranges (this CTA's tile of my
+// shard in every chunk) as ONE flat vector loop: chunk boundaries cost no
+// extra memory round trip (2*NP 128-bit loads in flight per thread across
+// ranges).  Scalar heads/tails first.
+template <int NP>
+__device__ void rs_ag_multi(const Env& E, const caramel_bucket& B, bool arena, Cursor& tc, const uint64_t* lo,
+                            const uint64_t* hi, int nr, int me) {
+  const float* src[NP];
+  float* dst[NP];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    src[q] = reinterpret_cast<const float*>(E.arena[q] + B.bucket_off);
+    dst[q] = arena ? reinterpret_cast<float*>(E.parena[q] + B.param_off)
+                   : reinterpret_cast<float*>(E.arena[q] + B.bucket_off);
+  }
+  const float* th = arena ? reinterpret_cast<const float*>(E.parena[me] + B.param_off) : nullptr;
+  const int epi = B.epilogue;
+  const bool sgd = epi == CARAMEL_EPI_SGD;
+  uint64_t va[CARAMEL_MAX_DEPTH], vpre[CARAMEL_MAX_DEPTH + 1];
+  vpre[0] = 0;
+  for (int k = 0; k < nr; ++k) {
+    uint64_t a = (lo[k] + 3) & ~3ull, b = hi[k] & ~3ull;
+    if (a > hi[k]) a = hi[k];
+    if (b < a) b = a;
+    va[k] = a;
+    vpre[k + 1] = vpre[k] + (b - a) / 4;
+    // scalar head [lo, a) and tail [b, hi)
+    const uint64_t nh = a - lo[k], nt = hi[k] - b;
+    for (uint64_t e = threadIdx.x; e < nh + nt; e += blockDim.x) {
+      const uint64_t x = e < nh ? lo[k] + e : b + (e - nh);
+      float acc = ld1(src[0] + x);
+#pragma unroll
+      for (int q = 1; q < NP; ++q) acc = __fadd_rn(acc, ld1(src[q] + x));
+      const float t = sgd ? (arena ? ld1(th + x) : seg_ld1(tc, x, 1)) : 0.f;
+      const float o = epi1(epi, acc, t, B.scale, B.lr);
+#pragma unroll
+      for (int q = 0; q < NP; ++q) st1(dst[q] + x, o);
+    }
+  }
+  const uint64_t V = vpre[nr], T = blockDim.x;
+  auto pos = [&](uint64_t v) {  // flat vector index -> bucket element position
+    int k = 0;
+    while (v >= vpre[k + 1]) ++k;
+    return va[k] + 4 * (v - vpre[k]);
+  };
+  uint64_t v = threadIdx.x;
+  for (; v + T < V; v += 2 * T) {
+    const uint64_t x0 = pos(v), x1 = pos(v + T);
+    float4 p0[NP], p1[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      p0[q] = ld4(src[q] + x0);
+      p1[q] = ld4(src[q] + x1);
+    }
+    float4 t0 = make_float4(0.f, 0.f, 0.f, 0.f), t1 = t0;
+    if (sgd) {
+      t0 = arena ? ld4(th + x0) : seg_ld4(tc, x0, 1);
+      t1 = arena ? ld4(th + x1) : seg_ld4(tc, x1, 1);
+    }
+    float4 s0 = p0[0], s1 = p1[0];
+#pragma unroll
+    for (int q = 1; q < NP; ++q) {
+      s0 = add4(s0, p0[q]);
+      s1 = add4(s1, p1[q]);
+    }
+    const float4 o0 = epi4(epi, s0, t0, B.scale, B.lr), o1 = epi4(epi, s1, t1, B.scale, B.lr);
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      st4(dst[q] + x0, o0);
+      st4(dst[q] + x1, o1);
+    }
+  }
+  if (v < V) {
+    const uint64_t x0 = pos(v);
+    float4 s0 = ld4(src[0] + x0);
+#pragma unroll
+    for (int q = 1; q < NP; ++q) s0 = add4(s0, ld4(src[q] + x0));
+    float4 t0 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (sgd) t0 = arena ? ld4(th + x0) : seg_ld4(tc, x0, 1);
+    const float4 o0 = epi4(epi, s0, t0, B.scale, B.lr);
+#pragma unroll
+    for (int q = 0; q < NP; ++q) st4(dst[q] + x0, o0);
+  }
+}
+
+// phase 2, two-shot: reduce own shard in rank order, epilogue, all-gather by
+// store.  DEFER (ready flags published together): wait for every chunk, then
+// one flat pass over all chunks; otherwise chunk by chunk with per-chunk DONE.
 template <int NP, bool DEFER = false>
 __device__ void phase_shuffle(const BucketRun& R) {
   Cursor tc;
   cur_init(tc, R.segs, R.B->nseg);
+  if (DEFER) {
+    uint64_t lo[CARAMEL_MAX_DEPTH], hi[CARAMEL_MAX_DEPTH];
+    int nr = 0;
+    for (int c = 0; c < R.B->depth; ++c) {
+      if (!R.mine(c)) continue;
+      R.X.wait_all(c, SLOT_READY, R.X.epoch);
+      R.shard(c, R.X.me, lo[nr], hi[nr]);
+      ++nr;
+    }
+    rs_ag_multi<NP>(*R.E, *R.B, R.arena, tc, lo, hi, nr, R.X.me);
+    return;
+  }
   for (int c = 0; c < R.B->depth; ++c) {
+    if (!R.mine(c)) continue;
     R.X.wait_all(c, SLOT_READY, R.X.epoch);
     uint64_t lo, hi;
     R.shard(c, R.X.me, lo, hi);
-    const float* srcs[NP];  // pull: every rank's packed bucket, in place
-#pragma unroll
-    for (int q = 0; q < NP; ++q) srcs[q] = R.bucket(q);
-    rs_ag_range<NP>(*R.E, *R.B, R.arena, tc, lo, hi, R.X.me, srcs);
-    if (!DEFER) R.X.publish_all(c, SLOT_DONE);
+    rs_ag_multi<NP>(*R.E, *R.B, R.arena, tc, &lo, &hi, 1, R.X.me);
+    R.X.publish_all(c, SLOT_DONE);
   }
 }
 
@@ -969,6 +1087,7 @@ __device__ void phase_ring(const BucketRun& R) {
   cur_init(tc, R.segs, R.B->nseg);
   const float* th = R.theta_flat();
   for (int c = 0; c < R.B->depth; ++c) {
+    if (!R.mine(c)) continue;
     // reduce-scatter: at step t rank r folds its own share of shard
     // (r-1-t) mod p into the left neighbour's running sum (the chain of
     // shard s starts at rank s+1 and ends at its owner s)
@@ -1007,6 +1126,7 @@ __device__ void phase_hd(const BucketRun& R) {
   cur_init(tc, R.segs, R.B->nseg);
   const float* th = R.theta_flat();
   for (int c = 0; c < R.B->depth; ++c) {
+    if (!R.mine(c)) continue;
     // vector halving, distance halving: round i pairs r with r ^ (p >> (i+1));
     // r keeps the half of its active block range that contains block r and
     // sums it as (lower rank's value) + (higher rank's value)
@@ -1086,7 +1206,7 @@ __device__ void phase_ll_scatter(const BucketRun& R) {
   Cursor gc;
   cur_init(gc, R.segs, R.B->nseg);
   for (int c = 0; c < R.B->depth; ++c)
-    for (int s = 0; s < p; ++s) {
+    for (int s = 0; s < p && R.mine(c); ++s) {
       uint64_t lo, hi;
       R.shard(c, s, lo, hi);
       uint64_t* dst = ll_in(R, s, me);
@@ -1110,6 +1230,7 @@ __device__ void phase_ll_reduce(const BucketRun& R) {
   const bool sgd = R.B->epilogue == CARAMEL_EPI_SGD;
   const uint32_t ep = R.X.epoch;
   for (int c = 0; c < R.B->depth; ++c) {
+    if (!R.mine(c)) continue;
     uint64_t lo, hi;
     R.shard(c, me, lo, hi);
     const uint64_t T = blockDim.x;
@@ -1153,7 +1274,7 @@ __device__ void phase_ll_finish(const BucketRun& R) {
   const uint32_t ep = R.X.epoch;
   const uint64_t T = blockDim.x;
   for (int c = 0; c < R.B->depth; ++c)
-    for (int s = 0; s < p; ++s) {
+    for (int s = 0; s < p && R.mine(c); ++s) {
       uint64_t lo, hi;
       R.shard(c, s, lo, hi);
       for (uint64_t x0 = lo + threadIdx.x; x0 < hi; x0 += 4 * LL_U * T) {
@@ -1179,12 +1300,13 @@ template <int PAT>
 __device__ void phase_finish(const BucketRun& R) {
   const int me = R.X.me, p = R.X.world;
   if (PAT == CARAMEL_SHUFFLE)
-    for (int c = 0; c < R.B->depth; ++c) R.X.wait_all(c, SLOT_DONE, R.X.epoch);
+    for (int c = 0; c < R.B->depth; ++c)
+      if (R.mine(c)) R.X.wait_all(c, SLOT_DONE, R.X.epoch);
   if ((R.B->flags & CARAMEL_F_UNPACK) && !R.arena) {
     const bool to_param = (R.B->epilogue == CARAMEL_EPI_SGD);
     const float* res = R.out(me);
     for (int c = 0; c < R.B->depth; ++c) {
-      for (int s = 0; s < p; ++s) {
+      for (int s = 0; s < p && R.mine(c); ++s) {
         uint64_t lo, hi;
         R.shard(c, s, lo, hi);
         unpack_range(R.segs, R.B->nseg, res, lo, hi, to_param, *R.tab);
@@ -1212,7 +1334,7 @@ __device__ __forceinline__ void publish_chunks(const BucketRun& R, int slot) {
     fence_acq_rel_sys();
     const int p = R.X.world;
     for (int idx = threadIdx.x; idx < R.B->depth * p; idx += 32)
-      st_relaxed_sys(R.X.flag(idx % p, idx / p, slot, R.X.me), R.X.epoch);
+      if (R.mine(idx / p)) st_relaxed_sys(R.X.flag(idx % p, idx / p, slot, R.X.me), R.X.epoch);
   }
 }
 
@@ -1605,8 +1727,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_collective_many(const __grid_con
           base = (base + B.ctas) % G;
           if (j < 0 || B.numel == 0 || use_ll(PAT, p, B.numel)) continue;
           const int ns = nslots(PAT, p);
+          BucketRun R;
+          make_run(R, E, B, PAT, lr_idx, epoch, j);
           for (int idx = threadIdx.x; idx < B.depth * p; idx += 32) {
             const int c = idx / p, q = idx % p;
+            if (!R.mine(c)) continue;
             uint32_t* f = reinterpret_cast<uint32_t*>(E.arena[q] + B.flag_off) +
                           ((((uint64_t)c * B.ctas + j) * ns + slot) * p + me);
             st_relaxed_sys(f, epoch);
@@ -1724,6 +1849,7 @@ int caramel_bucket_layout(uint64_t numel, int depth, int pattern, int world, int
     uint64_t cap = (uint64_t)default_max_ctas();
     if (g > cap) g = cap;
   }
+  if (world > 1 && g < (uint64_t)depth) g = depth;  // chunk-parallel: at least one CTA per chunk
   if (g < 1) g = 1;
   if (ctas) *ctas = (int32_t)g;
   if (bucket_bytes) {

@@ -357,3 +357,57 @@ class Aggregator:
     def close(self) -> None:
         self.detach_hooks()
         self.ctx.close()
+
+
+def calibrate_network_model(world: int, rank: int, sizes: tuple[int, ...] = (64, 4 << 20), reps: int = 8,
+                            iters: int = 20, group=None):
+    """Fit f(d) = latency + per_byte * d on THIS fabric.
+
+    Times the sm_100a two-shot (caramel_allreduce, adaptive-sized buckets at
+    depth 1) on `sizes` -- the paper's 64 B and 4 MB microbenchmarks
+     -- `reps` times each, `iters` back-to-back launches per
+    sample, takes the max over ranks of every sample (so every rank fits the
+    identical model and plans identical buckets) and applies the reference's
+    least-squares fit, fit_network_model (costmodel.py:84-108).  Returns
+    (NetworkModel, measurements)."""
+    import torch.distributed as dist
+
+    from .costmodel import Measurement, fit_network_model
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    nmax = max(sizes) // 4 + 1
+    _, bbytes, fbytes = N.bucket_layout(nmax, 1, N.SHUFFLE, world)
+    flag_off = _align(bbytes)
+    ctx = comm.Context(rank, world, arena_bytes=flag_off + 4 * _align(fbytes, 1 << 20) * len(sizes))
+    if world > 1:
+        ctx.bootstrap(group)
+    stream = torch.cuda.current_stream(dev)
+    meas = []
+    epoch = {}
+    for k, size in enumerate(sizes):
+        n = max(1, size // 4)
+        ctas, _, fb = N.bucket_layout(n, 1, N.SHUFFLE, world)
+        b = comm.make_bucket(n, 0, flag_off + k * _align(fbytes, 1 << 20), depth=1, pattern=N.SHUFFLE,
+                             epilogue=N.EPI_SUM, flags=0, ctas=ctas)
+        epoch[k] = 0
+        for r in range(reps + 1):
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier(group=group)
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            for _ in range(iters):
+                epoch[k] += 1
+                ctx.allreduce(b, epoch[k], stream.cuda_stream)
+            e.record(stream)
+            e.synchronize()
+            us = s.elapsed_time(e) * 1e3 / iters
+            if world > 1:
+                t = torch.tensor([us], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+                us = t.item()
+            if r > 0:  # first round warms up
+                meas.append(Measurement(size_bytes=4 * n, observed_time_us=us))
+    ctx.status()
+    ctx.close()
+    return fit_network_model(meas), meas
