@@ -147,7 +147,8 @@ class Aggregator:
     """
 
     def __init__(self, plan: ExecPlan, params: dict[str, torch.Tensor], *, rank: int = 0, lr: float = 0.01,
-                 epilogue: str = "sgd", param_arena: bool = True, group=None, bootstrap: bool = True):
+                 epilogue: str = "sgd", param_arena: bool = True, grad_arena: bool = True, group=None,
+                 bootstrap: bool = True):
         self.plan = plan
         self.rank, self.world = rank, plan.world
         self.lr = float(lr)
@@ -170,6 +171,17 @@ class Aggregator:
             self.ctx.bootstrap(group)
         if self.param_arena:
             self._adopt_params()
+        # gradients: views into one flat buffer with the parameter arena's layout
+        # (bucket order; gradient_as_bucket_view style), so host staging and
+        # packing touch contiguous memory
+        self.grad_flat = None
+        if grad_arena:
+            self.grad_flat = torch.zeros(plan.param_bytes // 4, device=dev)
+            for b in plan.buckets:
+                off = b.param_off // 4
+                for pid, n in zip(b.param_ids, b.numels):
+                    params[pid].grad = self.grad_flat[off:off + n].view(params[pid].shape)
+                    off += n
         for p in params.values():
             if p.grad is None:
                 p.grad = torch.zeros_like(p)
@@ -267,6 +279,92 @@ class Aggregator:
                                                self._dev_segprefix.data_ptr() + 8 * i, ctas, mode, 0,
                                                ctypes.c_void_p(stream)))
         self.launches += 1
+
+    def host_groups(self, group_bytes: int = 16 << 20) -> list[tuple[int, int]]:
+        """Consecutive launch-order bucket ranges of about `group_bytes` each
+        (identical on every rank)."""
+        out, i = [], 0
+        while i < len(self._live):
+            j, acc = i, 0
+            while j < len(self._live) and (j == i or acc + 4 * self._live[j].spec.numel <= group_bytes):
+                acc += 4 * self._live[j].spec.numel
+                j += 1
+            out.append((i, j))
+            i = j
+        return out
+
+    def flat_layout(self) -> list[tuple[str, int, int]]:
+        """(param id, element offset, numel) of every parameter in the flat
+        arena layout used by step_host_flat (bucket order, 256 B aligned buckets)."""
+        out = []
+        for b in self.plan.buckets:
+            off = b.param_off // 4
+            for pid, n in zip(b.param_ids, b.numels):
+                out.append((pid, off, n))
+                off += n
+        return out
+
+    def step_host_flat(self, host_grads: torch.Tensor, host_params: torch.Tensor | None = None,
+                       group_bytes: int = 16 << 20) -> int:
+        """step_host for flat pinned buffers in the arena layout (flat_layout()):
+        one H2D and one D2H cudaMemcpyAsync per group of buckets, overlapped
+        with the group's aggregation kernel."""
+        if self.grad_flat is None or not self.param_arena:
+            raise RuntimeError("step_host_flat needs grad_arena=True and the parameter arena")
+        cur = torch.cuda.current_stream(self.device)
+        if not hasattr(self, "_h2d"):
+            self._h2d = torch.cuda.Stream(device=self.device)
+            self._d2h = torch.cuda.Stream(device=self.device)
+        h2d, d2h = self._h2d, self._d2h
+        pflat = self.ctx.arena_view(0, 0, self.plan.param_bytes // 4, param=True)
+        h2d.wait_stream(cur)
+        N.check(N.lib().caramel_epoch_advance(self.ctx._ctx, ctypes.c_void_p(cur.cuda_stream)))
+        launches = 1
+        for i, j in self.host_groups(group_bytes):
+            a = self._live[i].spec.param_off // 4
+            last = self._live[j - 1].spec
+            b = last.param_off // 4 + last.numel
+            with torch.cuda.stream(h2d):
+                self.grad_flat[a:b].copy_(host_grads[a:b], non_blocking=True)
+            cur.wait_stream(h2d)
+            self._launch_range(i, j, cur.cuda_stream, N.MANY_FUSED, 0)
+            launches += 1
+            if host_params is not None:
+                d2h.wait_stream(cur)
+                with torch.cuda.stream(d2h):
+                    host_params[a:b].copy_(pflat[a:b], non_blocking=True)
+        cur.wait_stream(d2h)
+        return launches
+
+    def step_host(self, host_grads: dict, host_params: dict | None = None, group_bytes: int = 16 << 20) -> int:
+        """The plugin path with HOST buffers: pinned host gradients -> device,
+        aggregation + fused update, updated parameters -> pinned host, pipelined
+        per group of buckets on two copy streams so H2D of group i+1, the
+        collective of group i and D2H of group i-1 overlap (PCIe is full
+        duplex).  Returns the number of kernels launched."""
+        cur = torch.cuda.current_stream(self.device)
+        if not hasattr(self, "_h2d"):
+            self._h2d = torch.cuda.Stream(device=self.device)
+            self._d2h = torch.cuda.Stream(device=self.device)
+        h2d, d2h = self._h2d, self._d2h
+        h2d.wait_stream(cur)
+        N.check(N.lib().caramel_epoch_advance(self.ctx._ctx, ctypes.c_void_p(cur.cuda_stream)))
+        launches = 1
+        for i, j in self.host_groups(group_bytes):
+            members = [pid for lv in self._live[i:j] for pid in lv.members]
+            with torch.cuda.stream(h2d):
+                for pid in members:
+                    self.params[pid].grad.view(-1).copy_(host_grads[pid], non_blocking=True)
+            cur.wait_stream(h2d)
+            self._launch_range(i, j, cur.cuda_stream, N.MANY_FUSED, 0)
+            launches += 1
+            if host_params is not None:
+                d2h.wait_stream(cur)
+                with torch.cuda.stream(d2h):
+                    for pid in members:
+                        host_params[pid].copy_(self.params[pid].view(-1), non_blocking=True)
+        cur.wait_stream(d2h)
+        return launches
 
     def kernels_per_step(self, fused: bool = True) -> int:
         return 2 if fused else 1 + len(self._live)

@@ -108,3 +108,43 @@ def test_gradient_mean_mode_writes_back_grads():
     for k, p in params.items():
         assert torch.equal(p.grad, want[k])
     agg.close()
+
+
+def test_step_host_pipelined_matches_sgd():
+    from paper_2004_14020_b200.executor import Aggregator
+
+    lr = 0.1
+    model = _tiny_model(3)
+    plan, params = _plan_for(model)
+    agg = Aggregator(plan, params, lr=lr, epilogue="sgd")
+    theta0 = {k: v.detach().cpu().clone() for k, v in params.items()}
+    host_g = {k: torch.randn(v.numel()).pin_memory() for k, v in params.items()}
+    host_p = {k: torch.empty(v.numel()).pin_memory() for k, v in params.items()}
+    n = agg.step_host(host_g, host_p, group_bytes=4096)  # several groups
+    torch.cuda.synchronize()
+    assert n >= 3
+    for k in params:
+        want = theta0[k].view(-1) - lr * host_g[k]
+        assert torch.equal(host_p[k], want), k
+        assert torch.equal(params[k].detach().cpu().view(-1), want)
+    agg.close()
+
+
+def test_step_host_flat_matches_sgd():
+    from paper_2004_14020_b200.executor import Aggregator
+
+    lr = 0.1
+    model = _tiny_model(4)
+    plan, params = _plan_for(model)
+    agg = Aggregator(plan, params, lr=lr, epilogue="sgd")
+    theta0 = {k: v.detach().cpu().clone().view(-1) for k, v in params.items()}
+    hg = torch.zeros(plan.param_bytes // 4).pin_memory()
+    hp = torch.zeros(plan.param_bytes // 4).pin_memory()
+    layout = agg.flat_layout()
+    for pid, off, n in layout:
+        hg[off:off + n].normal_()
+    agg.step_host_flat(hg, hp, group_bytes=4096)
+    torch.cuda.synchronize()
+    for pid, off, n in layout:
+        assert torch.equal(hp[off:off + n], theta0[pid] - lr * hg[off:off + n]), pid
+    agg.close()
