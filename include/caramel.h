@@ -56,6 +56,10 @@ extern "C" {
                                     into .grad for SUM/SCALE, .param for SGD   */
 #define CARAMEL_F_PARAM_ARENA 4u /* SGD result is stored straight into every
                                     rank's symmetric parameter arena            */
+#define CARAMEL_F_FLAT 8u        /* caller asserts: the members form ONE
+                                    contiguous, 16-byte aligned gradient segment
+                                    (nseg == 1) -- enables the TMA bulk-copy
+                                    streaming path                              */
 
 /* One member tensor of a fusion bucket.  Members are listed in bucket order
  * (BatchGroup.param_ids, batching.py:28-33) with contiguous offsets. */

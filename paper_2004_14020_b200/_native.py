@@ -17,7 +17,7 @@ HEADER = HERE.parent / "include" / "caramel.h"
 
 RING, HD, SHUFFLE = 0, 1, 2
 EPI_SUM, EPI_SCALE, EPI_SGD = 0, 1, 2
-F_PACK, F_UNPACK, F_PARAM_ARENA = 1, 2, 4
+F_PACK, F_UNPACK, F_PARAM_ARENA, F_FLAT = 1, 2, 4, 8
 MANY_FUSED, MANY_FLAGS = 0, 1
 MAX_RANKS = 8
 MAX_DEPTH = 8

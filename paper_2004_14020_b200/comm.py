@@ -37,6 +37,22 @@ def segment_table(per_rank: list[list[SegmentSpec]], device) -> torch.Tensor:
     return host.to(device)
 
 
+def coalesce(segs: list[SegmentSpec]) -> list[SegmentSpec]:
+    """Merge runs of members that are contiguous in memory (gradient AND
+    parameter addresses continue where the previous member ends): the packed
+    bucket is unchanged, the kernels just see fewer, longer pieces."""
+    out: list[SegmentSpec] = []
+    for s in segs:
+        if out:
+            t = out[-1]
+            if (t.offset + t.numel == s.offset and t.grad and s.grad == t.grad + 4 * t.numel
+                    and ((not t.param and not s.param) or (t.param and s.param == t.param + 4 * t.numel))):
+                out[-1] = SegmentSpec(t.grad, t.param, t.offset, t.numel + s.numel)
+                continue
+        out.append(s)
+    return out
+
+
 def segments_for(tensors: list[torch.Tensor], params: list[torch.Tensor] | None = None) -> list[SegmentSpec]:
     """Segment list for tensors laid out back to back in bucket order."""
     out = []

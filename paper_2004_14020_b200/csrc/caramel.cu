@@ -1380,11 +1380,23 @@ __global__ void __launch_bounds__(THREADS, 1) k_collective(const __grid_constant
 // over the grid; a tile's pieces may come from several buckets and are all
 // described in one batch (prefix[0..nb] element prefix sums, prefix[nb+1 ..
 // 2nb+1] member-segment prefix sums).
+#define SMEM_PREFIX 512
 __global__ void __launch_bounds__(THREADS, 2) k_local_many(const __grid_constant__ MParams P) {
   const int lr_idx = blockIdx.y;
   const Env E = P.env;
-  const uint64_t* pre = P.prefix;
-  const uint64_t* spre = P.segprefix;
+  // prefix arrays in shared memory (the binary searches below are otherwise
+  // chains of dependent global loads at the start of every CTA)
+  __shared__ uint64_t s_pre[SMEM_PREFIX + 1], s_spre[SMEM_PREFIX + 1];
+  const bool cached = P.nb <= SMEM_PREFIX;
+  if (cached) {
+    for (int i = threadIdx.x; i <= P.nb; i += blockDim.x) {
+      s_pre[i] = P.prefix[i];
+      s_spre[i] = P.segprefix[i];
+    }
+    __syncthreads();
+  }
+  const uint64_t* pre = cached ? s_pre : P.prefix;
+  const uint64_t* spre = cached ? s_spre : P.segprefix;
   uint64_t lo, hi;
   tile_of(pre[0], pre[P.nb], gridDim.x, blockIdx.x, lo, hi);
   if (lo >= hi) return;
@@ -1683,6 +1695,169 @@ __global__ void __launch_bounds__(THREADS, 1) k_shuffle_fused(const __grid_const
       }, g_tab);
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// TMA bulk-copy streaming (world == 1, flat buckets): one CTA per SM, tiles of
+// TT floats staged in shared memory by cp.async.bulk (completion on an
+// mbarrier), the update computed in shared memory, the new parameters written
+// back with a bulk store -- bytes in flight live in shared memory, not in
+// registers, so a handful of warps keep HBM busy.
+// ---------------------------------------------------------------------------
+#define TT 4096  // floats per tile (16 KB)
+#define TS 6     // pipeline stages: 5 tiles (160 KB) in flight per SM
+#define TMA_THREADS 256
+#define TMA_MAX_BUCKETS 256
+
+struct TmaBucket {  // per-bucket pointers cached in shared memory
+  const float* g;
+  float* t;
+  uint64_t numel;
+  float scale, lr;
+};
+
+struct TmaSmem {
+  float g[TS][TT];
+  float t[TS][TT];
+  uint64_t bar[TS];
+  uint32_t tpre[TMA_MAX_BUCKETS + 1];
+  TmaBucket b[TMA_MAX_BUCKETS];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(sdst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// world == 1, every bucket CARAMEL_F_FLAT + PACK + PARAM_ARENA + SGD:
+// theta[b] <- theta[b] - lr * (grad[b] * scale), tile by tile.
+__global__ void __launch_bounds__(TMA_THREADS, 1) k_local_flat_tma(const __grid_constant__ MParams P) {
+  extern __shared__ __align__(128) unsigned char dyn_smem[];
+  TmaSmem& S = *reinterpret_cast<TmaSmem*>(dyn_smem);
+  const Env E = P.env;
+  const int me = E.rank_base + blockIdx.y;
+  // tile prefix over the buckets
+  uint32_t carry = 0;
+  __shared__ uint32_t scan_scratch[32];
+  for (int b0 = 0; b0 < P.nb; b0 += blockDim.x) {
+    const int i = b0 + threadIdx.x;
+    uint32_t cnt = 0;
+    if (i < P.nb) {
+      const caramel_bucket B = P.bs[i];
+      cnt = (uint32_t)((B.numel + TT - 1) / TT);
+      const caramel_segment* segs = reinterpret_cast<const caramel_segment*>(B.segs) + (uint64_t)blockIdx.y * B.nseg;
+      S.b[i].g = reinterpret_cast<const float*>(__ldg(reinterpret_cast<const unsigned long long*>(segs)));
+      S.b[i].t = reinterpret_cast<float*>(E.parena[me] + B.param_off);
+      S.b[i].numel = B.numel;
+      S.b[i].scale = B.scale;
+      S.b[i].lr = B.lr;
+    }
+    uint32_t excl;
+    const uint32_t tot = block_scan(cnt, &excl, scan_scratch);
+    if (i < P.nb) S.tpre[i] = carry + excl;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    S.tpre[P.nb] = carry;
+    for (int s = 0; s < TS; ++s) mbar_init(&S.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t T = carry, G = gridDim.x;
+  // tile t -> bucket, element offset, length, global pointers
+  struct Tile {
+    const float* g;
+    float* t;
+    uint32_t len;
+    float scale, lr;
+  };
+  auto tile = [&](uint32_t t) {
+    int a = 0, b = P.nb - 1;
+    while (a < b) {
+      const int m = (a + b + 1) >> 1;
+      if (S.tpre[m] <= t) a = m; else b = m - 1;
+    }
+    const TmaBucket& B = S.b[a];
+    const uint64_t o = (uint64_t)(t - S.tpre[a]) * TT;
+    Tile r;
+    r.g = B.g + o;
+    r.t = B.t + o;
+    r.len = (uint32_t)((B.numel - o) < TT ? (B.numel - o) : TT);
+    r.scale = B.scale;
+    r.lr = B.lr;
+    return r;
+  };
+  auto issue = [&](uint32_t k) {  // thread 0 only
+    const uint32_t t = blockIdx.x + k * G;
+    if (t >= T) return;
+    const Tile r = tile(t);
+    const int s = k % TS;
+    const uint32_t vb = (r.len & ~3u) * 4;
+    mbar_expect_tx(&S.bar[s], 2 * vb);
+    if (vb) {
+      bulk_load(S.g[s], r.g, vb, &S.bar[s]);
+      bulk_load(S.t[s], r.t, vb, &S.bar[s]);
+    }
+  };
+  const uint32_t K = blockIdx.x < T ? (T - blockIdx.x + G - 1) / G : 0;
+  // prefetch distance TS-2: the stage refilled at iteration k held tile k-2,
+  // whose bulk store must have finished reading shared memory; the store of
+  // tile k-1 may still be in flight (wait_group.read 1)
+  if (threadIdx.x == 0)
+    for (uint32_t k = 0; k + 2 < TS && k < K; ++k) issue(k);
+  for (uint32_t k = 0; k < K; ++k) {
+    if (threadIdx.x == 0 && k + TS - 2 < K) {
+      bulk_wait_read1();
+      issue(k + TS - 2);
+    }
+    const int s = k % TS;
+    mbar_wait(&S.bar[s], (k / TS) & 1);
+    const Tile r = tile(blockIdx.x + k * G);
+    const uint32_t nv = r.len & ~3u;
+    float4* t4 = reinterpret_cast<float4*>(S.t[s]);
+    const float4* g4 = reinterpret_cast<const float4*>(S.g[s]);
+    for (uint32_t v = threadIdx.x; v < nv / 4; v += blockDim.x)
+      t4[v] = epi4(CARAMEL_EPI_SGD, g4[v], t4[v], r.scale, r.lr);
+    for (uint32_t e = nv + threadIdx.x; e < r.len; e += blockDim.x)  // < 4 ragged elements
+      r.t[e] = epi1(CARAMEL_EPI_SGD, ld1(r.g + e), ld1(r.t + e), r.scale, r.lr);
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0 && nv) {
+      bulk_store(r.t, S.t[s], nv * 4);
+      bulk_commit();
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
 }
 
 // Many buckets in one launch (launch order).  world == 1: the concatenated
@@ -2186,7 +2361,8 @@ int caramel_allreduce_many(caramel_ctx* c, const caramel_bucket* host, int32_t c
   int gmax = 1;
   uint64_t total = 0;
   for (int i = 0; i < count; ++i) {
-    if (host[i].pattern != pattern || host[i].epilogue != host[0].epilogue || host[i].flags != host[0].flags)
+    if (host[i].pattern != pattern || host[i].epilogue != host[0].epilogue ||
+        (host[i].flags & ~CARAMEL_F_FLAT) != (host[0].flags & ~CARAMEL_F_FLAT))
       return set_err(CARAMEL_EINVAL, "allreduce_many: buckets must share pattern, epilogue and flags");
     int rc = validate_bucket(c, &host[i]);
     if (rc) return rc;
@@ -2195,8 +2371,9 @@ int caramel_allreduce_many(caramel_ctx* c, const caramel_bucket* host, int32_t c
   }
   if (total == 0) return 0;
   if (c->world == 1) {
+    // one wave at 2 CTAs per SM (per-CTA setup is paid once per SM slot)
     uint64_t g = (total + (uint64_t)THREADS * 16 - 1) / ((uint64_t)THREADS * 16);
-    uint64_t cap = (uint64_t)c->sms * 4;
+    uint64_t cap = (uint64_t)c->sms * 2;
     gmax = (int)(g < 1 ? 1 : (g > cap ? cap : g));
   }
   MParams P;
@@ -2206,6 +2383,20 @@ int caramel_allreduce_many(caramel_ctx* c, const caramel_bucket* host, int32_t c
   P.segprefix = reinterpret_cast<const uint64_t*>(dev_segprefix);
   P.nb = count;
   mfn_t fn;
+  bool flat_tma = c->world == 1 && c->nlocal == 1 && count <= TMA_MAX_BUCKETS && !getenv("CARAMEL_NO_TMA");
+  for (int i = 0; i < count && flat_tma; ++i)
+    flat_tma = (host[i].flags & CARAMEL_F_FLAT) && (host[i].flags & CARAMEL_F_PACK) &&
+               (host[i].flags & CARAMEL_F_PARAM_ARENA) && host[i].epilogue == CARAMEL_EPI_SGD && host[i].nseg == 1;
+  if (flat_tma) {
+    static bool attr = false;
+    if (!attr) {
+      CUDA_TRY(cudaFuncSetAttribute(k_local_flat_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(TmaSmem)));
+      attr = true;
+    }
+    k_local_flat_tma<<<dim3(c->sms, 1), TMA_THREADS, sizeof(TmaSmem), (cudaStream_t)stream>>>(P);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
   if (c->world == 1) fn = k_local_many;
   else if (pattern == CARAMEL_SHUFFLE && mode == CARAMEL_MANY_FLAGS) {
     fn = pick_np_many<CARAMEL_SHUFFLE>(c->world);

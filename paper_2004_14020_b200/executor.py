@@ -211,10 +211,12 @@ class Aggregator:
                 off += 4 * n
 
     def _make_live(self, b: ExecBucket) -> _Live:
-        segs = comm.segments_for([self.params[p].grad for p in b.param_ids],
-                                 None if self.param_arena else [self.params[p] for p in b.param_ids])
+        segs = comm.coalesce(comm.segments_for([self.params[p].grad for p in b.param_ids],
+                                               None if self.param_arena else [self.params[p] for p in b.param_ids]))
         table = comm.segment_table([segs], self.device)
         flags = N.F_PACK | (N.F_PARAM_ARENA if self.param_arena else N.F_UNPACK)
+        if len(segs) == 1 and segs[0].grad % 16 == 0:
+            flags |= N.F_FLAT  # one contiguous aligned gradient run: TMA streaming path
         scale = 1.0 / self.world
         desc = comm.make_bucket(b.numel, b.bucket_off, b.flag_off, depth=b.depth, pattern=self.plan.pattern,
                                 epilogue=self.epi, flags=flags, ctas=b.ctas, segs=table, nseg=len(segs),
@@ -231,7 +233,7 @@ class Aggregator:
         prefix, segpre = [0], [0]
         for lv in self._live:
             prefix.append(prefix[-1] + lv.spec.numel)
-            segpre.append(segpre[-1] + len(lv.members))
+            segpre.append(segpre[-1] + lv.desc.nseg)
         self._prefix = prefix
         self._dev_prefix = torch.tensor(prefix, dtype=torch.int64, device=self.device)
         self._dev_segprefix = torch.tensor(segpre, dtype=torch.int64, device=self.device)
@@ -245,11 +247,13 @@ class Aggregator:
     def check_tables(self) -> bool:
         """True if every gradient still lives where the segment tables point."""
         for lv in self._live:
-            rows = lv.table.view(-1, 4).cpu()
-            for i, pid in enumerate(lv.members):
-                g = self.params[pid].grad
-                if g is None or int(rows[i, 0]) != g.data_ptr():
-                    return False
+            segs = comm.coalesce(comm.segments_for([self.params[p].grad for p in lv.members],
+                                                   None if self.param_arena else
+                                                   [self.params[p] for p in lv.members]))
+            rows = lv.table.view(-1, 4).cpu().tolist()[:len(segs)]
+            if len(segs) != lv.desc.nseg or [list(map(int, r)) for r in rows] != \
+                    [[s_.grad, s_.param, s_.offset, s_.numel] for s_ in segs]:
+                return False
         return True
 
     # -- launches --------------------------------------------------------------

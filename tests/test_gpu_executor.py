@@ -148,3 +148,19 @@ def test_step_host_flat_matches_sgd():
     for pid, off, n in layout:
         assert torch.equal(hp[off:off + n], theta0[pid] - lr * hg[off:off + n]), pid
     agg.close()
+
+
+def test_tables_track_gradient_storage():
+    from paper_2004_14020_b200.executor import Aggregator
+
+    model = _tiny_model(5)
+    plan, params = _plan_for(model)
+    agg = Aggregator(plan, params, lr=0.1, epilogue="sgd")
+    assert agg.check_tables()
+    # coalesced: with the flat gradient buffer every bucket is one contiguous piece
+    assert all(lv.desc.nseg == 1 for lv in agg._live)
+    next(iter(params.values())).grad = torch.zeros_like(next(iter(params.values())))
+    assert not agg.check_tables()
+    agg.refresh_tables()
+    assert agg.check_tables()
+    agg.close()
