@@ -1775,8 +1775,12 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) k_local_flat_tma(const __grid_
     if (i < P.nb) {
       const caramel_bucket B = P.bs[i];
       cnt = (uint32_t)((B.numel + TT - 1) / TT);
-      const caramel_segment* segs = reinterpret_cast<const caramel_segment*>(B.segs) + (uint64_t)blockIdx.y * B.nseg;
-      S.b[i].g = reinterpret_cast<const float*>(__ldg(reinterpret_cast<const unsigned long long*>(segs)));
+      if (B.flags & CARAMEL_F_PACK) {
+        const caramel_segment* segs = reinterpret_cast<const caramel_segment*>(B.segs) + (uint64_t)blockIdx.y * B.nseg;
+        S.b[i].g = reinterpret_cast<const float*>(__ldg(reinterpret_cast<const unsigned long long*>(segs)));
+      } else {
+        S.b[i].g = reinterpret_cast<const float*>(E.arena[me] + B.bucket_off);
+      }
       S.b[i].t = reinterpret_cast<float*>(E.parena[me] + B.param_off);
       S.b[i].numel = B.numel;
       S.b[i].scale = B.scale;
@@ -2384,9 +2388,10 @@ int caramel_allreduce_many(caramel_ctx* c, const caramel_bucket* host, int32_t c
   P.nb = count;
   mfn_t fn;
   bool flat_tma = c->world == 1 && c->nlocal == 1 && count <= TMA_MAX_BUCKETS && !getenv("CARAMEL_NO_TMA");
-  for (int i = 0; i < count && flat_tma; ++i)
-    flat_tma = (host[i].flags & CARAMEL_F_FLAT) && (host[i].flags & CARAMEL_F_PACK) &&
-               (host[i].flags & CARAMEL_F_PARAM_ARENA) && host[i].epilogue == CARAMEL_EPI_SGD && host[i].nseg == 1;
+  for (int i = 0; i < count && flat_tma; ++i)  // packed from one flat run, or already in the bucket
+    flat_tma = (((host[i].flags & CARAMEL_F_FLAT) && (host[i].flags & CARAMEL_F_PACK) && host[i].nseg == 1) ||
+                !(host[i].flags & CARAMEL_F_PACK)) &&
+               (host[i].flags & CARAMEL_F_PARAM_ARENA) && host[i].epilogue == CARAMEL_EPI_SGD;
   if (flat_tma) {
     static bool attr = false;
     if (!attr) {

@@ -147,7 +147,7 @@ class Aggregator:
     """
 
     def __init__(self, plan: ExecPlan, params: dict[str, torch.Tensor], *, rank: int = 0, lr: float = 0.01,
-                 epilogue: str = "sgd", param_arena: bool = True, grad_arena: bool = True, group=None,
+                 epilogue: str = "sgd", param_arena: bool = True, grads: str = "flat", group=None,
                  bootstrap: bool = True):
         self.plan = plan
         self.rank, self.world = rank, plan.world
@@ -171,16 +171,32 @@ class Aggregator:
             self.ctx.bootstrap(group)
         if self.param_arena:
             self._adopt_params()
-        # gradients: views into one flat buffer with the parameter arena's layout
-        # (bucket order; gradient_as_bucket_view style), so host staging and
-        # packing touch contiguous memory
+        # Gradient storage:
+        #   "flat"   views into one flat buffer with the parameter arena's layout
+        #            (bucket order, gradient_as_bucket_view style): the pack kernel
+        #            gathers contiguous runs, host staging is one copy per group
+        #   "bucket" zero-copy: views into the symmetric bucket arena itself --
+        #            autograd writes every bucket in place, peers read it over
+        #            NVLink, no pack at all
+        #   "own"    keep the caller's gradient tensors (arbitrary addresses)
+        if grads not in ("flat", "bucket", "own"):
+            raise ValueError("grads must be 'flat', 'bucket' or 'own'")
+        self.grads = grads
         self.grad_flat = None
-        if grad_arena:
+        if grads == "flat":
             self.grad_flat = torch.zeros(plan.param_bytes // 4, device=dev)
             for b in plan.buckets:
                 off = b.param_off // 4
                 for pid, n in zip(b.param_ids, b.numels):
                     params[pid].grad = self.grad_flat[off:off + n].view(params[pid].shape)
+                    off += n
+        elif grads == "bucket":
+            for b in plan.buckets:
+                region = self.ctx.arena_view(0, b.bucket_off, b.numel)
+                region.zero_()
+                off = 0
+                for pid, n in zip(b.param_ids, b.numels):
+                    params[pid].grad = region[off:off + n].view(params[pid].shape)
                     off += n
         for p in params.values():
             if p.grad is None:
@@ -214,9 +230,14 @@ class Aggregator:
         segs = comm.coalesce(comm.segments_for([self.params[p].grad for p in b.param_ids],
                                                None if self.param_arena else [self.params[p] for p in b.param_ids]))
         table = comm.segment_table([segs], self.device)
-        flags = N.F_PACK | (N.F_PARAM_ARENA if self.param_arena else N.F_UNPACK)
-        if len(segs) == 1 and segs[0].grad % 16 == 0:
-            flags |= N.F_FLAT  # one contiguous aligned gradient run: TMA streaming path
+        if self.grads == "bucket":
+            # zero-copy: the bucket IS the gradient storage; results land in the
+            # parameter arena (SGD) or in place (mean / sum; ring/hd unpack)
+            flags = N.F_PARAM_ARENA if self.param_arena else N.F_UNPACK
+        else:
+            flags = N.F_PACK | (N.F_PARAM_ARENA if self.param_arena else N.F_UNPACK)
+            if len(segs) == 1 and segs[0].grad % 16 == 0:
+                flags |= N.F_FLAT  # one contiguous aligned gradient run: TMA streaming path
         scale = 1.0 / self.world
         desc = comm.make_bucket(b.numel, b.bucket_off, b.flag_off, depth=b.depth, pattern=self.plan.pattern,
                                 epilogue=self.epi, flags=flags, ctas=b.ctas, segs=table, nseg=len(segs),
@@ -314,7 +335,7 @@ class Aggregator:
         one H2D and one D2H cudaMemcpyAsync per group of buckets, overlapped
         with the group's aggregation kernel."""
         if self.grad_flat is None or not self.param_arena:
-            raise RuntimeError("step_host_flat needs grad_arena=True and the parameter arena")
+            raise RuntimeError("step_host_flat needs grads='flat' and the parameter arena")
         cur = torch.cuda.current_stream(self.device)
         if not hasattr(self, "_h2d"):
             self._h2d = torch.cuda.Stream(device=self.device)

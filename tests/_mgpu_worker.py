@@ -88,6 +88,7 @@ def main() -> int:
     ctx.close()
     failures += mixed_grouping_check(rank, world, dev)
     failures += overlapped_hooks_check(rank, world, dev)
+    failures += overlapped_hooks_check(rank, world, dev, grads="bucket")
     t = torch.tensor([failures], device=dev)
     dist.all_reduce(t)
     if rank == 0:
@@ -165,7 +166,7 @@ def mixed_grouping_check(rank: int, world: int, dev) -> int:
     return fails
 
 
-def overlapped_hooks_check(rank: int, world: int, dev) -> int:
+def overlapped_hooks_check(rank: int, world: int, dev, grads: str = "flat") -> int:
     """Real backward on every rank, buckets launched from gradient hooks in the
     enforced order, SGD fused into the all-gather; every replica must equal
     theta - lr * ((sum of all ranks' grads in rank order) * (1/p))."""
@@ -188,7 +189,7 @@ def overlapped_hooks_check(rank: int, world: int, dev) -> int:
                        SimConfig(workers=world, network=NetworkModel(10.0, 1e-4), reduce=ReduceModel(400.0, 10.0)))
     ids = [gradsets.param_id(i, len(tensors)) for i in range(len(tensors))]
     plan = lower(art, {pid: t.numel for pid, t in zip(ids, tensors)}, world, Pattern.SHUFFLE)
-    agg = Aggregator(plan, dict(zip(ids, model.parameters())), rank=rank, lr=lr, epilogue="sgd")
+    agg = Aggregator(plan, dict(zip(ids, model.parameters())), rank=rank, lr=lr, epilogue="sgd", grads=grads)
     agg.attach_hooks()
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
     fails = 0
@@ -218,7 +219,7 @@ def overlapped_hooks_check(rank: int, world: int, dev) -> int:
         for a, b in zip(model.parameters(), ref.parameters()):
             if not torch.equal(a, b):
                 fails += 1
-                print(f"rank {rank}: overlapped hooks mismatch at iteration {it}", flush=True)
+                print(f"rank {rank}: overlapped hooks ({grads}) mismatch at iteration {it}", flush=True)
                 break
     agg.close()
     return fails

@@ -164,3 +164,38 @@ def test_tables_track_gradient_storage():
     agg.refresh_tables()
     assert agg.check_tables()
     agg.close()
+
+
+@pytest.mark.parametrize("grads", ["bucket", "own"])
+def test_gradient_storage_modes_match_sgd(grads):
+    from paper_2004_14020_b200.executor import Aggregator
+
+    lr = 0.05
+    model = _tiny_model(6)
+    ref = _tiny_model(6)
+    plan, params = _plan_for(model)
+    agg = Aggregator(plan, params, lr=lr, epilogue="sgd", grads=grads)
+    agg.attach_hooks()
+    x = torch.randn(16, 37, device="cuda")
+    for it in range(2):
+        ref.zero_grad(set_to_none=False)
+        ref(x * (it + 1)).square().mean().backward()
+        with torch.no_grad():
+            for p in ref.parameters():
+                p.copy_(p - lr * p.grad)
+        model.zero_grad(set_to_none=False)
+        agg.begin_iteration()
+        model(x * (it + 1)).square().mean().backward()
+        agg.finish_iteration()
+        torch.cuda.synchronize()
+        for a, b in zip(model.parameters(), ref.parameters()):
+            assert torch.equal(a, b)
+    # the one-launch pass too
+    for p in params.values():
+        p.grad.normal_()
+    theta0 = {k: v.detach().clone() for k, v in params.items()}
+    agg.step()
+    torch.cuda.synchronize()
+    for k, p in params.items():
+        assert torch.equal(p, theta0[k] - lr * p.grad)
+    agg.close()
