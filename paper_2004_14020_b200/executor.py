@@ -212,6 +212,8 @@ class Aggregator:
         self.epoch = 0
         self.launches = 0
         self._last_done = None
+        self._fp_pending = set()
+        self._gated = False
         self._build_list()
 
     # -- setup -----------------------------------------------------------------
@@ -412,10 +414,10 @@ class Aggregator:
 
     def begin_iteration(self) -> None:
         """Arm every bucket for one backward pass (gradients must be zeroed in
-        place, e.g. zero_grad(set_to_none=False), so the segment tables stay valid)."""
+        place -- Aggregator.zero_grad(), or zero_grad(set_to_none=False) -- so
+        the segment tables stay valid)."""
         for lv in self._live:
             lv.remaining = len(lv.members)
-            lv.done = None
         self._next = 0
         self._last_done = None
         cur = torch.cuda.current_stream(self.device)
@@ -460,14 +462,77 @@ class Aggregator:
         self._last_done = ev
         self._next = j
 
-    def finish_iteration(self) -> None:
+    def finish_iteration(self, postpone: bool = False) -> None:
         """Launch whatever is still held back, then make the current stream
-        wait for every bucket."""
+        wait for the buckets.  postpone=True executes the plan's postponed
+        update (transfer.py:156-160): buckets placed into the next forward pass
+        (FP_OVERLAP) are not waited for here but by the forward gate of the
+        first module that reads one of their parameters (gate_forward)."""
         self._drain(force=True)
         if self._next != len(self._live):
             missing = [lv.spec.group_id for lv in self._live[self._next:]]
             raise RuntimeError(f"buckets never became ready: {missing[:5]}")
-        torch.cuda.current_stream(self.device).wait_stream(self.comm_stream)
+        cur = torch.cuda.current_stream(self.device)
+        fp = [i for i, lv in enumerate(self._live) if lv.spec.placement == PlacementKind.FP_OVERLAP.value]
+        if not postpone or not fp or not self._gated:
+            cur.wait_stream(self.comm_stream)
+            return
+        bp = [i for i in range(len(self._live)) if i not in set(fp)]
+        if bp:  # the comm stream is FIFO: the last BP bucket covers every earlier one
+            cur.wait_event(self._live[bp[-1]].done)
+        self._fp_pending = {i for i in fp if not bp or i > bp[-1]}
+
+    # -- postponed update: forward gates -----------------------------------------
+    _gated = False
+    _fp_pending: set = set()
+
+    def gate_forward(self, modules: dict) -> int:
+        """Register forward pre-hooks: `modules` maps param id -> the module that
+        reads it.  A module whose parameters sit in a postponed (FP_OVERLAP)
+        bucket makes the current stream wait for that bucket's kernel before it
+        runs, and zeroes the bucket's gradients then (the kernel may read them
+        until it completes).  Returns the number of gated modules."""
+        by_mod: dict = {}
+        for i, lv in enumerate(self._live):
+            if lv.spec.placement != PlacementKind.FP_OVERLAP.value:
+                continue
+            for pid in lv.members:
+                m = modules[pid]
+                by_mod.setdefault(id(m), (m, set()))[1].add(i)
+        for m, idxs in by_mod.values():
+            self._hooks.append(m.register_forward_pre_hook(self._make_gate(sorted(idxs))))
+        self._gated = bool(by_mod)
+        return len(by_mod)
+
+    def _make_gate(self, idxs):
+        def gate(_m, _inp):
+            if not self._fp_pending:
+                return
+            cur = torch.cuda.current_stream(self.device)
+            for i in idxs:
+                if i in self._fp_pending:
+                    lv = self._live[i]
+                    if lv.done is not None:
+                        cur.wait_event(lv.done)
+                    torch._foreach_zero_([self.params[pid].grad for pid in lv.members])
+                    self._fp_pending.discard(i)
+        return gate
+
+    def zero_grad(self) -> None:
+        """Zero every gradient in place, except those of postponed buckets
+        still in flight (their forward gate zeroes them after the wait)."""
+        grads = [self.params[pid].grad for i, lv in enumerate(self._live) if i not in self._fp_pending
+                 for pid in lv.members]
+        if grads:
+            torch._foreach_zero_(grads)
+
+    def sync(self) -> None:
+        """Wait for everything, including postponed buckets (e.g. before evaluation)."""
+        cur = torch.cuda.current_stream(self.device)
+        cur.wait_stream(self.comm_stream)
+        for i in sorted(self._fp_pending):
+            torch._foreach_zero_([self.params[pid].grad for pid in self._live[i].members])
+        self._fp_pending = set()
 
     def detach_hooks(self) -> None:
         for h in self._hooks:
