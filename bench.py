@@ -51,7 +51,7 @@ def parse_args():
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--no-exposed", action="store_true", help="skip the model fwd/bwd exposed-comm measurement")
     ap.add_argument("--batch", type=int, default=64, help="per-GPU batch for the exposed-comm measurement")
-    ap.add_argument("--exposed-iters", type=int, default=10)
+    ap.add_argument("--exposed-iters", type=int, default=20)
     ap.add_argument("--no-sweep", action="store_true", help="skip the bucket-size sweep (N > 1)")
     ap.add_argument("--no-zero-copy", action="store_true", help="skip the zero-copy gradient variant")
     return ap.parse_args()
@@ -320,7 +320,10 @@ def nccl_baseline(torch, dist, params, grads_dev, world, steps, warmup, bucket_b
     return t.item(), len(buckets)
 
 
-def measure_exposed(args, plan, ids, world, rank, dev, dist):
+B200_REDUCE_MODEL = (2e6, 1.0)  # the reduction runs inside the collective kernel (~2 TB/s effective, 1 us)
+
+
+def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
     """Exposed communication per iteration, T - C (sim.py:155-157), measured on
     the real model: torchvision `args.model` (random init, synthetic batch,
     bf16 autocast, fp32 parameters and gradients), forward + backward on every
@@ -386,13 +389,45 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist):
         model.zero_grad(set_to_none=False)
         fwd_bwd(model)
 
-    agg = Aggregator(plan, dict(zip(ids, model.parameters())), rank=rank, lr=LR, epilogue="sgd")
+    # The full Caramel configuration for this model: DAG ingested from the real
+    # model (module-level ops, device-measured durations, min of 5 runs; max
+    # over ranks so every rank plans identically), calibrated network model,
+    # fused-reduction model, and the postponed update executed by forward gates.
+    from dataclasses import replace as _replace
+
+    from paper_2004_14020_b200.collective import Pattern as _P
+    from paper_2004_14020_b200.collective import ReduceModel as _RM
+    from paper_2004_14020_b200.costmodel import NetworkModel as _NM
+    from paper_2004_14020_b200.dag import DataflowDag as _DAG
+    from paper_2004_14020_b200.executor import lower as _lower
+    from paper_2004_14020_b200.ingest import ingest_model
+    from paper_2004_14020_b200.pipeline import run_pipeline as _rp
+    from paper_2004_14020_b200.sim import SimConfig as _SC
+
+    ing = ingest_model(model, compute_only, runs=5)
+    op_ids = sorted(o for o, op in ing.dag.ops.items() if op.kind.value == "compute")
+    durs = torch.tensor([float(ing.dag.ops[o].duration_us) for o in op_ids], device=dev)
+    if dist is not None:
+        dist.all_reduce(durs, op=dist.ReduceOp.MAX)
+    ops = dict(ing.dag.ops)
+    for o, d in zip(op_ids, durs.tolist()):
+        ops[o] = _replace(ops[o], duration_us=int(d))
+    dag = _DAG(ops=ops, params=dict(ing.dag.params))
+    net = network or _NM(*NVLINK_MODEL)
+    art = _rp(dag, _SC(workers=max(2, world), network=net, reduce=_RM(*B200_REDUCE_MODEL), pattern=_P(args.pattern)))
+    numels = {pid: p.numel() for pid, p in ing.params.items()}
+    mplan = _lower(art, numels, world, _P(args.pattern))
+    agg = Aggregator(mplan, dict(ing.params), rank=rank, lr=LR, epilogue="sgd")
+    gated = agg.gate_forward(ing.modules)
+    placements = {}
+    for b in mplan.buckets:
+        placements[b.placement] = placements.get(b.placement, 0) + 1
 
     def caramel_step():
-        model.zero_grad(set_to_none=False)
+        agg.zero_grad()
         agg.begin_iteration()
         fwd_bwd(model)
-        agg.finish_iteration()
+        agg.finish_iteration(postpone=True)
 
     # alternate compute-only and Caramel rounds (clock / thermal drift hits
     # both alike); medians over rounds
@@ -403,6 +438,7 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist):
         ks.append(timed(caramel_step))
         agg.detach_hooks()
     c_ms, k_ms = sorted(cs)[1], sorted(ks)[1]
+    agg.sync()
     agg.status()
     agg.close()
     del model, agg
@@ -428,7 +464,11 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist):
     out = {"compute_ms": round(c_ms, 4), "caramel_ms": round(k_ms, 4),
            "caramel_exposed_ms": round(k_ms - c_ms, 4),
            "model": f"torchvision {args.model}, batch {B}/GPU, {size}x{size}, bf16 autocast, fp32 grads",
-           "iters": K, "rounds": 3, "stat": "median of 3 alternating rounds"}
+           "iters": K, "rounds": 3, "stat": "median of 3 alternating rounds",
+           "plan": {"source": "ingested model DAG (measured, min of 5 runs, max over ranks)",
+                    "network_model": [round(net.latency_us, 3), net.per_byte_us], "reduce_model": list(B200_REDUCE_MODEL),
+                    "buckets": len(mplan.buckets), "placements": placements, "gated_modules": gated,
+                    "modelled_exposed_us": round(art.transfer_schedule.added_iteration_time_us, 1)}}
     if nccl_ms is not None:
         out.update({"nccl_ddp_ms": round(nccl_ms, 4), "nccl_ddp_exposed_ms": round(nccl_ms - c_ms, 4)})
     return out
@@ -722,7 +762,10 @@ def run_caramel(args) -> int:
         for pid in ids:  # free the step's tensors before the model runs
             params[pid] = None
         torch.cuda.empty_cache()
-        exposed = measure_exposed(args, plan, ids, world, rank, dev, dist)
+        from paper_2004_14020_b200.costmodel import NetworkModel as _NM
+
+        net = _NM(calibrated["latency_us"], calibrated["per_byte_us"]) if calibrated else None
+        exposed = measure_exposed(args, plan, ids, world, rank, dev, dist, network=net)
 
     # ---- CPU baseline (rank 0, N = 1 only) ----------------------------------
     cpu = None

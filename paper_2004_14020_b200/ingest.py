@@ -13,7 +13,10 @@ from a real model instead of the synthetic layered chain:
   module's forward and backward, over several runs, each op's duration the
   minimum across runs (estimate_op_times, costmodel.py:74-81, PAPER.md:350);
   the time between two parameterised modules (activations, pooling, residual
-  adds) is charged to the later one, so the ops partition the iteration.
+  adds) is charged to the later one, so the ops partition the iteration;
+  backward boundaries are the moments a module's parameter gradients are
+  accumulated (post-accumulate-grad hooks), i.e. the update times the batcher
+  works from.
 
 Parameter ids are gradsets.param_id(i) over named_parameters() order, the ids
 the gradient inventories and the executor use.
@@ -69,14 +72,20 @@ def ingest_model(model: torch.nn.Module, step_fn, runs: int = 5) -> IngestedMode
         ev.record()
         fwd_events[-1].append((m, ev))
 
-    def b_hook(m, *_):
-        ev = torch.cuda.Event(enable_timing=True)
-        ev.record()
-        bwd_events[-1].append((m, ev))
+    # backward boundaries: the moment each module's parameter gradients are
+    # accumulated (post-accumulate-grad hooks; module backward hooks would wrap
+    # outputs and break in-place activations)
+    def make_b_hook(m):
+        def b_hook(_p):
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            bwd_events[-1].append((m, ev))
+        return b_hook
 
     for m in mods:
         handles.append(m.register_forward_hook(f_hook))
-        handles.append(m.register_full_backward_hook(b_hook))
+        for p in m.parameters(recurse=False):
+            handles.append(p.register_post_accumulate_grad_hook(make_b_hook(m)))
     samples: dict[str, list[int]] = {}
     try:
         for r in range(runs + 1):  # the first run warms up
@@ -99,10 +108,14 @@ def ingest_model(model: torch.nn.Module, step_fn, runs: int = 5) -> IngestedMode
             for m, ev in fwd_events[-1]:
                 t_f[id(m)] = t_f.get(id(m), 0.0) + prev.elapsed_time(ev)
                 prev = ev
-            # backward: hooks fire in reverse module order
-            t_b = {}
+            # backward: a module's boundary is its last parameter's accumulation
+            last = {}
             for m, ev in bwd_events[-1]:
-                t_b[id(m)] = t_b.get(id(m), 0.0) + prev.elapsed_time(ev)
+                last[id(m)] = ev
+            seq = sorted(last.items(), key=lambda kv: prev.elapsed_time(kv[1]))
+            t_b = {}
+            for mid, ev in seq:
+                t_b[mid] = max(0.0, prev.elapsed_time(ev))
                 prev = ev
             for k, m in enumerate(order):
                 for kind, t in (("f", t_f), ("b", t_b)):
