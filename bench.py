@@ -52,6 +52,8 @@ def parse_args():
     ap.add_argument("--no-exposed", action="store_true", help="skip the model fwd/bwd exposed-comm measurement")
     ap.add_argument("--batch", type=int, default=64, help="per-GPU batch for the exposed-comm measurement")
     ap.add_argument("--exposed-iters", type=int, default=20)
+    ap.add_argument("--exposed-grads", default="bucket", choices=["flat", "bucket"],
+                    help="gradient storage of the overlapped Aggregator (bucket = zero-copy)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the bucket-size sweep (N > 1)")
     ap.add_argument("--no-zero-copy", action="store_true", help="skip the zero-copy gradient variant")
     return ap.parse_args()
@@ -352,9 +354,10 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
     def fwd_bwd(m):
         with torch.autocast("cuda", dtype=torch.bfloat16):
             out = m(x)
-            if isinstance(out, tuple) or hasattr(out, "logits"):
-                out = out[0] if isinstance(out, tuple) else out.logits
-            loss = loss_fn(out.float(), y)
+            if isinstance(out, tuple):  # inception_v3 in training: (logits, aux_logits)
+                loss = loss_fn(out[0].float(), y) + 0.4 * loss_fn(out[1].float(), y)
+            else:
+                loss = loss_fn(out.float(), y)
         loss.backward()
 
     def timed(fn):
@@ -417,7 +420,7 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
     art = _rp(dag, _SC(workers=max(2, world), network=net, reduce=_RM(*B200_REDUCE_MODEL), pattern=_P(args.pattern)))
     numels = {pid: p.numel() for pid, p in ing.params.items()}
     mplan = _lower(art, numels, world, _P(args.pattern))
-    agg = Aggregator(mplan, dict(ing.params), rank=rank, lr=LR, epilogue="sgd")
+    agg = Aggregator(mplan, dict(ing.params), rank=rank, lr=LR, epilogue="sgd", grads=args.exposed_grads)
     gated = agg.gate_forward(ing.modules)
     placements = {}
     for b in mplan.buckets:
@@ -465,6 +468,7 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
            "caramel_exposed_ms": round(k_ms - c_ms, 4),
            "model": f"torchvision {args.model}, batch {B}/GPU, {size}x{size}, bf16 autocast, fp32 grads",
            "iters": K, "rounds": 3, "stat": "median of 3 alternating rounds",
+           "grads": args.exposed_grads,
            "plan": {"source": "ingested model DAG (measured, min of 5 runs, max over ranks)",
                     "network_model": [round(net.latency_us, 3), net.per_byte_us], "reduce_model": list(B200_REDUCE_MODEL),
                     "buckets": len(mplan.buckets), "placements": placements, "gated_modules": gated,
