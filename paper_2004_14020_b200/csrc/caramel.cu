@@ -770,35 +770,87 @@ __device__ __forceinline__ void rs_ag_range(const Env& E, const caramel_bucket& 
 
 // Pairwise step used by ring and halving-doubling: out = a + b (a first),
 // optionally followed by the epilogue (last reduction of the owner's shard).
+// [lo, hi) split into a scalar head, a 4-aligned float4 body and a scalar tail
+__device__ __forceinline__ void split4(uint64_t lo, uint64_t hi, uint64_t& a, uint64_t& b) {
+  a = (lo + 3) & ~3ull;
+  if (a > hi) a = hi;
+  b = hi & ~3ull;
+  if (b < a) b = a;
+}
+
+// Pairwise step used by ring and halving-doubling: out = a + b (a first),
+// optionally followed by the epilogue (last reduction of the owner's shard).
+// Four float4 per thread per trip, loads of both operands issued first (the
+// operands are peer memory: one NVLink round trip per trip, not per vector).
 __device__ __forceinline__ void pair_range(const float* a_src, const float* b_src, float* out,
                                            uint64_t lo, uint64_t hi, bool final_epi, const caramel_bucket& B,
                                            const float* theta_flat, Cursor& tc) {
   const int epi = B.epilogue;
   const bool need_theta = final_epi && epi == CARAMEL_EPI_SGD;
-  walk(lo, hi,
-       [&](uint64_t v) {
-         float4 s = add4(ld4(a_src + v), ld4(b_src + v));
-         if (final_epi) {
-           float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-           if (need_theta) t = theta_flat ? ld4(theta_flat + v) : seg_ld4(tc, v, 1);
-           s = epi4(epi, s, t, B.scale, B.lr);
-         }
-         st4(out + v, s);
-       },
-       [&](uint64_t i) {
-         float s = __fadd_rn(ld1(a_src + i), ld1(b_src + i));
-         if (final_epi) {
-           float t = 0.f;
-           if (need_theta) t = theta_flat ? ld1(theta_flat + i) : seg_ld1(tc, i, 1);
-           s = epi1(epi, s, t, B.scale, B.lr);
-         }
-         st1(out + i, s);
-       });
+  auto scalar = [&](uint64_t i) {
+    float s = __fadd_rn(ld1(a_src + i), ld1(b_src + i));
+    if (final_epi) {
+      float t = 0.f;
+      if (need_theta) t = theta_flat ? ld1(theta_flat + i) : seg_ld1(tc, i, 1);
+      s = epi1(epi, s, t, B.scale, B.lr);
+    }
+    st1(out + i, s);
+  };
+  if (lo >= hi) return;
+  uint64_t a, b;
+  split4(lo, hi, a, b);
+  for (uint64_t i = lo + threadIdx.x; i < a; i += blockDim.x) scalar(i);
+  constexpr int U = 4;
+  const uint64_t step = 4ull * blockDim.x;
+  uint64_t v = a + 4ull * threadIdx.x;
+  for (; v + (U - 1) * step < b; v += U * step) {
+    float4 x[U], y[U], t[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      x[u] = ld4(a_src + v + u * step);
+      y[u] = ld4(b_src + v + u * step);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      t[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (need_theta) t[u] = theta_flat ? ld4(theta_flat + v + u * step) : seg_ld4(tc, v + u * step, 1);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float4 s = add4(x[u], y[u]);
+      if (final_epi) s = epi4(epi, s, t[u], B.scale, B.lr);
+      st4(out + v + u * step, s);
+    }
+  }
+  for (; v < b; v += step) {
+    float4 s = add4(ld4(a_src + v), ld4(b_src + v));
+    if (final_epi) {
+      float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (need_theta) t = theta_flat ? ld4(theta_flat + v) : seg_ld4(tc, v, 1);
+      s = epi4(epi, s, t, B.scale, B.lr);
+    }
+    st4(out + v, s);
+  }
+  for (uint64_t i = b + threadIdx.x; i < hi; i += blockDim.x) scalar(i);
 }
 
 __device__ __forceinline__ void copy_range(const float* src, float* dst, uint64_t lo, uint64_t hi) {
-  walk(lo, hi, [&](uint64_t v) { st4(dst + v, ld4(src + v)); },
-       [&](uint64_t i) { st1(dst + i, ld1(src + i)); });
+  if (lo >= hi) return;
+  uint64_t a, b;
+  split4(lo, hi, a, b);
+  for (uint64_t i = lo + threadIdx.x; i < a; i += blockDim.x) st1(dst + i, ld1(src + i));
+  constexpr int U = 8;
+  const uint64_t step = 4ull * blockDim.x;
+  uint64_t v = a + 4ull * threadIdx.x;
+  for (; v + (U - 1) * step < b; v += U * step) {
+    float4 x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) x[u] = ld4(src + v + u * step);
+#pragma unroll
+    for (int u = 0; u < U; ++u) st4(dst + v + u * step, x[u]);
+  }
+  for (; v < b; v += step) st4(dst + v, ld4(src + v));
+  for (uint64_t i = b + threadIdx.x; i < hi; i += blockDim.x) st1(dst + i, ld1(src + i));
 }
 
 // Single-rank path (world == 1): no exchange; gather, epilogue and scatter
