@@ -484,8 +484,9 @@ SWEEP_SIZES = (4096, 65536, 1 << 20, 4 << 20, 16 << 20, 64 << 20, 256 << 20)
 def bucket_sweep(torch, dist, world, rank, dev, iters=20):
     """Config 5: one bucket of S bytes, adaptive depth from the NVLink model,
     two-shot over NVLink (caramel_allreduce, packed input, result in place)
-    vs torch.distributed.all_reduce (NCCL) on the same bytes.  Back-to-back
-    launches between two CUDA events, max over ranks; bus GB/s = 2(p-1)/p*S/t."""
+    vs torch.distributed.all_reduce (NCCL) on the same bytes.  `iters` calls
+    captured in a CUDA graph (both sides; host launch cost excluded), replayed
+    between two CUDA events, max over ranks; bus GB/s = 2(p-1)/p*S/t."""
     import ctypes
 
     from paper_2004_14020_b200 import _native as N
@@ -510,34 +511,53 @@ def bucket_sweep(torch, dist, world, rank, dev, iters=20):
         b = comm.make_bucket(n, 0, region + k * (1 << 20), depth=depth, pattern=N.SHUFFLE, epilogue=N.EPI_SUM,
                              flags=0, ctas=ctas)
 
-        def timed(fn):
+        def timed(fn, graphed=True):
+            """Per-call device time of `fn`: `iters` calls captured in one CUDA
+            graph (no host launch overhead in the measurement), replayed
+            between two events; eager back-to-back calls if capture fails."""
             for _ in range(5):
                 fn()
             torch.cuda.synchronize()
+            g = None
+            if graphed:
+                try:
+                    g = torch.cuda.CUDAGraph()
+                    side = torch.cuda.Stream()
+                    side.wait_stream(torch.cuda.current_stream())
+                    with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
+                        for _ in range(iters):
+                            fn(side)
+                    torch.cuda.current_stream().wait_stream(side)
+                    g.replay()
+                    torch.cuda.synchronize()
+                except Exception:
+                    g = None
             dist.barrier()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record(stream)
-            for _ in range(iters):
-                fn()
+            if g is not None:
+                g.replay()
+            else:
+                for _ in range(iters):
+                    fn()
             e.record(stream)
             e.synchronize()
             t = torch.tensor([s.elapsed_time(e) / iters], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            return t.item() * 1e3  # us
+            return t.item() * 1e3, g is not None  # us
 
-        ep = [0]
-
-        def caramel():
-            ep[0] += 1
-            ctx.allreduce(b, ep[0], stream.cuda_stream)
+        def caramel(st=None):
+            st = st or stream
+            N.check(N.lib().caramel_epoch_advance(ctx._ctx, ctypes.c_void_p(st.cuda_stream)))
+            ctx.allreduce(b, 0, st.cuda_stream)  # epoch 0: device counter (graph-replayable)
 
         x = torch.empty(n, device=dev).normal_()
-        us_c = timed(caramel)
-        us_n = timed(lambda: dist.all_reduce(x))
+        us_c, gc = timed(caramel)
+        us_n, gn = timed(lambda st=None: dist.all_reduce(x))
         bus = 2 * (world - 1) / world * size / 1e3
         rows.append({"bytes": size, "depth": depth, "caramel_us": round(us_c, 2),
                      "caramel_bus_gbs": round(bus / us_c, 1), "nccl_us": round(us_n, 2),
-                     "nccl_bus_gbs": round(bus / us_n, 1)})
+                     "nccl_bus_gbs": round(bus / us_n, 1), "graphed": [gc, gn]})
     ctx.status()
     ctx.close()
     return rows

@@ -623,8 +623,18 @@ __host__ __device__ __forceinline__ uint64_t out_region_elems(uint64_t numel) {
 // (numel x 8 B) | LL in (p slots x numel x 8 B)].  Chosen from numel alone, so
 // every rank and every launch kind agrees.
 #define LL_MAX_ELEMS 16384
+// LL cutoff in elements: compile-time default, CARAMEL_LL_MAX overrides it at
+// library load (host layout and device kernels read the same value; every
+// rank must use the same setting, like every other layout parameter)
+__device__ uint64_t d_ll_max = LL_MAX_ELEMS;
+static uint64_t h_ll_max = LL_MAX_ELEMS;
 __host__ __device__ __forceinline__ bool use_ll(int pattern, int world, uint64_t numel) {
-  return pattern == CARAMEL_SHUFFLE && world > 1 && numel > 0 && numel <= LL_MAX_ELEMS;
+#ifdef __CUDA_ARCH__
+  const uint64_t cut = d_ll_max;
+#else
+  const uint64_t cut = h_ll_max;
+#endif
+  return pattern == CARAMEL_SHUFFLE && world > 1 && numel > 0 && numel <= cut;
 }
 __host__ __device__ __forceinline__ uint64_t ll_out_off(uint64_t numel) {  // bytes from bucket start
   return 4 * ((numel + 3) & ~3ull);
@@ -2028,6 +2038,14 @@ struct Blob {
 
 extern "C" {
 
+static void load_ll_max() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  if (const char* e = getenv("CARAMEL_LL_MAX")) h_ll_max = strtoull(e, 0, 10);
+  cudaMemcpyToSymbol(d_ll_max, &h_ll_max, sizeof(h_ll_max));
+}
+
 int caramel_abi_version(void) { return CARAMEL_ABI_VERSION; }
 const char* caramel_last_error(void) { return g_err; }
 
@@ -2062,6 +2080,7 @@ static int default_max_ctas() {
 
 int caramel_bucket_layout(uint64_t numel, int depth, int pattern, int world, int32_t* ctas,
                           uint64_t* bucket_bytes, uint64_t* flag_bytes) {
+  if (getenv("CARAMEL_LL_MAX")) h_ll_max = strtoull(getenv("CARAMEL_LL_MAX"), 0, 10);
   int rc = validate_workers(pattern, world);
   if (rc) return rc;
   if (depth < 1 || depth > CARAMEL_MAX_DEPTH)
@@ -2099,6 +2118,7 @@ int caramel_init(int rank, int world, int nlocal, uint64_t arena_bytes, uint64_t
                  caramel_ctx** out) {
   if (!out) return set_err(CARAMEL_EINVAL, "null ctx output");
   *out = nullptr;
+  load_ll_max();
   if (world < 1 || world > MAXR) return set_err(CARAMEL_EWORKERS, "world %d outside [1, %d]", world, MAXR);
   if (nlocal != 1 && nlocal != world) return set_err(CARAMEL_EINVAL, "nlocal must be 1 or world");
   if (nlocal == world && rank != 0) return set_err(CARAMEL_EINVAL, "rank emulation requires rank 0");
