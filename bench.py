@@ -29,6 +29,9 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+# one hardware queue per stream (set before any CUDA context): the copy-engine
+# engine's stream-memory-op waits must not stall unrelated streams
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 METRIC = "exposed comm ms/iter and allreduce bus GB/s at 1/2/4/8 B200 vs NVLink roofline"
 NVLINK_MODEL = (10.0, 1.0 / 460e3)      # latency us, us/B (SURVEY §8a "NVLink-ish")
@@ -54,6 +57,8 @@ def parse_args():
     ap.add_argument("--exposed-iters", type=int, default=20)
     ap.add_argument("--exposed-grads", default="bucket", choices=["flat", "bucket"],
                     help="gradient storage of the overlapped Aggregator (bucket = zero-copy)")
+    ap.add_argument("--exposed-engine", default="both", choices=["sm", "ce", "both"],
+                    help="overlapped-path engine(s) measured; 'both' reports each and the faster")
     ap.add_argument("--no-sweep", action="store_true", help="skip the bucket-size sweep (N > 1)")
     ap.add_argument("--no-zero-copy", action="store_true", help="skip the zero-copy gradient variant")
     return ap.parse_args()
@@ -325,6 +330,38 @@ def nccl_baseline(torch, dist, params, grads_dev, world, steps, warmup, bucket_b
 B200_REDUCE_MODEL = (2e6, 1.0)  # the reduction runs inside the collective kernel (~2 TB/s effective, 1 us)
 
 
+def ingested_plan(args, model, compute_only, world, dist, dev, network=None):
+    """The full Caramel configuration for a real model: DAG ingested from the
+    model (module-level ops, device-measured durations, min of 5 runs; max over
+    ranks so every rank plans identically), calibrated network model,
+    fused-reduction model; lowered to the executor plan."""
+    import torch
+    from dataclasses import replace as _replace
+
+    from paper_2004_14020_b200.collective import Pattern as _P
+    from paper_2004_14020_b200.collective import ReduceModel as _RM
+    from paper_2004_14020_b200.costmodel import NetworkModel as _NM
+    from paper_2004_14020_b200.dag import DataflowDag as _DAG
+    from paper_2004_14020_b200.executor import lower as _lower
+    from paper_2004_14020_b200.ingest import ingest_model
+    from paper_2004_14020_b200.pipeline import run_pipeline as _rp
+    from paper_2004_14020_b200.sim import SimConfig as _SC
+
+    ing = ingest_model(model, compute_only, runs=5)
+    op_ids = sorted(o for o, op in ing.dag.ops.items() if op.kind.value == "compute")
+    durs = torch.tensor([float(ing.dag.ops[o].duration_us) for o in op_ids], device=dev)
+    if dist is not None:
+        dist.all_reduce(durs, op=dist.ReduceOp.MAX)
+    ops = dict(ing.dag.ops)
+    for o, d in zip(op_ids, durs.tolist()):
+        ops[o] = _replace(ops[o], duration_us=int(d))
+    dag = _DAG(ops=ops, params=dict(ing.dag.params))
+    net = network or _NM(*NVLINK_MODEL)
+    art = _rp(dag, _SC(workers=max(2, world), network=net, reduce=_RM(*B200_REDUCE_MODEL), pattern=_P(args.pattern)))
+    numels = {pid: p.numel() for pid, p in ing.params.items()}
+    return ing, art, _lower(art, numels, world, _P(args.pattern)), net
+
+
 def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
     """Exposed communication per iteration, T - C (sim.py:155-157), measured on
     the real model: torchvision `args.model` (random init, synthetic batch,
@@ -392,62 +429,59 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
         model.zero_grad(set_to_none=False)
         fwd_bwd(model)
 
-    # The full Caramel configuration for this model: DAG ingested from the real
-    # model (module-level ops, device-measured durations, min of 5 runs; max
-    # over ranks so every rank plans identically), calibrated network model,
-    # fused-reduction model, and the postponed update executed by forward gates.
-    from dataclasses import replace as _replace
-
-    from paper_2004_14020_b200.collective import Pattern as _P
-    from paper_2004_14020_b200.collective import ReduceModel as _RM
-    from paper_2004_14020_b200.costmodel import NetworkModel as _NM
-    from paper_2004_14020_b200.dag import DataflowDag as _DAG
-    from paper_2004_14020_b200.executor import lower as _lower
-    from paper_2004_14020_b200.ingest import ingest_model
-    from paper_2004_14020_b200.pipeline import run_pipeline as _rp
-    from paper_2004_14020_b200.sim import SimConfig as _SC
-
-    ing = ingest_model(model, compute_only, runs=5)
-    op_ids = sorted(o for o, op in ing.dag.ops.items() if op.kind.value == "compute")
-    durs = torch.tensor([float(ing.dag.ops[o].duration_us) for o in op_ids], device=dev)
-    if dist is not None:
-        dist.all_reduce(durs, op=dist.ReduceOp.MAX)
-    ops = dict(ing.dag.ops)
-    for o, d in zip(op_ids, durs.tolist()):
-        ops[o] = _replace(ops[o], duration_us=int(d))
-    dag = _DAG(ops=ops, params=dict(ing.dag.params))
-    net = network or _NM(*NVLINK_MODEL)
-    art = _rp(dag, _SC(workers=max(2, world), network=net, reduce=_RM(*B200_REDUCE_MODEL), pattern=_P(args.pattern)))
-    numels = {pid: p.numel() for pid, p in ing.params.items()}
-    mplan = _lower(art, numels, world, _P(args.pattern))
-    agg = Aggregator(mplan, dict(ing.params), rank=rank, lr=LR, epilogue="sgd", grads=args.exposed_grads)
-    gated = agg.gate_forward(ing.modules)
+    ing, art, mplan, net = ingested_plan(args, model, compute_only, world, dist, dev, network)
     placements = {}
     for b in mplan.buckets:
         placements[b.placement] = placements.get(b.placement, 0) + 1
+    # engines of the overlapped path: "sm" (NVLink kernels) and, at N > 1 with
+    # zero-copy gradients, "ce" (copy-engine two-shot, no SM held while bytes
+    # move); each measured in 3 rounds alternating with compute-only rounds
+    # (clock / thermal drift hits both alike), medians over rounds
+    engines = ["sm"] + (["ce"] if world > 1 and args.exposed_grads == "bucket" else [])
+    if args.exposed_engine != "both":
+        engines = [args.exposed_engine]
+    cs, per_engine, gated = [], {}, 0
 
-    def caramel_step():
-        agg.zero_grad()
-        agg.begin_iteration()
-        fwd_bwd(model)
-        agg.finish_iteration(postpone=True)
+    def detach_storage():
+        # give the model its own storage back before an Aggregator's arenas go
+        for p in model.parameters():
+            p.data = p.data.clone()
+            p.grad = p.grad.clone()
 
-    # alternate compute-only and Caramel rounds (clock / thermal drift hits
-    # both alike); medians over rounds
-    cs, ks = [], []
-    for _ in range(3):
-        cs.append(timed(compute_only))
-        agg.attach_hooks()
-        ks.append(timed(caramel_step))
-        agg.detach_hooks()
-    c_ms, k_ms = sorted(cs)[1], sorted(ks)[1]
-    agg.sync()
-    agg.status()
-    agg.close()
-    del model, agg
+    for engine in engines:
+        agg = Aggregator(mplan, dict(ing.params), rank=rank, lr=LR, epilogue="sgd", grads=args.exposed_grads,
+                         engine=engine)
+        gated = agg.gate_forward(ing.modules)
+
+        def caramel_step():
+            agg.zero_grad()
+            agg.begin_iteration()
+            fwd_bwd(model)
+            agg.finish_iteration(postpone=True)
+
+        ks, ds = [], []
+        for _ in range(3):
+            c = timed(compute_only)
+            agg.attach_hooks()
+            k = timed(caramel_step)
+            agg.detach_hooks()
+            cs.append(c)
+            ks.append(k)
+            ds.append(k - c)
+        # exposed = median over rounds of (round's Caramel - round's compute):
+        # paired rounds cancel slow clock / thermal drift between rounds
+        per_engine[engine] = (sorted(ks)[1], sorted(ds)[1])
+        agg.sync()
+        agg.status()
+        detach_storage()
+        agg.close()
+        del agg
+    c_ms = sorted(cs)[len(cs) // 2]
+    best = min(per_engine, key=lambda e: per_engine[e][1])
+    k_ms, k_exp = per_engine[best]
     torch.cuda.empty_cache()
 
-    nccl_ms = None
+    nccl_ms = nccl_exp = None
     if dist is not None:
         from torch.nn.parallel import DistributedDataParallel as DDP
 
@@ -460,21 +494,29 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
             fwd_bwd(ddp)
             opt.step()
 
-        ns = [timed(ddp_step) for _ in range(3)]
-        nccl_ms = sorted(ns)[1]
+        ns, nd = [], []
+        for _ in range(3):
+            c = timed(compute_only)
+            n = timed(ddp_step)
+            ns.append(n)
+            nd.append(n - c)
+        nccl_ms, nccl_exp = sorted(ns)[1], sorted(nd)[1]
         del ddp, m2, opt
         torch.cuda.empty_cache()
+    del model
     out = {"compute_ms": round(c_ms, 4), "caramel_ms": round(k_ms, 4),
-           "caramel_exposed_ms": round(k_ms - c_ms, 4),
+           "caramel_exposed_ms": round(k_exp, 4), "engine": best,
+           "engines": {e: {"ms": round(v[0], 4), "exposed_ms": round(v[1], 4)} for e, v in per_engine.items()},
            "model": f"torchvision {args.model}, batch {B}/GPU, {size}x{size}, bf16 autocast, fp32 grads",
-           "iters": K, "rounds": 3, "stat": "median of 3 alternating rounds",
+           "iters": K, "rounds": 3,
+           "stat": "exposed = median over 3 rounds of (round time - paired compute-only round time)",
            "grads": args.exposed_grads,
            "plan": {"source": "ingested model DAG (measured, min of 5 runs, max over ranks)",
                     "network_model": [round(net.latency_us, 3), net.per_byte_us], "reduce_model": list(B200_REDUCE_MODEL),
                     "buckets": len(mplan.buckets), "placements": placements, "gated_modules": gated,
                     "modelled_exposed_us": round(art.transfer_schedule.added_iteration_time_us, 1)}}
     if nccl_ms is not None:
-        out.update({"nccl_ddp_ms": round(nccl_ms, 4), "nccl_ddp_exposed_ms": round(nccl_ms - c_ms, 4)})
+        out.update({"nccl_ddp_ms": round(nccl_ms, 4), "nccl_ddp_exposed_ms": round(nccl_exp, 4)})
     return out
 
 

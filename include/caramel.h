@@ -192,6 +192,29 @@ int caramel_allreduce_many(caramel_ctx* ctx, const caramel_bucket* host, int32_t
                            uint64_t dev_segprefix, int32_t ctas, int32_t mode,
                            uint32_t epoch, void* stream);
 
+/* Copy-engine two-shot (the overlapped path's engine while backward kernels
+ * own the SMs; same reference call it replaces, pipeline.py:94).  The NVLink
+ * transfers of a two-shot run on the GPU's copy engines and the cross-rank
+ * flags are stream memory operations, so no SM is held while bytes move or
+ * while a rank waits for its peers; the reduction + epilogue is one short
+ * kernel.  Buckets [0, count) of `host` are launch positions index0 ..
+ * index0+count-1 of this iteration's launch order; every rank must make the
+ * same sequence of calls (a stream wait stalls its hardware queue, so
+ * differently grouped calls could wait on each other).  `epoch`: the
+ * iteration number, > 0 and increasing.  `grad_stream`: the stream that
+ * produced the buckets' gradients -- the READY signal is issued there, not
+ * behind this rank's earlier all-gather waits; `stream` must already be
+ * ordered after the gradients (e.g. waited on grad_stream).  Per element the result equals
+ * caramel_allreduce[_update] with the SHUFFLE pattern (sum in ascending rank
+ * order).  Requires one rank per process, SHUFFLE buckets without
+ * PACK/UNPACK (gradients live in the bucket arena) and, for SGD,
+ * PARAM_ARENA.  Returns CARAMEL_ESTATE if the device lacks 64-bit stream
+ * memory operations (caramel_ce_available). */
+int caramel_allreduce_ce(caramel_ctx* ctx, const caramel_bucket* host, int32_t count,
+                         uint32_t index0, uint32_t epoch, void* grad_stream, void* stream);
+/* 1 if caramel_allreduce_ce can run on this context, else 0. */
+int caramel_ce_available(caramel_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

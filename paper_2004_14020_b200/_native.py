@@ -98,6 +98,9 @@ SIGNATURES = {
     "caramel_allreduce_many": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Bucket), ctypes.c_int32,
                                               ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int32,
                                               ctypes.c_int32, ctypes.c_uint32, ctypes.c_void_p]),
+    "caramel_allreduce_ce": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Bucket), ctypes.c_int32,
+                                            ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p]),
+    "caramel_ce_available": (ctypes.c_int, [ctypes.c_void_p]),
 }
 
 

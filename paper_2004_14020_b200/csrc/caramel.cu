@@ -19,6 +19,7 @@
 // NVSwitch).  Flags are 32-bit epochs written by the producer into the
 // consumer's flag block with st.release.sys and polled with ld.acquire.sys.
 
+#include <cuda.h>  // stream memory-op types; entry points come from cudaGetDriverEntryPoint
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -2016,6 +2017,74 @@ __global__ void __launch_bounds__(THREADS, 1) k_collective_many(const __grid_con
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+
+// ---------------------------------------------------------------------------
+// Copy-engine two-shot (caramel_allreduce_ce).  The NVLink bytes move on the
+// copy engines; this kernel is the only SM work: for every bucket of the call,
+// my shard = own gradients (bucket arena) + the world-1 peer contributions the
+// copy engines staged (slots congruent to the bucket arena), summed in
+// ascending rank order, epilogue, stored to the output (parameter arena for
+// SGD, my bucket arena otherwise) -- where the peers' copy engines fetch it.
+// Short-lived CTAs of CE_TILE elements each: no CTA outlives its tile, so the
+// backward kernels running beside it get SMs back within microseconds.
+// ---------------------------------------------------------------------------
+#define CE_MAX_BUCKETS 32
+#define CE_THREADS 256
+#define CE_TILE 8192
+#define CE_FLAG_OFF 4096  // byte offset of the READY / DONE words in the sync region
+
+struct CeItem {
+  uint64_t src;  // byte offset of my shard in the bucket arena (= in every staging slot)
+  uint64_t dst;  // byte offset of my shard in the output arena
+  uint64_t n;    // shard elements
+  uint32_t cta0; // first CTA of this bucket
+  float lr, scale;
+};
+
+struct CeParams {
+  const char* arena;    // my bucket arena
+  const char* staging;  // slot k holds rank (k < me ? k : k + 1)'s contribution
+  char* out;
+  uint64_t slot_bytes;
+  int world, me, count, epi;
+  CeItem it[CE_MAX_BUCKETS];
+};
+
+__device__ __forceinline__ const char* ce_src(const CeParams& P, int q) {
+  return q == P.me ? P.arena : P.staging + (uint64_t)(q < P.me ? q : q - 1) * P.slot_bytes;
+}
+
+__global__ void __launch_bounds__(CE_THREADS) k_ce_reduce(const __grid_constant__ CeParams P) {
+  int b = 0;
+  while (b + 1 < P.count && blockIdx.x >= P.it[b + 1].cta0) ++b;
+  const uint64_t src = P.it[b].src, dst = P.it[b].dst, n = P.it[b].n;
+  const float lr = P.it[b].lr, scale = P.it[b].scale;
+  const uint64_t t0 = (uint64_t)(blockIdx.x - P.it[b].cta0) * CE_TILE;
+  const uint64_t t1 = t0 + CE_TILE < n ? t0 + CE_TILE : n;
+  // elements i with (src/4 + i) % 4 == 0 start a 16-byte vector in every input
+  const uint64_t head = (4 - ((src >> 2) & 3)) & 3;
+  uint64_t va = t0 + head < t1 ? t0 + head : t1;
+  const uint64_t vb = va + (t1 - va) / 4 * 4;
+  const int world = P.world, epi = P.epi;
+  for (uint64_t i = va + 4 * (uint64_t)threadIdx.x; i < vb; i += 4 * CE_THREADS) {
+    float4 acc = ld4(reinterpret_cast<const float*>(ce_src(P, 0) + src + 4 * i));
+    for (int q = 1; q < world; ++q)
+      acc = add4(acc, ld4(reinterpret_cast<const float*>(ce_src(P, q) + src + 4 * i)));
+    float4* o = reinterpret_cast<float4*>(P.out + dst + 4 * i);
+    const float4 th = epi == CARAMEL_EPI_SGD ? *o : acc;
+    *o = epi4(epi, acc, th, scale, lr);
+  }
+  // scalar head [t0, va) and tail [vb, t1)
+  const uint64_t nh = va - t0, nt = t1 - vb;
+  if (threadIdx.x < nh + nt) {
+    const uint64_t i = threadIdx.x < nh ? t0 + threadIdx.x : vb + (threadIdx.x - nh);
+    float acc = *reinterpret_cast<const float*>(ce_src(P, 0) + src + 4 * i);
+    for (int q = 1; q < world; ++q) acc = __fadd_rn(acc, *reinterpret_cast<const float*>(ce_src(P, q) + src + 4 * i));
+    float* o = reinterpret_cast<float*>(P.out + dst + 4 * i);
+    *o = epi1(epi, acc, epi == CARAMEL_EPI_SGD ? *o : acc, scale, lr);
+  }
+}
+
 struct caramel_ctx {
   int rank, world, nlocal, device, sms;
   uint64_t arena_bytes, param_bytes;
@@ -2028,6 +2097,12 @@ struct caramel_ctx {
   int* status;
   uint32_t* epoch_dev;
   uint64_t timeout_ns;
+  // copy-engine two-shot (caramel_allreduce_ce), created on first use
+  bool ce_ready;
+  int ce_nstreams;
+  cudaStream_t ce_stream[MAXR];
+  cudaEvent_t ce_fork, ce_join[MAXR];
+  char* ce_staging;  // world-1 slots, each congruent to the bucket arena
 };
 
 struct Blob {
@@ -2245,6 +2320,14 @@ int caramel_finalize(caramel_ctx* c) {
     if (c->param_local[i]) cudaFree(c->param_local[i]);
   }
   if (c->status) cudaFree(c->status);
+  if (c->ce_ready) {
+    for (int k = 0; k < c->ce_nstreams; ++k) {
+      cudaStreamDestroy(c->ce_stream[k]);
+      cudaEventDestroy(c->ce_join[k]);
+    }
+    if (c->ce_nstreams) cudaEventDestroy(c->ce_fork);
+    cudaFree(c->ce_staging);
+  }
   free(c);
   return 0;
 }
@@ -2501,6 +2584,207 @@ int caramel_allreduce_many(caramel_ctx* c, const caramel_bucket* host, int32_t c
   }
   fn<<<grid, THREADS, 0, (cudaStream_t)stream>>>(P);
   CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// caramel_allreduce_ce: two-shot on the copy engines.  Per call (buckets
+// [index0, index0+count) of the iteration's launch order, tag = epoch:next):
+//   1. READY[me] = tag on every peer (stream write, fenced after my gradients)
+//   2. per peer q, on a copy stream: wait READY[q] >= tag in my sync words,
+//      copy q's gradients of my shards into staging slot q  (reduce-scatter)
+//   3. k_ce_reduce on `stream` (sum in rank order + epilogue, my shards)
+//   4. DONE[me] = tag on every peer
+//   5. per peer q: wait DONE[q] >= tag, copy q's result shards into my output
+//      arena (all-gather)
+// Tags are monotone in (epoch, launch position).  Every rank must group the
+// launch order into the same calls: a stream wait stalls the hardware queue it
+// sits in, and a queue shared with the stream that will later issue a READY
+// the peer is waiting for would otherwise close a cycle.  READY goes out on
+// the gradient stream, DONE(t) depends only on READY(<= t) and earlier DONEs.
+// ---------------------------------------------------------------------------
+typedef CUresult (*pfn_value64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+typedef CUresult (*pfn_dev_attr)(int*, CUdevice_attribute, CUdevice);
+typedef CUresult (*pfn_dev_get)(CUdevice*, int);
+static pfn_value64 g_wait64 = nullptr, g_write64 = nullptr;
+
+static bool ce_probe(const caramel_ctx* c) {
+  static int state = 0;  // 1 usable, -1 not
+  if (state) return state > 0;
+  state = -1;
+  void *fa = nullptr, *fg = nullptr, *fw = nullptr, *fs = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuDeviceGetAttribute", &fa, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return false;
+  if (cudaGetDriverEntryPoint("cuDeviceGet", &fg, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return false;
+  if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &fw, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return false;
+  if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &fs, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return false;
+  CUdevice d;
+  int v = 0;
+  if (((pfn_dev_get)fg)(&d, c->device) != CUDA_SUCCESS) return false;
+  if (((pfn_dev_attr)fa)(&v, CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, d) != CUDA_SUCCESS || !v) return false;
+  g_wait64 = (pfn_value64)fw;
+  g_write64 = (pfn_value64)fs;
+  state = 1;
+  return true;
+}
+
+static int ce_setup(caramel_ctx* c) {
+  if (c->ce_ready) return 0;
+  // Copies run on the caller's stream by default (one copy at a time already
+  // streams near the NVLink rate and costs no fork/join); CARAMEL_CE_STREAMS=k
+  // spreads the peers over k side streams instead.
+  int ns = 0;
+  if (const char* e = getenv("CARAMEL_CE_STREAMS")) {
+    int v = atoi(e);
+    ns = v < 0 ? 0 : (v > c->world - 1 ? c->world - 1 : v);
+  }
+  for (int k = 0; k < ns; ++k) CUDA_TRY(cudaStreamCreateWithFlags(&c->ce_stream[k], cudaStreamNonBlocking));
+  c->ce_nstreams = ns;
+  if (ns) {
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ce_fork, cudaEventDisableTiming));
+    for (int k = 0; k < ns; ++k) CUDA_TRY(cudaEventCreateWithFlags(&c->ce_join[k], cudaEventDisableTiming));
+  }
+  CUDA_TRY(cudaMalloc((void**)&c->ce_staging, (uint64_t)(c->world - 1) * c->arena_bytes));
+  c->ce_ready = true;
+  return 0;
+}
+
+static inline uint64_t shard_lo(uint64_t n, int p, int s) { return (n * (uint64_t)s) / (uint64_t)p; }
+
+static CUresult ce_wait(cudaStream_t s, uint64_t addr, uint64_t tag) {
+  return g_wait64((CUstream)s, (CUdeviceptr)addr, tag, CU_STREAM_WAIT_VALUE_GEQ);
+}
+static CUresult ce_signal(cudaStream_t s, uint64_t addr, uint64_t tag) {
+  return g_write64((CUstream)s, (CUdeviceptr)addr, tag, CU_STREAM_WRITE_VALUE_DEFAULT);  // fenced after prior work
+}
+
+#define CU_TRY(expr)                                                                         \
+  do {                                                                                       \
+    CUresult _r = (expr);                                                                    \
+    if (_r != CUDA_SUCCESS) return set_err(CARAMEL_ECUDA, "%s failed: CUresult %d", #expr, (int)_r); \
+  } while (0)
+
+int caramel_ce_available(caramel_ctx* c) {
+  return c && c->nlocal == 1 && c->world > 1 && ce_probe(c) ? 1 : 0;
+}
+
+int caramel_allreduce_ce(caramel_ctx* c, const caramel_bucket* host, int32_t count, uint32_t index0,
+                         uint32_t epoch, void* grad_stream, void* stream) {
+  if (!c || !host || count < 1) return set_err(CARAMEL_EINVAL, "allreduce_ce: null argument or empty list");
+  if (c->nlocal != 1 || c->world < 2) return set_err(CARAMEL_ESTATE, "allreduce_ce: one rank per process, world >= 2");
+  if (!c->imported) return set_err(CARAMEL_ESTATE, "peer arenas not mapped (call caramel_import)");
+  if (epoch == 0) return set_err(CARAMEL_EINVAL, "allreduce_ce: epoch must be > 0");
+  if (!ce_probe(c)) return set_err(CARAMEL_ESTATE, "allreduce_ce: device lacks 64-bit stream memory operations");
+  const int epi = host[0].epilogue;
+  for (int i = 0; i < count; ++i) {
+    const caramel_bucket& b = host[i];
+    if (b.pattern != CARAMEL_SHUFFLE) return set_err(CARAMEL_EINVAL, "allreduce_ce: SHUFFLE buckets only");
+    if (b.epilogue != epi || b.flags != host[0].flags)
+      return set_err(CARAMEL_EINVAL, "allreduce_ce: buckets must share epilogue and flags");
+    if (b.flags & (CARAMEL_F_PACK | CARAMEL_F_UNPACK))
+      return set_err(CARAMEL_EINVAL, "allreduce_ce: gradients must live in the bucket arena (no PACK/UNPACK)");
+    if (epi == CARAMEL_EPI_SGD && !(b.flags & CARAMEL_F_PARAM_ARENA))
+      return set_err(CARAMEL_EINVAL, "allreduce_ce: the SGD epilogue needs PARAM_ARENA");
+    if (b.numel > 0 && b.bucket_off + 4 * b.numel > c->arena_bytes)
+      return set_err(CARAMEL_EINVAL, "allreduce_ce: bucket exceeds the arena");
+    int rc = validate_bucket(c, &b);
+    if (rc) return rc;
+  }
+  int rc = ce_setup(c);
+  if (rc) return rc;
+  const int me = c->rank, p = c->world, ns = c->ce_nstreams;
+  const bool sgd = epi == CARAMEL_EPI_SGD;
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t tag = ((uint64_t)epoch << 32) | (uint64_t)(index0 + (uint32_t)count);
+  const uint64_t ready = c->arena_bytes + CE_FLAG_OFF, done = ready + 8 * MAXR;
+  auto slot = [&](int q) { return (uint64_t)(q < me ? q : q - 1); };
+  // 1-2: reduce-scatter on the copy engines.  READY goes out on the stream
+  // that produced the gradients, not behind this stream's all-gather waits.
+  cudaStream_t gs = grad_stream ? (cudaStream_t)grad_stream : s;
+  for (int q = 0; q < p; ++q)
+    if (q != me) CU_TRY(ce_signal(gs, c->arena[q] + ready + 8 * me, tag));
+  if (ns) {
+    CUDA_TRY(cudaEventRecord(c->ce_fork, s));
+    for (int k = 0; k < ns; ++k) CUDA_TRY(cudaStreamWaitEvent(c->ce_stream[k], c->ce_fork, 0));
+  }
+  for (int q = 0; q < p; ++q) {
+    if (q == me) continue;
+    cudaStream_t cs = ns ? c->ce_stream[slot(q) % ns] : s;
+    CU_TRY(ce_wait(cs, c->arena[me] + ready + 8 * q, tag));
+    for (int i = 0; i < count; ++i) {
+      const uint64_t lo = shard_lo(host[i].numel, p, me), hi = shard_lo(host[i].numel, p, me + 1);
+      if (hi <= lo) continue;
+      const uint64_t off = host[i].bucket_off + 4 * lo;
+      CUDA_TRY(cudaMemcpyAsync(c->ce_staging + slot(q) * c->arena_bytes + off, (const void*)(c->arena[q] + off),
+                               4 * (hi - lo), cudaMemcpyDeviceToDevice, cs));
+    }
+  }
+  for (int k = 0; k < ns; ++k) {
+    CUDA_TRY(cudaEventRecord(c->ce_join[k], c->ce_stream[k]));
+    CUDA_TRY(cudaStreamWaitEvent(s, c->ce_join[k], 0));
+  }
+  // 3: reduction + epilogue of my shards
+  for (int i0 = 0; i0 < count; i0 += CE_MAX_BUCKETS) {
+    CeParams P;
+    memset(&P, 0, sizeof(P));
+    P.arena = (const char*)c->arena[me];
+    P.staging = c->ce_staging;
+    P.out = (char*)(sgd ? c->parena[me] : c->arena[me]);
+    P.slot_bytes = c->arena_bytes;
+    P.world = p;
+    P.me = me;
+    P.epi = epi;
+    uint32_t ctas = 0;
+    for (int i = i0; i < count && i < i0 + CE_MAX_BUCKETS; ++i) {
+      const uint64_t lo = shard_lo(host[i].numel, p, me), hi = shard_lo(host[i].numel, p, me + 1);
+      if (hi <= lo) continue;
+      CeItem& it = P.it[P.count++];
+      it.src = host[i].bucket_off + 4 * lo;
+      it.dst = (sgd ? host[i].param_off : host[i].bucket_off) + 4 * lo;
+      it.n = hi - lo;
+      it.cta0 = ctas;
+      it.lr = host[i].lr;
+      it.scale = host[i].scale;
+      ctas += (uint32_t)((it.n + CE_TILE - 1) / CE_TILE);
+    }
+    if (ctas) {
+      k_ce_reduce<<<ctas, CE_THREADS, 0, s>>>(P);
+      CUDA_TRY(cudaGetLastError());
+    }
+  }
+  // 4-5: all-gather on the copy engines
+  for (int q = 0; q < p; ++q)
+    if (q != me) CU_TRY(ce_signal(s, c->arena[q] + done + 8 * me, tag));
+  if (ns) {
+    CUDA_TRY(cudaEventRecord(c->ce_fork, s));
+    for (int k = 0; k < ns; ++k) CUDA_TRY(cudaStreamWaitEvent(c->ce_stream[k], c->ce_fork, 0));
+  }
+  for (int q = 0; q < p; ++q) {
+    if (q == me) continue;
+    cudaStream_t cs = ns ? c->ce_stream[slot(q) % ns] : s;
+    CU_TRY(ce_wait(cs, c->arena[me] + done + 8 * q, tag));
+    const uint64_t base_peer = sgd ? c->parena[q] : c->arena[q];
+    char* base_me = (char*)(sgd ? c->parena[me] : c->arena[me]);
+    for (int i = 0; i < count; ++i) {
+      const uint64_t lo = shard_lo(host[i].numel, p, q), hi = shard_lo(host[i].numel, p, q + 1);
+      if (hi <= lo) continue;
+      const uint64_t off = (sgd ? host[i].param_off : host[i].bucket_off) + 4 * lo;
+      CUDA_TRY(cudaMemcpyAsync(base_me + off, (const void*)(base_peer + off), 4 * (hi - lo),
+                               cudaMemcpyDeviceToDevice, cs));
+    }
+  }
+  for (int k = 0; k < ns; ++k) {
+    CUDA_TRY(cudaEventRecord(c->ce_join[k], c->ce_stream[k]));
+    CUDA_TRY(cudaStreamWaitEvent(s, c->ce_join[k], 0));
+  }
   return 0;
 }
 

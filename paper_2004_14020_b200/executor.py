@@ -144,11 +144,22 @@ class Aggregator:
                every replica directly.
     epilogue : "sgd" (fused postponed update), "mean" or "sum" (gradient
                all-reduce, result written back into .grad).
+    engine   : overlapped-mode (hooks) engine.  "sm": the NVLink kernels
+               (caramel_allreduce / _many).  "ce": the copy-engine two-shot
+               (caramel_allreduce_ce) -- bytes move on the copy engines and
+               ranks wait on stream memory operations, so the backward kernels
+               keep every SM; needs grads="bucket", world > 1, SHUFFLE.
+               step() / step_host*() always use the SM kernels.
     """
 
     def __init__(self, plan: ExecPlan, params: dict[str, torch.Tensor], *, rank: int = 0, lr: float = 0.01,
                  epilogue: str = "sgd", param_arena: bool = True, grads: str = "flat", group=None,
-                 bootstrap: bool = True):
+                 bootstrap: bool = True, engine: str = "sm"):
+        if engine not in ("sm", "ce"):
+            raise ValueError("engine must be 'sm' or 'ce'")
+        if engine == "ce" and (grads != "bucket" or plan.world < 2 or plan.pattern != N.SHUFFLE):
+            raise ValueError("engine='ce' needs grads='bucket', world > 1 and the SHUFFLE pattern")
+        self.engine = engine
         self.plan = plan
         self.rank, self.world = rank, plan.world
         self.lr = float(lr)
@@ -169,6 +180,8 @@ class Aggregator:
             if len(set(digests)) != 1:
                 raise RuntimeError("ranks disagree on the execution plan (digest mismatch)")
             self.ctx.bootstrap(group)
+        if engine == "ce" and not N.lib().caramel_ce_available(self.ctx._ctx):
+            raise RuntimeError("engine='ce': this device lacks 64-bit stream memory operations")
         if self.param_arena:
             self._adopt_params()
         # Gradient storage:
@@ -210,6 +223,7 @@ class Aggregator:
         self._next = 0
         self._hooks = []
         self.epoch = 0
+        self._ce_epoch = 0
         self.launches = 0
         self._last_done = None
         self._fp_pending = set()
@@ -236,6 +250,8 @@ class Aggregator:
             # zero-copy: the bucket IS the gradient storage; results land in the
             # parameter arena (SGD) or in place (mean / sum; ring/hd unpack)
             flags = N.F_PARAM_ARENA if self.param_arena else N.F_UNPACK
+            if self.engine == "ce" and not self.param_arena:
+                flags = 0  # the copy-engine all-gather lands in the bucket = the gradients
         else:
             flags = N.F_PACK | (N.F_PARAM_ARENA if self.param_arena else N.F_UNPACK)
             if len(segs) == 1 and segs[0].grad % 16 == 0:
@@ -305,6 +321,17 @@ class Aggregator:
                                                self._dev_prefix.data_ptr() + 8 * i,
                                                self._dev_segprefix.data_ptr() + 8 * i, ctas, mode, 0,
                                                ctypes.c_void_p(stream)))
+        self.launches += 1
+
+    def _launch_ce(self, i: int, j: int, stream: int, grad_stream: int | None = None) -> None:
+        """Buckets [i, j) of the launch order on the copy engines
+        (caramel_allreduce_ce); READY is signalled on `grad_stream` (default:
+        the current stream, where autograd produced the gradients)."""
+        bsz = ctypes.sizeof(N.Bucket)
+        host = ctypes.cast(ctypes.byref(self._host_list, i * bsz), ctypes.POINTER(N.Bucket))
+        gs = grad_stream if grad_stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        N.check(N.lib().caramel_allreduce_ce(self.ctx._ctx, host, j - i, i, self._ce_epoch, ctypes.c_void_p(gs),
+                                             ctypes.c_void_p(stream)))
         self.launches += 1
 
     def host_groups(self, group_bytes: int = 16 << 20) -> list[tuple[int, int]]:
@@ -424,6 +451,7 @@ class Aggregator:
         self.comm_stream.wait_stream(cur)
         N.check(N.lib().caramel_epoch_advance(self.ctx._ctx,
                                               ctypes.c_void_p(self.comm_stream.cuda_stream)))
+        self._ce_epoch += 1
 
     #: overlapped mode: while the comm stream is busy, ready buckets are held
     #: back and coalesced into one list launch (per-bucket flags, so ranks may
@@ -444,6 +472,20 @@ class Aggregator:
         if j == self._next:
             return
         pending_bytes = 4 * (self._prefix[j] - self._prefix[self._next])
+        if self.engine == "ce":
+            # one call per bucket: every rank must group the launch order into
+            # the same calls (a stream-memory-op wait stalls its hardware queue)
+            cur = torch.cuda.current_stream(self.device)
+            self.comm_stream.wait_stream(cur)
+            for k in range(self._next, j):
+                self._launch_ce(k, k + 1, self.comm_stream.cuda_stream, cur.cuda_stream)
+            ev = torch.cuda.Event()  # the comm stream is FIFO: one event covers the run
+            ev.record(self.comm_stream)
+            for lv in self._live[self._next:j]:
+                lv.done = ev
+            self._last_done = ev
+            self._next = j
+            return
         if not force and self._comm_busy() and j - self._next < self.coalesce_buckets \
                 and pending_bytes < self.coalesce_bytes:
             return

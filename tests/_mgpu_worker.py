@@ -7,6 +7,8 @@ every rank over NCCL -- test plumbing only)."""
 from __future__ import annotations
 
 import os
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # before any CUDA context: one hardware queue per stream
 import sys
 from pathlib import Path
 
@@ -89,10 +91,12 @@ def main() -> int:
     failures += mixed_grouping_check(rank, world, dev)
     failures += overlapped_hooks_check(rank, world, dev)
     failures += overlapped_hooks_check(rank, world, dev, grads="bucket")
+    failures += ce_check(rank, world, dev)
+    failures += overlapped_hooks_check(rank, world, dev, grads="bucket", engine="ce")
     t = torch.tensor([failures], device=dev)
     dist.all_reduce(t)
     if rank == 0:
-        print(f"multigpu parity: world={world} cases={len(layout) * 6 + 3} failures={int(t.item())}", flush=True)
+        print(f"multigpu parity: world={world} cases={len(layout) * 6 + 5} failures={int(t.item())}", flush=True)
     dist.destroy_process_group()
     return 0 if int(t.item()) == 0 else 1
 
@@ -166,7 +170,84 @@ def mixed_grouping_check(rank: int, world: int, dev) -> int:
     return fails
 
 
-def overlapped_hooks_check(rank: int, world: int, dev, grads: str = "flat") -> int:
+def ce_check(rank: int, world: int, dev) -> int:
+    """Copy-engine two-shot (caramel_allreduce_ce) through the C ABI: six
+    buckets, gradients in the bucket arena, SUM and fused SGD, the same launch
+    order grouped differently per rank (rank 0: one call; odd ranks: one call
+    per bucket; others: two calls).  Bit-exact with the oracle's SHUFFLE order."""
+    import ctypes
+
+    rng = np.random.default_rng(500 + rank)
+    theta_rng = np.random.default_rng(9)
+    sizes = [1, 5, 300, 4099, 70_001, 1 << 20]
+    specs, off, poff = [], 0, 0
+    for n in sizes:
+        ctas, bbytes, fbytes = N.bucket_layout(n, 1, N.SHUFFLE, world)
+        boff = off
+        foff = (boff + bbytes + 255) // 256 * 256
+        off = (foff + fbytes + 255) // 256 * 256
+        specs.append((n, ctas, boff, foff, poff))
+        poff = (poff + 4 * n + 255) // 256 * 256
+    ctx = comm.Context(rank, world, arena_bytes=off, param_bytes=poff)
+    ctx.bootstrap()
+    if not N.lib().caramel_ce_available(ctx._ctx):
+        print(f"rank {rank}: copy-engine path unavailable on this device", flush=True)
+        ctx.close()
+        return 1
+    stream = torch.cuda.current_stream().cuda_stream  # gradients' stream: READY goes out here
+    side = torch.cuda.Stream()                         # the collective's stream
+    fails = 0
+    epoch = 0
+    for epi in (N.EPI_SUM, N.EPI_SGD):
+        for grouping in range(3):
+            epoch += 1
+            grads = [rng.standard_normal(n).astype(np.float32) for n in sizes]
+            theta = [theta_rng.standard_normal(n).astype(np.float32) for n in sizes]
+            descs = []
+            for (n, ctas, boff, foff, po), g, th in zip(specs, grads, theta):
+                ctx.arena_view(0, boff, n).copy_(torch.from_numpy(g).to(dev))
+                ctx.arena_view(0, po, n, param=True).copy_(torch.from_numpy(th).to(dev))
+                descs.append(comm.make_bucket(n, boff, foff, pattern=N.SHUFFLE, epilogue=epi, ctas=ctas,
+                                              flags=N.F_PARAM_ARENA if epi == N.EPI_SGD else 0, param_off=po,
+                                              lr=0.05, scale=1.0 / world))
+            host = (N.Bucket * len(descs))(*descs)
+            bsz = ctypes.sizeof(N.Bucket)
+
+            def call(i, j):
+                h = ctypes.cast(ctypes.byref(host, i * bsz), ctypes.POINTER(N.Bucket))
+                N.check(N.lib().caramel_allreduce_ce(ctx._ctx, h, j - i, i, epoch, ctypes.c_void_p(stream),
+                                                     ctypes.c_void_p(side.cuda_stream)))
+
+            torch.cuda.synchronize()
+            dist.barrier()
+            side.wait_stream(torch.cuda.current_stream())
+            if grouping == 0:
+                call(0, len(descs))
+            elif grouping == 1:
+                for i in range(len(descs)):
+                    call(i, i + 1)
+            else:
+                call(0, 3)
+                call(3, len(descs))
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            for i, (n, ctas, boff, foff, po) in enumerate(specs):
+                flat = torch.from_numpy(grads[i]).to(dev)
+                allg = [torch.empty_like(flat) for _ in range(world)]
+                dist.all_gather(allg, flat)
+                want = O.np_allreduce(N.SHUFFLE, [a.cpu().numpy() for a in allg], 1, epi, 1.0 / world, 0.05,
+                                      theta[i])
+                got = ctx.arena_view(0, po if epi == N.EPI_SGD else boff, n, param=epi == N.EPI_SGD).cpu().numpy()
+                if not np.array_equal(got.view(np.uint32), want.view(np.uint32)):
+                    fails += 1
+                    bad = np.nonzero(got.view(np.uint32) != want.view(np.uint32))[0]
+                    print(f"rank {rank}: copy-engine mismatch bucket {i} (n={n}) epi={epi} epoch {epoch}: "
+                          f"{bad.size} elems, first {bad[:5]}", flush=True)
+    ctx.close()
+    return fails
+
+
+def overlapped_hooks_check(rank: int, world: int, dev, grads: str = "flat", engine: str = "sm") -> int:
     """Real backward on every rank, buckets launched from gradient hooks in the
     enforced order, SGD fused into the all-gather; every replica must equal
     theta - lr * ((sum of all ranks' grads in rank order) * (1/p))."""
@@ -189,7 +270,8 @@ def overlapped_hooks_check(rank: int, world: int, dev, grads: str = "flat") -> i
                        SimConfig(workers=world, network=NetworkModel(10.0, 1e-4), reduce=ReduceModel(400.0, 10.0)))
     ids = [gradsets.param_id(i, len(tensors)) for i in range(len(tensors))]
     plan = lower(art, {pid: t.numel for pid, t in zip(ids, tensors)}, world, Pattern.SHUFFLE)
-    agg = Aggregator(plan, dict(zip(ids, model.parameters())), rank=rank, lr=lr, epilogue="sgd", grads=grads)
+    agg = Aggregator(plan, dict(zip(ids, model.parameters())), rank=rank, lr=lr, epilogue="sgd", grads=grads,
+                     engine=engine)
     agg.attach_hooks()
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
     fails = 0
@@ -219,7 +301,7 @@ def overlapped_hooks_check(rank: int, world: int, dev, grads: str = "flat") -> i
         for a, b in zip(model.parameters(), ref.parameters()):
             if not torch.equal(a, b):
                 fails += 1
-                print(f"rank {rank}: overlapped hooks ({grads}) mismatch at iteration {it}", flush=True)
+                print(f"rank {rank}: overlapped hooks ({grads}, {engine}) mismatch at iteration {it}", flush=True)
                 break
     agg.close()
     return fails

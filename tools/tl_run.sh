@@ -1,0 +1,8 @@
+set -x
+export PYTHONUNBUFFERED=1
+timeout 300 python -m pytest tests/test_multigpu.py -x -q -k two > gpurun_out/mg2.txt 2>&1
+for m in alexnet vgg16 resnet50; do
+  B=64; [ $m = vgg16 ] && B=32
+  timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29612 bench.py --gpus 2 --model $m --batch $B --no-cpu-baseline --no-sweep > gpurun_out/m_${m}_n2.json 2> gpurun_out/m_${m}_n2.err
+done
+echo done
