@@ -59,6 +59,8 @@ def parse_args():
                     help="gradient storage of the overlapped Aggregator (bucket = zero-copy)")
     ap.add_argument("--exposed-engine", default="both", choices=["sm", "ce", "both"],
                     help="overlapped-path engine(s) measured; 'both' reports each and the faster")
+    ap.add_argument("--ce-min-mb", type=float, default=None,
+                    help="copy-engine engine: buckets below this size use the SM kernels (default: Aggregator's)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the bucket-size sweep (N > 1)")
     ap.add_argument("--no-zero-copy", action="store_true", help="skip the zero-copy gradient variant")
     return ap.parse_args()
@@ -451,6 +453,8 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
     for engine in engines:
         agg = Aggregator(mplan, dict(ing.params), rank=rank, lr=LR, epilogue="sgd", grads=args.exposed_grads,
                          engine=engine)
+        if args.ce_min_mb is not None:
+            agg.ce_min_bytes = int(args.ce_min_mb * (1 << 20))
         gated = agg.gate_forward(ing.modules)
 
         def caramel_step():
@@ -546,6 +550,13 @@ def bucket_sweep(torch, dist, world, rank, dev, iters=20):
     comm._view_fp32(base, big // 4).normal_()
     stream = torch.cuda.current_stream()
     rows = []
+    # the copy-engine two-shot on its own context (same layout)
+    ce_ctx, ce_epoch = {}, {}
+    if N.lib().caramel_ce_available(ctx._ctx):
+        c = comm.Context(rank, world, arena_bytes=region + (32 << 20))
+        c.bootstrap()
+        comm._view_fp32(c.arena_ptrs(0)[0], big // 4).normal_()
+        ce_ctx["ce"], ce_epoch["ce"] = c, 0
     for k, size in enumerate(SWEEP_SIZES):
         n = size // 4
         depth = adaptive_depth(size, thr)
@@ -597,11 +608,26 @@ def bucket_sweep(torch, dist, world, rank, dev, iters=20):
         us_c, gc = timed(caramel)
         us_n, gn = timed(lambda st=None: dist.all_reduce(x))
         bus = 2 * (world - 1) / world * size / 1e3
-        rows.append({"bytes": size, "depth": depth, "caramel_us": round(us_c, 2),
-                     "caramel_bus_gbs": round(bus / us_c, 1), "nccl_us": round(us_n, 2),
-                     "nccl_bus_gbs": round(bus / us_n, 1), "graphed": [gc, gn]})
+        row = {"bytes": size, "depth": depth, "caramel_us": round(us_c, 2),
+               "caramel_bus_gbs": round(bus / us_c, 1), "nccl_us": round(us_n, 2),
+               "nccl_bus_gbs": round(bus / us_n, 1), "graphed": [gc, gn]}
+        if size >= (1 << 20) and ce_ctx:
+            # the copy-engine two-shot (eager: its host-side tags cannot replay)
+            for key, c in ce_ctx.items():
+                def ce_call(st=None, c=c):
+                    ce_epoch[key] += 1
+                    N.check(N.lib().caramel_allreduce_ce(c._ctx, ctypes.byref(b), 1, 0, ce_epoch[key],
+                                                         ctypes.c_void_p(stream.cuda_stream),
+                                                         ctypes.c_void_p(stream.cuda_stream)))
+                us_e, _ = timed(ce_call, graphed=False)
+                row[f"{key}_us"] = round(us_e, 2)
+                row[f"{key}_bus_gbs"] = round(bus / us_e, 1)
+        rows.append(row)
     ctx.status()
     ctx.close()
+    for c in ce_ctx.values():
+        c.status()
+        c.close()
     return rows
 
 

@@ -107,7 +107,9 @@ int caramel_chunk_bounds(uint64_t numel, int depth, int workers, uint64_t* out);
  * bucket region and bytes of its flag block.  Bucket region: shuffle = the
  * bucket itself (packed input, all-gathered in place); ring/hd = input and
  * partials + a second, output half (a fast neighbour never overwrites a
- * partial sum still to be pulled). */
+ * partial sum still to be pulled).  SHUFFLE with world > 1 adds world-1
+ * staging slots of ceil(numel/world)+3 elements (256-byte aligned, after the
+ * kernels' part) that peers' copy engines push into (caramel_allreduce_ce). */
 int caramel_bucket_layout(uint64_t numel, int depth, int pattern, int world,
                           int32_t* ctas, uint64_t* bucket_bytes,
                           uint64_t* flag_bytes);
@@ -194,10 +196,11 @@ int caramel_allreduce_many(caramel_ctx* ctx, const caramel_bucket* host, int32_t
 
 /* Copy-engine two-shot (the overlapped path's engine while backward kernels
  * own the SMs; same reference call it replaces, pipeline.py:94).  The NVLink
- * transfers of a two-shot run on the GPU's copy engines and the cross-rank
- * flags are stream memory operations, so no SM is held while bytes move or
- * while a rank waits for its peers; the reduction + epilogue is one short
- * kernel.  Buckets [0, count) of `host` are launch positions index0 ..
+ * transfers of a two-shot run on the GPU's copy engines (each rank pushes its
+ * gradients of peer q's shard into q's staging slot, then its result shard
+ * into every peer's output) and the cross-rank flags are stream memory
+ * operations, so no SM is held while bytes move or while a rank waits for
+ * its peers; the reduction + epilogue is one short kernel.  Buckets [0, count) of `host` are launch positions index0 ..
  * index0+count-1 of this iteration's launch order; every rank must make the
  * same sequence of calls (a stream wait stalls its hardware queue, so
  * differently grouped calls could wait on each other).  `epoch`: the

@@ -2034,54 +2034,54 @@ __global__ void __launch_bounds__(THREADS, 1) k_collective_many(const __grid_con
 #define CE_FLAG_OFF 4096  // byte offset of the READY / DONE words in the sync region
 
 struct CeItem {
-  uint64_t src;  // byte offset of my shard in the bucket arena (= in every staging slot)
-  uint64_t dst;  // byte offset of my shard in the output arena
-  uint64_t n;    // shard elements
-  uint32_t cta0; // first CTA of this bucket
+  uint64_t src;    // byte offset of my shard's first element in my bucket arena
+  uint64_t stg;    // byte offset of its staged copy in slot 0 (slot k at + k * slot)
+  uint64_t slot;   // staging slot bytes
+  uint64_t dst;    // byte offset of my shard in the output arena
+  uint64_t n;      // shard elements
+  uint32_t cta0;   // first CTA of this bucket
   float lr, scale;
 };
 
 struct CeParams {
-  const char* arena;    // my bucket arena
-  const char* staging;  // slot k holds rank (k < me ? k : k + 1)'s contribution
+  const char* arena;  // my bucket arena (own gradients + staging slots)
   char* out;
-  uint64_t slot_bytes;
   int world, me, count, epi;
   CeItem it[CE_MAX_BUCKETS];
 };
 
-__device__ __forceinline__ const char* ce_src(const CeParams& P, int q) {
-  return q == P.me ? P.arena : P.staging + (uint64_t)(q < P.me ? q : q - 1) * P.slot_bytes;
+// Input q of element i (shard-relative byte offset o = 4i): my own gradients,
+// or the slot rank q's copy engine pushed into (slot k = q < me ? q : q - 1).
+__device__ __forceinline__ const char* ce_in(const CeParams& P, const CeItem& I, int q) {
+  return q == P.me ? P.arena + I.src : P.arena + I.stg + (uint64_t)(q < P.me ? q : q - 1) * I.slot;
 }
 
 __global__ void __launch_bounds__(CE_THREADS) k_ce_reduce(const __grid_constant__ CeParams P) {
   int b = 0;
   while (b + 1 < P.count && blockIdx.x >= P.it[b + 1].cta0) ++b;
-  const uint64_t src = P.it[b].src, dst = P.it[b].dst, n = P.it[b].n;
-  const float lr = P.it[b].lr, scale = P.it[b].scale;
-  const uint64_t t0 = (uint64_t)(blockIdx.x - P.it[b].cta0) * CE_TILE;
-  const uint64_t t1 = t0 + CE_TILE < n ? t0 + CE_TILE : n;
+  const CeItem I = P.it[b];
+  const uint64_t t0 = (uint64_t)(blockIdx.x - I.cta0) * CE_TILE;
+  const uint64_t t1 = t0 + CE_TILE < I.n ? t0 + CE_TILE : I.n;
   // elements i with (src/4 + i) % 4 == 0 start a 16-byte vector in every input
-  const uint64_t head = (4 - ((src >> 2) & 3)) & 3;
-  uint64_t va = t0 + head < t1 ? t0 + head : t1;
+  const uint64_t head = (4 - ((I.src >> 2) & 3)) & 3;
+  const uint64_t va = t0 + head < t1 ? t0 + head : t1;
   const uint64_t vb = va + (t1 - va) / 4 * 4;
   const int world = P.world, epi = P.epi;
   for (uint64_t i = va + 4 * (uint64_t)threadIdx.x; i < vb; i += 4 * CE_THREADS) {
-    float4 acc = ld4(reinterpret_cast<const float*>(ce_src(P, 0) + src + 4 * i));
-    for (int q = 1; q < world; ++q)
-      acc = add4(acc, ld4(reinterpret_cast<const float*>(ce_src(P, q) + src + 4 * i)));
-    float4* o = reinterpret_cast<float4*>(P.out + dst + 4 * i);
+    float4 acc = ld4(reinterpret_cast<const float*>(ce_in(P, I, 0) + 4 * i));
+    for (int q = 1; q < world; ++q) acc = add4(acc, ld4(reinterpret_cast<const float*>(ce_in(P, I, q) + 4 * i)));
+    float4* o = reinterpret_cast<float4*>(P.out + I.dst + 4 * i);
     const float4 th = epi == CARAMEL_EPI_SGD ? *o : acc;
-    *o = epi4(epi, acc, th, scale, lr);
+    *o = epi4(epi, acc, th, I.scale, I.lr);
   }
   // scalar head [t0, va) and tail [vb, t1)
   const uint64_t nh = va - t0, nt = t1 - vb;
   if (threadIdx.x < nh + nt) {
     const uint64_t i = threadIdx.x < nh ? t0 + threadIdx.x : vb + (threadIdx.x - nh);
-    float acc = *reinterpret_cast<const float*>(ce_src(P, 0) + src + 4 * i);
-    for (int q = 1; q < world; ++q) acc = __fadd_rn(acc, *reinterpret_cast<const float*>(ce_src(P, q) + src + 4 * i));
-    float* o = reinterpret_cast<float*>(P.out + dst + 4 * i);
-    *o = epi1(epi, acc, epi == CARAMEL_EPI_SGD ? *o : acc, scale, lr);
+    float acc = *reinterpret_cast<const float*>(ce_in(P, I, 0) + 4 * i);
+    for (int q = 1; q < world; ++q) acc = __fadd_rn(acc, *reinterpret_cast<const float*>(ce_in(P, I, q) + 4 * i));
+    float* o = reinterpret_cast<float*>(P.out + I.dst + 4 * i);
+    *o = epi1(epi, acc, epi == CARAMEL_EPI_SGD ? *o : acc, I.scale, I.lr);
   }
 }
 
@@ -2099,10 +2099,8 @@ struct caramel_ctx {
   uint64_t timeout_ns;
   // copy-engine two-shot (caramel_allreduce_ce), created on first use
   bool ce_ready;
-  int ce_nstreams;
-  cudaStream_t ce_stream[MAXR];
-  cudaEvent_t ce_fork, ce_join[MAXR];
-  char* ce_staging;  // world-1 slots, each congruent to the bucket arena
+  cudaStream_t ce_send;  // reduce-scatter pushes + READY: never waits on a peer
+  cudaEvent_t ce_grads;  // gradients produced (recorded on the caller's grad stream)
 };
 
 struct Blob {
@@ -2153,6 +2151,24 @@ static int default_max_ctas() {
   return 64;
 }
 
+// Bucket region: the kernels' part (packed bucket; LL region; ring/hd halves),
+// then -- SHUFFLE, world > 1 -- world-1 staging slots where peers' copy
+// engines push their contributions to my shard (caramel_allreduce_ce).  A
+// slot holds ceil(n/p) elements after a (lo & 3)-element pad, so staged data
+// keeps the 16-byte phase of the shard it belongs to.
+static uint64_t kernel_region_bytes(uint64_t numel, int pattern, int world) {
+  const uint64_t e = out_region_elems(numel);
+  return use_ll(pattern, world, numel) ? (ll_region_bytes(numel, world) + 15) & ~15ull
+                                       : 4 * ((world > 1 && pattern != CARAMEL_SHUFFLE) ? 2 * e : e);
+}
+static uint64_t ce_slot_bytes(uint64_t numel, int world) {
+  const uint64_t m = (numel + world - 1) / world;
+  return (4 * (m + 3) + 15) & ~15ull;
+}
+static uint64_t ce_stage_off(uint64_t numel, int pattern, int world) {
+  return (kernel_region_bytes(numel, pattern, world) + 255) & ~255ull;
+}
+
 int caramel_bucket_layout(uint64_t numel, int depth, int pattern, int world, int32_t* ctas,
                           uint64_t* bucket_bytes, uint64_t* flag_bytes) {
   if (getenv("CARAMEL_LL_MAX")) h_ll_max = strtoull(getenv("CARAMEL_LL_MAX"), 0, 10);
@@ -2178,9 +2194,9 @@ int caramel_bucket_layout(uint64_t numel, int depth, int pattern, int world, int
   if (g < 1) g = 1;
   if (ctas) *ctas = (int32_t)g;
   if (bucket_bytes) {
-    const uint64_t e = out_region_elems(numel);
-    *bucket_bytes = use_ll(pattern, world, numel) ? (ll_region_bytes(numel, world) + 15) & ~15ull
-                                                  : 4 * ((world > 1 && pattern != CARAMEL_SHUFFLE) ? 2 * e : e);
+    *bucket_bytes = kernel_region_bytes(numel, pattern, world);
+    if (world > 1 && pattern == CARAMEL_SHUFFLE)  // + the copy-engine engine's staging slots
+      *bucket_bytes = ce_stage_off(numel, pattern, world) + (uint64_t)(world - 1) * ce_slot_bytes(numel, world);
   }
   if (flag_bytes) {
     uint64_t fb = world == 1 ? 0 : (uint64_t)depth * g * nslots(pattern, world) * world * 4;
@@ -2321,12 +2337,8 @@ int caramel_finalize(caramel_ctx* c) {
   }
   if (c->status) cudaFree(c->status);
   if (c->ce_ready) {
-    for (int k = 0; k < c->ce_nstreams; ++k) {
-      cudaStreamDestroy(c->ce_stream[k]);
-      cudaEventDestroy(c->ce_join[k]);
-    }
-    if (c->ce_nstreams) cudaEventDestroy(c->ce_fork);
-    cudaFree(c->ce_staging);
+    cudaStreamDestroy(c->ce_send);
+    cudaEventDestroy(c->ce_grads);
   }
   free(c);
   return 0;
@@ -2588,31 +2600,32 @@ int caramel_allreduce_many(caramel_ctx* c, const caramel_bucket* host, int32_t c
 }
 
 // ---------------------------------------------------------------------------
-// caramel_allreduce_ce: two-shot on the copy engines.  Per call (buckets
-// [index0, index0+count) of the iteration's launch order, tag = epoch:next):
-//   1. READY[me] = tag on every peer (stream write, fenced after my gradients)
-//   2. per peer q, on a copy stream: wait READY[q] >= tag in my sync words,
-//      copy q's gradients of my shards into staging slot q  (reduce-scatter)
-//   3. k_ce_reduce on `stream` (sum in rank order + epilogue, my shards)
-//   4. DONE[me] = tag on every peer
-//   5. per peer q: wait DONE[q] >= tag, copy q's result shards into my output
-//      arena (all-gather)
-// Tags are monotone in (epoch, launch position).  Every rank must group the
-// launch order into the same calls: a stream wait stalls the hardware queue it
-// sits in, and a queue shared with the stream that will later issue a READY
-// the peer is waiting for would otherwise close a cycle.  READY goes out on
-// the gradient stream, DONE(t) depends only on READY(<= t) and earlier DONEs.
+// caramel_allreduce_ce: two-shot on the copy engines, push-based (remote
+// writes stream faster than remote reads: ~690 vs ~420-640 GB/s per GPU on
+// 4 B200s, tools/ce_bw.py).  Per call (buckets [index0, index0+count) of the
+// iteration's launch order, tag = epoch:next position):
+//   1. send stream (after the gradients): push my gradients of peer q's shard
+//      into q's staging slot for me, for every q; READY[me] = tag on every peer
+//   2. `stream`: wait READY[q] >= tag for all q; k_ce_reduce (sum in rank
+//      order + epilogue) on my shards
+//   3. `stream`: push my result shards into every peer's output arena;
+//      DONE[me] = tag on every peer; wait DONE[q] >= tag for all q
+// Stream writes are fenced after the stream's prior work, so a peer that
+// sees a tag sees the bytes.  The send stream never waits on a peer, so READY
+// always goes out; DONE(t) depends only on READY(<= t) and earlier DONEs.
+// Every rank must group the launch order into the same calls (a stream wait
+// stalls its hardware queue; differently grouped waits could close a cycle).
 // ---------------------------------------------------------------------------
-typedef CUresult (*pfn_value64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+typedef CUresult (*pfn_batch)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int);
 typedef CUresult (*pfn_dev_attr)(int*, CUdevice_attribute, CUdevice);
 typedef CUresult (*pfn_dev_get)(CUdevice*, int);
-static pfn_value64 g_wait64 = nullptr, g_write64 = nullptr;
+static pfn_batch g_batch = nullptr;
 
 static bool ce_probe(const caramel_ctx* c) {
   static int state = 0;  // 1 usable, -1 not
   if (state) return state > 0;
   state = -1;
-  void *fa = nullptr, *fg = nullptr, *fw = nullptr, *fs = nullptr;
+  void *fa = nullptr, *fg = nullptr, *fw = nullptr;
   cudaDriverEntryPointQueryResult q;
   if (cudaGetDriverEntryPoint("cuDeviceGetAttribute", &fa, cudaEnableDefault, &q) != cudaSuccess ||
       q != cudaDriverEntryPointSuccess)
@@ -2620,50 +2633,48 @@ static bool ce_probe(const caramel_ctx* c) {
   if (cudaGetDriverEntryPoint("cuDeviceGet", &fg, cudaEnableDefault, &q) != cudaSuccess ||
       q != cudaDriverEntryPointSuccess)
     return false;
-  if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &fw, cudaEnableDefault, &q) != cudaSuccess ||
-      q != cudaDriverEntryPointSuccess)
-    return false;
-  if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &fs, cudaEnableDefault, &q) != cudaSuccess ||
+  if (cudaGetDriverEntryPoint("cuStreamBatchMemOp", &fw, cudaEnableDefault, &q) != cudaSuccess ||
       q != cudaDriverEntryPointSuccess)
     return false;
   CUdevice d;
   int v = 0;
   if (((pfn_dev_get)fg)(&d, c->device) != CUDA_SUCCESS) return false;
   if (((pfn_dev_attr)fa)(&v, CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, d) != CUDA_SUCCESS || !v) return false;
-  g_wait64 = (pfn_value64)fw;
-  g_write64 = (pfn_value64)fs;
+  g_batch = (pfn_batch)fw;
   state = 1;
   return true;
 }
 
 static int ce_setup(caramel_ctx* c) {
   if (c->ce_ready) return 0;
-  // Copies run on the caller's stream by default (one copy at a time already
-  // streams near the NVLink rate and costs no fork/join); CARAMEL_CE_STREAMS=k
-  // spreads the peers over k side streams instead.
-  int ns = 0;
-  if (const char* e = getenv("CARAMEL_CE_STREAMS")) {
-    int v = atoi(e);
-    ns = v < 0 ? 0 : (v > c->world - 1 ? c->world - 1 : v);
-  }
-  for (int k = 0; k < ns; ++k) CUDA_TRY(cudaStreamCreateWithFlags(&c->ce_stream[k], cudaStreamNonBlocking));
-  c->ce_nstreams = ns;
-  if (ns) {
-    CUDA_TRY(cudaEventCreateWithFlags(&c->ce_fork, cudaEventDisableTiming));
-    for (int k = 0; k < ns; ++k) CUDA_TRY(cudaEventCreateWithFlags(&c->ce_join[k], cudaEventDisableTiming));
-  }
-  CUDA_TRY(cudaMalloc((void**)&c->ce_staging, (uint64_t)(c->world - 1) * c->arena_bytes));
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->ce_send, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&c->ce_grads, cudaEventDisableTiming));
   c->ce_ready = true;
   return 0;
 }
 
 static inline uint64_t shard_lo(uint64_t n, int p, int s) { return (n * (uint64_t)s) / (uint64_t)p; }
 
-static CUresult ce_wait(cudaStream_t s, uint64_t addr, uint64_t tag) {
-  return g_wait64((CUstream)s, (CUdeviceptr)addr, tag, CU_STREAM_WAIT_VALUE_GEQ);
-}
-static CUresult ce_signal(cudaStream_t s, uint64_t addr, uint64_t tag) {
-  return g_write64((CUstream)s, (CUdeviceptr)addr, tag, CU_STREAM_WRITE_VALUE_DEFAULT);  // fenced after prior work
+// One stream memory-op batch: WRITE (fenced after the stream's prior work, so
+// a peer that sees the tag sees the data) or WAIT (>= tag, cyclic 64-bit) on
+// `n` addresses.
+static CUresult ce_memops(cudaStream_t s, bool wait, const uint64_t* addr, int n, uint64_t tag) {
+  CUstreamBatchMemOpParams ops[MAXR];
+  memset(ops, 0, sizeof(ops));
+  for (int i = 0; i < n; ++i) {
+    if (wait) {
+      ops[i].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_64;
+      ops[i].waitValue.address = (CUdeviceptr)addr[i];
+      ops[i].waitValue.value64 = tag;
+      ops[i].waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+    } else {
+      ops[i].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
+      ops[i].writeValue.address = (CUdeviceptr)addr[i];
+      ops[i].writeValue.value64 = tag;
+      ops[i].writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+    }
+  }
+  return n ? g_batch((CUstream)s, (unsigned)n, ops, 0) : CUDA_SUCCESS;
 }
 
 #define CU_TRY(expr)                                                                         \
@@ -2683,6 +2694,7 @@ int caramel_allreduce_ce(caramel_ctx* c, const caramel_bucket* host, int32_t cou
   if (!c->imported) return set_err(CARAMEL_ESTATE, "peer arenas not mapped (call caramel_import)");
   if (epoch == 0) return set_err(CARAMEL_EINVAL, "allreduce_ce: epoch must be > 0");
   if (!ce_probe(c)) return set_err(CARAMEL_ESTATE, "allreduce_ce: device lacks 64-bit stream memory operations");
+  const int me = c->rank, p = c->world;
   const int epi = host[0].epilogue;
   for (int i = 0; i < count; ++i) {
     const caramel_bucket& b = host[i];
@@ -2693,61 +2705,64 @@ int caramel_allreduce_ce(caramel_ctx* c, const caramel_bucket* host, int32_t cou
       return set_err(CARAMEL_EINVAL, "allreduce_ce: gradients must live in the bucket arena (no PACK/UNPACK)");
     if (epi == CARAMEL_EPI_SGD && !(b.flags & CARAMEL_F_PARAM_ARENA))
       return set_err(CARAMEL_EINVAL, "allreduce_ce: the SGD epilogue needs PARAM_ARENA");
-    if (b.numel > 0 && b.bucket_off + 4 * b.numel > c->arena_bytes)
-      return set_err(CARAMEL_EINVAL, "allreduce_ce: bucket exceeds the arena");
     int rc = validate_bucket(c, &b);
     if (rc) return rc;
+    const uint64_t end = b.bucket_off + ce_stage_off(b.numel, CARAMEL_SHUFFLE, p) + (uint64_t)(p - 1) * ce_slot_bytes(b.numel, p);
+    if (b.numel && end > c->arena_bytes)
+      return set_err(CARAMEL_EINVAL, "allreduce_ce: bucket + staging slots exceed the arena (size it with caramel_bucket_layout)");
   }
   int rc = ce_setup(c);
   if (rc) return rc;
-  const int me = c->rank, p = c->world, ns = c->ce_nstreams;
   const bool sgd = epi == CARAMEL_EPI_SGD;
   cudaStream_t s = (cudaStream_t)stream;
+  cudaStream_t gs = grad_stream ? (cudaStream_t)grad_stream : s;
   const uint64_t tag = ((uint64_t)epoch << 32) | (uint64_t)(index0 + (uint32_t)count);
   const uint64_t ready = c->arena_bytes + CE_FLAG_OFF, done = ready + 8 * MAXR;
-  auto slot = [&](int q) { return (uint64_t)(q < me ? q : q - 1); };
-  // 1-2: reduce-scatter on the copy engines.  READY goes out on the stream
-  // that produced the gradients, not behind this stream's all-gather waits.
-  cudaStream_t gs = grad_stream ? (cudaStream_t)grad_stream : s;
-  for (int q = 0; q < p; ++q)
-    if (q != me) CU_TRY(ce_signal(gs, c->arena[q] + ready + 8 * me, tag));
-  if (ns) {
-    CUDA_TRY(cudaEventRecord(c->ce_fork, s));
-    for (int k = 0; k < ns; ++k) CUDA_TRY(cudaStreamWaitEvent(c->ce_stream[k], c->ce_fork, 0));
-  }
+  uint64_t peer_ready[MAXR], my_ready[MAXR], peer_done[MAXR], my_done[MAXR];
+  int np_ = 0;
   for (int q = 0; q < p; ++q) {
     if (q == me) continue;
-    cudaStream_t cs = ns ? c->ce_stream[slot(q) % ns] : s;
-    CU_TRY(ce_wait(cs, c->arena[me] + ready + 8 * q, tag));
+    peer_ready[np_] = c->arena[q] + ready + 8 * me;
+    my_ready[np_] = c->arena[me] + ready + 8 * q;
+    peer_done[np_] = c->arena[q] + done + 8 * me;
+    my_done[np_] = c->arena[me] + done + 8 * q;
+    ++np_;
+  }
+  // 1. reduce-scatter: push my gradients of every peer's shard into that
+  //    peer's staging slot for me, then READY -- on the send stream, which
+  //    never waits on a peer (so READY can always go out)
+  CUDA_TRY(cudaEventRecord(c->ce_grads, gs));
+  CUDA_TRY(cudaStreamWaitEvent(c->ce_send, c->ce_grads, 0));
+  for (int r = 1; r < p; ++r) {
+    const int q = (me + r) % p;
+    const uint64_t k = (uint64_t)(me < q ? me : me - 1);  // my slot at q
     for (int i = 0; i < count; ++i) {
-      const uint64_t lo = shard_lo(host[i].numel, p, me), hi = shard_lo(host[i].numel, p, me + 1);
+      const uint64_t n = host[i].numel, lo = shard_lo(n, p, q), hi = shard_lo(n, p, q + 1);
       if (hi <= lo) continue;
-      const uint64_t off = host[i].bucket_off + 4 * lo;
-      CUDA_TRY(cudaMemcpyAsync(c->ce_staging + slot(q) * c->arena_bytes + off, (const void*)(c->arena[q] + off),
-                               4 * (hi - lo), cudaMemcpyDeviceToDevice, cs));
+      const uint64_t stg = host[i].bucket_off + ce_stage_off(n, CARAMEL_SHUFFLE, p) + k * ce_slot_bytes(n, p) + 4 * (lo & 3);
+      CUDA_TRY(cudaMemcpyAsync((void*)(c->arena[q] + stg), (const void*)(c->arena[me] + host[i].bucket_off + 4 * lo),
+                               4 * (hi - lo), cudaMemcpyDeviceToDevice, c->ce_send));
     }
   }
-  for (int k = 0; k < ns; ++k) {
-    CUDA_TRY(cudaEventRecord(c->ce_join[k], c->ce_stream[k]));
-    CUDA_TRY(cudaStreamWaitEvent(s, c->ce_join[k], 0));
-  }
-  // 3: reduction + epilogue of my shards
+  CU_TRY(ce_memops(c->ce_send, false, peer_ready, np_, tag));
+  // 2. every peer's contribution to my shards has landed: reduce + epilogue
+  CU_TRY(ce_memops(s, true, my_ready, np_, tag));
   for (int i0 = 0; i0 < count; i0 += CE_MAX_BUCKETS) {
     CeParams P;
     memset(&P, 0, sizeof(P));
     P.arena = (const char*)c->arena[me];
-    P.staging = c->ce_staging;
     P.out = (char*)(sgd ? c->parena[me] : c->arena[me]);
-    P.slot_bytes = c->arena_bytes;
     P.world = p;
     P.me = me;
     P.epi = epi;
     uint32_t ctas = 0;
     for (int i = i0; i < count && i < i0 + CE_MAX_BUCKETS; ++i) {
-      const uint64_t lo = shard_lo(host[i].numel, p, me), hi = shard_lo(host[i].numel, p, me + 1);
+      const uint64_t n = host[i].numel, lo = shard_lo(n, p, me), hi = shard_lo(n, p, me + 1);
       if (hi <= lo) continue;
       CeItem& it = P.it[P.count++];
       it.src = host[i].bucket_off + 4 * lo;
+      it.stg = host[i].bucket_off + ce_stage_off(n, CARAMEL_SHUFFLE, p) + 4 * (lo & 3);
+      it.slot = ce_slot_bytes(n, p);
       it.dst = (sgd ? host[i].param_off : host[i].bucket_off) + 4 * lo;
       it.n = hi - lo;
       it.cta0 = ctas;
@@ -2760,31 +2775,22 @@ int caramel_allreduce_ce(caramel_ctx* c, const caramel_bucket* host, int32_t cou
       CUDA_TRY(cudaGetLastError());
     }
   }
-  // 4-5: all-gather on the copy engines
-  for (int q = 0; q < p; ++q)
-    if (q != me) CU_TRY(ce_signal(s, c->arena[q] + done + 8 * me, tag));
-  if (ns) {
-    CUDA_TRY(cudaEventRecord(c->ce_fork, s));
-    for (int k = 0; k < ns; ++k) CUDA_TRY(cudaStreamWaitEvent(c->ce_stream[k], c->ce_fork, 0));
-  }
-  for (int q = 0; q < p; ++q) {
-    if (q == me) continue;
-    cudaStream_t cs = ns ? c->ce_stream[slot(q) % ns] : s;
-    CU_TRY(ce_wait(cs, c->arena[me] + done + 8 * q, tag));
-    const uint64_t base_peer = sgd ? c->parena[q] : c->arena[q];
-    char* base_me = (char*)(sgd ? c->parena[me] : c->arena[me]);
+  // 3. all-gather: push my result shards into every peer's output arena, DONE,
+  //    and wait until every peer's shards have landed here
+  const uint64_t out_me = sgd ? c->parena[me] : c->arena[me];
+  for (int r = 1; r < p; ++r) {
+    const int q = (me + r) % p;
+    const uint64_t out_q = sgd ? c->parena[q] : c->arena[q];
     for (int i = 0; i < count; ++i) {
-      const uint64_t lo = shard_lo(host[i].numel, p, q), hi = shard_lo(host[i].numel, p, q + 1);
+      const uint64_t n = host[i].numel, lo = shard_lo(n, p, me), hi = shard_lo(n, p, me + 1);
       if (hi <= lo) continue;
       const uint64_t off = (sgd ? host[i].param_off : host[i].bucket_off) + 4 * lo;
-      CUDA_TRY(cudaMemcpyAsync(base_me + off, (const void*)(base_peer + off), 4 * (hi - lo),
-                               cudaMemcpyDeviceToDevice, cs));
+      CUDA_TRY(cudaMemcpyAsync((void*)(out_q + off), (const void*)(out_me + off), 4 * (hi - lo),
+                               cudaMemcpyDeviceToDevice, s));
     }
   }
-  for (int k = 0; k < ns; ++k) {
-    CUDA_TRY(cudaEventRecord(c->ce_join[k], c->ce_stream[k]));
-    CUDA_TRY(cudaStreamWaitEvent(s, c->ce_join[k], 0));
-  }
+  CU_TRY(ce_memops(s, false, peer_done, np_, tag));
+  CU_TRY(ce_memops(s, true, my_done, np_, tag));
   return 0;
 }
 

@@ -144,19 +144,22 @@ class Aggregator:
                every replica directly.
     epilogue : "sgd" (fused postponed update), "mean" or "sum" (gradient
                all-reduce, result written back into .grad).
-    engine   : overlapped-mode (hooks) engine.  "sm": the NVLink kernels
+    engine   : overlapped-mode (hooks) engine; "auto" picks "ce" where it
+               applies (zero-copy gradients, world > 1, SHUFFLE), else "sm".
+               "sm": the NVLink kernels
                (caramel_allreduce / _many).  "ce": the copy-engine two-shot
                (caramel_allreduce_ce) -- bytes move on the copy engines and
                ranks wait on stream memory operations, so the backward kernels
-               keep every SM; needs grads="bucket", world > 1, SHUFFLE.
+               keep every SM; buckets under `ce_min_bytes` still take the SM
+               kernels.  Needs grads="bucket", world > 1, SHUFFLE.
                step() / step_host*() always use the SM kernels.
     """
 
     def __init__(self, plan: ExecPlan, params: dict[str, torch.Tensor], *, rank: int = 0, lr: float = 0.01,
                  epilogue: str = "sgd", param_arena: bool = True, grads: str = "flat", group=None,
-                 bootstrap: bool = True, engine: str = "sm"):
-        if engine not in ("sm", "ce"):
-            raise ValueError("engine must be 'sm' or 'ce'")
+                 bootstrap: bool = True, engine: str = "auto"):
+        if engine not in ("auto", "sm", "ce"):
+            raise ValueError("engine must be 'auto', 'sm' or 'ce'")
         if engine == "ce" and (grads != "bucket" or plan.world < 2 or plan.pattern != N.SHUFFLE):
             raise ValueError("engine='ce' needs grads='bucket', world > 1 and the SHUFFLE pattern")
         self.engine = engine
@@ -182,6 +185,10 @@ class Aggregator:
             self.ctx.bootstrap(group)
         if engine == "ce" and not N.lib().caramel_ce_available(self.ctx._ctx):
             raise RuntimeError("engine='ce': this device lacks 64-bit stream memory operations")
+        if engine == "auto":
+            ok = grads == "bucket" and self.world > 1 and plan.pattern == N.SHUFFLE
+            engine = "ce" if ok and N.lib().caramel_ce_available(self.ctx._ctx) else "sm"
+        self.engine = engine
         if self.param_arena:
             self._adopt_params()
         # Gradient storage:
@@ -459,6 +466,9 @@ class Aggregator:
     coalesce_buckets = 16
     coalesce_bytes = 8 << 20
     coalesce_ctas = 32  # grid of a coalesced launch: leave SMs to the backward pass
+    #: engine="ce": buckets below this size still run on the SM kernels (their
+    #: latency is lower and they hold SMs only for microseconds)
+    ce_min_bytes = 8 << 20
 
     def _comm_busy(self) -> bool:
         return self._last_done is not None and not self._last_done.query()
@@ -474,11 +484,24 @@ class Aggregator:
         pending_bytes = 4 * (self._prefix[j] - self._prefix[self._next])
         if self.engine == "ce":
             # one call per bucket: every rank must group the launch order into
-            # the same calls (a stream-memory-op wait stalls its hardware queue)
+            # the same calls (a stream-memory-op wait stalls its hardware queue);
+            # the engine choice per bucket is by size, identical on every rank
             cur = torch.cuda.current_stream(self.device)
             self.comm_stream.wait_stream(cur)
-            for k in range(self._next, j):
-                self._launch_ce(k, k + 1, self.comm_stream.cuda_stream, cur.cuda_stream)
+            k = self._next
+            while k < j:
+                if 4 * self._live[k].spec.numel >= self.ce_min_bytes:
+                    self._launch_ce(k, k + 1, self.comm_stream.cuda_stream, cur.cuda_stream)
+                    k += 1
+                    continue
+                e = k  # a run of small buckets: one SM list launch (per-bucket flags)
+                while e < j and 4 * self._live[e].spec.numel < self.ce_min_bytes:
+                    e += 1
+                if e - k == 1:
+                    self._launch(self._live[k], self.comm_stream.cuda_stream)
+                else:
+                    self._launch_range(k, e, self.comm_stream.cuda_stream, N.MANY_FLAGS, 0)
+                k = e
             ev = torch.cuda.Event()  # the comm stream is FIFO: one event covers the run
             ev.record(self.comm_stream)
             for lv in self._live[self._next:j]:

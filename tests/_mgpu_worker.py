@@ -272,6 +272,8 @@ def overlapped_hooks_check(rank: int, world: int, dev, grads: str = "flat", engi
     plan = lower(art, {pid: t.numel for pid, t in zip(ids, tensors)}, world, Pattern.SHUFFLE)
     agg = Aggregator(plan, dict(zip(ids, model.parameters())), rank=rank, lr=lr, epilogue="sgd", grads=grads,
                      engine=engine)
+    if engine == "ce":
+        agg.ce_min_bytes = 4 * 1024 if world % 2 == 0 else 0  # mixed SM / copy-engine buckets, or all copy-engine
     agg.attach_hooks()
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
     fails = 0

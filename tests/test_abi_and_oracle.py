@@ -79,7 +79,10 @@ def test_chunk_rule_agrees_with_reference_float_bytes():
 def test_bucket_layout_and_errors():
     N = _lib()
     ctas, bb, fb = N.bucket_layout(1 << 20, 2, N.SHUFFLE, 8)
-    assert 1 <= ctas <= 64 and bb == 4 << 20 and fb > 0
+    # packed bucket + 7 copy-engine staging slots of ceil(n/8)+3 elements
+    slot = (4 * ((1 << 20) // 8 + 3) + 15) & ~15
+    assert 1 <= ctas <= 64 and bb == (4 << 20) + 7 * slot and fb > 0
+    assert N.bucket_layout(1 << 20, 2, N.SHUFFLE, 1)[1] == 4 << 20  # one rank: no staging
     _, bb_ring, _ = N.bucket_layout(1 << 20, 2, N.RING, 8)
     assert bb_ring == 8 << 20  # input + output halves
     with pytest.raises(N.CaramelError, match="power-of-two"):

@@ -73,6 +73,8 @@ agg = Aggregator(plan, dict(ing.params), rank=rank, lr=0.01, epilogue="sgd", gra
                  engine=os.environ.get("ENGINE", "sm"))
 gated = agg.gate_forward(ing.modules)
 cap = int(os.environ.get("HOOK_CTAS", "0"))
+if "CE_MIN" in os.environ:
+    agg.ce_min_bytes = int(os.environ["CE_MIN"])
 if cap:
     agg.coalesce_ctas = cap
 launches = []
