@@ -731,8 +731,7 @@ def run_caramel(args) -> int:
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
     roof.update({"achieved": round(achieved, 1), "frac": round(achieved / roof["peak"], 4),
                  "traffic": None,
-                 "kernel": ("k_local_many" if world == 1 else
-                            "k_shuffle_fused" if args.pattern == "shuffle" else "k_collective_many") + " (caramel.cu)",
+                 "kernel": agg.step_kernel() + " (caramel.cu)",
                  "launches_per_step": 1,
                  "kernel_ms_per_step": round(kern_ms, 4),
                  "alg_bytes_per_step": alg_bytes,

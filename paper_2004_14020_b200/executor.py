@@ -30,6 +30,7 @@ from __future__ import annotations
 import ctypes
 import hashlib
 import json
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -426,6 +427,17 @@ class Aggregator:
                         host_params[pid].copy_(self.params[pid].view(-1), non_blocking=True)
         cur.wait_stream(d2h)
         return launches
+
+    def step_kernel(self) -> str:
+        """Name of the kernel step() launches (mirrors caramel_allreduce_many's dispatch)."""
+        if self.world > 1:
+            return "k_shuffle_fused" if self.plan.pattern == N.SHUFFLE else "k_collective_many"
+        tma = len(self._live) <= 256 and not os.environ.get("CARAMEL_NO_TMA")
+        for lv in self._live:
+            d = lv.desc
+            flat_ok = (d.flags & N.F_FLAT and d.flags & N.F_PACK and d.nseg == 1) or not d.flags & N.F_PACK
+            tma = tma and bool(flat_ok) and bool(d.flags & N.F_PARAM_ARENA) and d.epilogue == N.EPI_SGD
+        return "k_local_flat_tma" if tma else "k_local_many"
 
     def kernels_per_step(self, fused: bool = True) -> int:
         return 2 if fused else 1 + len(self._live)
