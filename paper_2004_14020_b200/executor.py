@@ -91,22 +91,30 @@ class ExecPlan:
 def lower(art: PipelineArtifacts, numels: dict[str, int], world: int, pattern: Pattern = Pattern.SHUFFLE,
           max_ctas: int | None = None) -> ExecPlan:
     """Rank-invariant launch plan of a pipeline run (see module docstring)."""
-    code = PATTERN_CODE[pattern]
     groups = {g.group_id: g for g in art.batch_plan.groups}
     launch = [t for t in art.transfer_schedule.transfers]
     if {t.group_id for t in launch} != set(groups):
         raise ValueError("transfer schedule and batch plan disagree")
-    placement = {t.group_id: t.placement.value for t in launch}
+    rows = [(t.group_id, tuple(groups[t.group_id].param_ids), groups[t.group_id].total_bytes,
+             int(art.depths[t.group_id]), t.placement.value, groups[t.group_id].ready_time_us) for t in launch]
+    return lower_groups(rows, numels, world, pattern, max_ctas)
+
+
+def lower_groups(rows, numels: dict[str, int], world: int, pattern: Pattern = Pattern.SHUFFLE,
+                 max_ctas: int | None = None) -> ExecPlan:
+    """ExecPlan from buckets in launch order: rows of (group_id, param_ids,
+    total_bytes, depth, placement, ready_time_us) -- from a pipeline run
+    (lower) or from persisted plan files (planio.load_exec_plan)."""
+    code = PATTERN_CODE[pattern]
     buckets = []
     off = 0
     poff = 0
-    for idx, t in enumerate(launch):
-        g = groups[t.group_id]
-        ns = tuple(int(numels[p]) for p in g.param_ids)
+    for idx, (gid, pids, total_bytes, depth, placement, ready) in enumerate(rows):
+        ns = tuple(int(numels[p]) for p in pids)
         n = sum(ns)
-        if 4 * n != g.total_bytes:
-            raise ValueError(f"{g.group_id}: fp32 member sizes {4 * n} B != planned {g.total_bytes} B")
-        depth = int(art.depths[g.group_id])
+        if 4 * n != total_bytes:
+            raise ValueError(f"{gid}: fp32 member sizes {4 * n} B != planned {total_bytes} B")
+        depth = int(depth)
         ctas, bbytes, _ = N.bucket_layout(n, depth, code, world)
         if max_ctas:
             ctas = max(1, min(ctas, max_ctas))
@@ -114,10 +122,9 @@ def lower(art: PipelineArtifacts, numels: dict[str, int], world: int, pattern: P
         boff = off
         foff = _align(boff + bbytes)
         off = _align(foff + fbytes)
-        buckets.append(ExecBucket(index=idx, group_id=g.group_id, param_ids=tuple(g.param_ids), numels=ns,
+        buckets.append(ExecBucket(index=idx, group_id=gid, param_ids=tuple(pids), numels=ns,
                                   numel=n, depth=depth, ctas=ctas, bucket_off=boff, flag_off=foff,
-                                  param_off=poff, placement=placement[g.group_id],
-                                  ready_time_us=g.ready_time_us))
+                                  param_off=poff, placement=placement, ready_time_us=float(ready)))
         poff = _align(poff + 4 * n)
     return ExecPlan(world=world, pattern=code, buckets=tuple(buckets), arena_bytes=max(off, ALIGN),
                     param_bytes=max(poff, ALIGN), total_numel=sum(b.numel for b in buckets))
