@@ -38,6 +38,7 @@ NVLINK_MODEL = (10.0, 1.0 / 460e3)      # latency us, us/B (SURVEY §8a "NVLink-
 REDUCE_MODEL = (400.0, 10.0)            # CLI defaults (cli.py:102-105); only shapes the modelled times
 NVLINK_PEAK_GBS = 770.0                 # B200_PROFILING.md measured peer copy per direction (fallback)
 NVLINK_NOMINAL_GBS = 900.0
+E2E_GROUP = 16 << 20                    # host-path pipelining granularity (H2D / kernel / D2H per group)
 LR = 0.1
 MODEL_INDEX = {"vgg16": 0, "resnet50": 1, "inception_v3": 2, "alexnet": 3}
 
@@ -62,7 +63,10 @@ def parse_args():
     ap.add_argument("--ce-min-mb", type=float, default=None,
                     help="copy-engine engine: buckets below this size use the SM kernels (default: Aggregator's)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the bucket-size sweep (N > 1)")
-    ap.add_argument("--no-zero-copy", action="store_true", help="skip the zero-copy gradient variant")
+    ap.add_argument("--grads", default="bucket", choices=["bucket", "flat"],
+                    help="gradient layout of the measured Aggregator: bucket = zero-copy (gradients live in the "
+                         "symmetric buckets, like DDP gradient_as_bucket_view), flat = one flat buffer + pack")
+    ap.add_argument("--no-zero-copy", action="store_true", help="skip the other gradient layout's variant")
     return ap.parse_args()
 
 
@@ -659,7 +663,7 @@ def run_caramel(args) -> int:
     grads_h = {pid: g.standard_normal(t.numel, dtype=np.float32) for pid, t in zip(ids, tensors)}
     shapes = {pid: t.shape for pid, t in zip(ids, tensors)}
     params = {pid: torch.from_numpy(params_h[pid]).to(dev).view(shapes[pid]) for pid in ids}
-    agg = Aggregator(plan, params, rank=rank, lr=LR, epilogue="sgd", param_arena=True)
+    agg = Aggregator(plan, params, rank=rank, lr=LR, epilogue="sgd", param_arena=True, grads=args.grads)
     for pid in ids:
         params[pid].grad.copy_(torch.from_numpy(grads_h[pid]).view(shapes[pid]))
     nbytes = 4 * plan.total_numel
@@ -742,40 +746,49 @@ def run_caramel(args) -> int:
         roof["traffic"] = json.loads(tr.read_text()).get(key)
 
     # ---- e2e: through the public API with host buffers --------------------
-    # Aggregator.step_host_flat: pinned host gradients in, updated parameters
-    # out (flat, arena layout), H2D / kernels / D2H pipelined per ~16 MB group
-    pinned_g = torch.zeros(plan.param_bytes // 4).pin_memory()
-    pinned_p = torch.zeros(plan.param_bytes // 4).pin_memory()
-    for pid, off, n in agg.flat_layout():
-        pinned_g[off:off + n].copy_(torch.from_numpy(grads_h[pid]))
-    for _ in range(2):
-        agg.step_host_flat(pinned_g, pinned_p)
-    torch.cuda.synchronize()
-    barrier()
-    e2e_steps = max(3, min(args.steps, 20))
-    s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s2.record()
-    e2e_launches = 0
-    for _ in range(e2e_steps):
-        e2e_launches += agg.step_host_flat(pinned_g, pinned_p)
-    e2.record()
-    e2.synchronize()
-    e2e_ms = s2.elapsed_time(e2) / e2e_steps
-    if dist is not None:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = t.item()
-    agg.status()
-    e2e = {"value": round(world * nbytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
-           "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": round(e2e_ms, 4),
-           "api": "Aggregator.step_host_flat (pinned host grads -> fused aggregation + SGD -> pinned host params)",
-           "groups": len(agg.host_groups()), "launches_per_step": e2e_launches // e2e_steps}
+    def measure_e2e(hagg):
+        """Aggregator.step_host_flat on a flat-layout Aggregator (host buffers
+        are flat; one H2D per group of buckets)."""
+        # Aggregator.step_host_flat: pinned host gradients in, updated parameters
+        # out (flat, arena layout), H2D / kernels / D2H pipelined per ~16 MB group
+        pinned_g = torch.zeros(plan.param_bytes // 4).pin_memory()
+        pinned_p = torch.zeros(plan.param_bytes // 4).pin_memory()
+        for pid, off, n in hagg.flat_layout():
+            pinned_g[off:off + n].copy_(torch.from_numpy(grads_h[pid]))
+        for _ in range(2):
+            hagg.step_host_flat(pinned_g, pinned_p, group_bytes=E2E_GROUP)
+        torch.cuda.synchronize()
+        barrier()
+        e2e_steps = max(3, min(args.steps, 20))
+        s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s2.record()
+        e2e_launches = 0
+        for _ in range(e2e_steps):
+            e2e_launches += hagg.step_host_flat(pinned_g, pinned_p, group_bytes=E2E_GROUP)
+        e2.record()
+        e2.synchronize()
+        e2e_ms = s2.elapsed_time(e2) / e2e_steps
+        if dist is not None:
+            t = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = t.item()
+        hagg.status()
+        e2e = {"value": round(world * nbytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": round(e2e_ms, 4),
+               "api": "Aggregator.step_host_flat (pinned host grads -> fused aggregation + SGD -> pinned host params)",
+               "groups": len(hagg.host_groups(E2E_GROUP)), "launches_per_step": e2e_launches // e2e_steps,
+               "grads": hagg.grads}
+        return e2e
 
-    # ---- zero-copy variant: gradients live in the symmetric buckets ----------
-    zero_copy = None
+    # ---- the other gradient layout: packed (flat buffer + K1 pack phase) or
+    # zero-copy (gradients live in the symmetric buckets) -----------------------
+    variant = None
+    e2e = measure_e2e(agg) if args.grads == "flat" else None
+    other = "flat" if args.grads == "bucket" else "bucket"
+    vkey = "packed" if other == "flat" else "zero_copy"
     if not args.no_zero_copy:
         zparams = {pid: torch.from_numpy(params_h[pid]).to(dev).view(shapes[pid]) for pid in ids}
-        zagg = Aggregator(plan, zparams, rank=rank, lr=LR, epilogue="sgd", param_arena=True, grads="bucket")
+        zagg = Aggregator(plan, zparams, rank=rank, lr=LR, epilogue="sgd", param_arena=True, grads=other)
         for pid in ids:
             zparams[pid].grad.copy_(torch.from_numpy(grads_h[pid]).view(shapes[pid]))
         zg = torch.cuda.CUDAGraph()
@@ -804,13 +817,19 @@ def run_caramel(args) -> int:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             zms = t.item()
         zagg.status()
-        zero_copy = {"ms_per_step": round(zms, 4), "value": round(world * nbytes / (zms * 1e-3) / 1e9, 3),
-                     "bus_gbs": round(plan.bus_bytes() / (zms * 1e-3) / 1e9, 1) if world > 1 else None,
-                     "what": "Aggregator(grads='bucket'): autograd writes gradients straight into the symmetric "
-                             "NVLink-mapped buckets, no pack phase"}
+        if other == "flat":
+            e2e = measure_e2e(zagg)
+        variant = {"ms_per_step": round(zms, 4), "value": round(world * nbytes / (zms * 1e-3) / 1e9, 3),
+                   "bus_gbs": round(plan.bus_bytes() / (zms * 1e-3) / 1e9, 1) if world > 1 else None,
+                   "what": ("Aggregator(grads='flat'): gradients in one flat buffer, packed into the buckets "
+                            "by the kernel's phase 0" if other == "flat" else
+                            "Aggregator(grads='bucket'): autograd writes gradients straight into the symmetric "
+                            "NVLink-mapped buckets, no pack phase")}
         del zg
         zagg.close()
         del zparams
+    if e2e is None:
+        e2e = measure_e2e(agg)
 
     # ---- NCCL bucketed baseline (N > 1) -------------------------------------
     nccl = None
@@ -887,8 +906,8 @@ def run_caramel(args) -> int:
         "warmup": max(3, args.warmup), "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{args.model} fp32 gradient set ({len(tensors)} tensors, {nbytes / 1e6:.1f} MB/GPU): "
-                               f"Caramel plan -> pack + {args.pattern} all-reduce + fused SGD update",
-                   "model": args.model, "pattern": args.pattern, "buckets": len(plan.buckets),
+                               f"Caramel plan -> {'pack + ' if args.grads == 'flat' else ''}{args.pattern} all-reduce + fused SGD update",
+                   "model": args.model, "pattern": args.pattern, "grads": args.grads, "buckets": len(plan.buckets),
                    "depths": sorted({b.depth for b in plan.buckets}), "parallelism": f"dp{world}",
                    "l2": "working set (grads + params) > 126 MB L2; no flush", "graph": "CUDA graph per step",
                    "network_model": {"latency_us": NVLINK_MODEL[0], "per_byte_us": NVLINK_MODEL[1]},
@@ -897,7 +916,7 @@ def run_caramel(args) -> int:
         "exposed_comm_ms_per_iter": exposed["caramel_exposed_ms"] if exposed else None,
         "exposed_comm": exposed,
         "bucket_sweep": sweep,
-        "zero_copy": zero_copy,
+        vkey: variant,
         "calibrated_network_model": calibrated,
         "roofline": roof,
         "cpu_baseline": cpu,

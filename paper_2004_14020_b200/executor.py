@@ -164,7 +164,7 @@ class Aggregator:
     """
 
     def __init__(self, plan: ExecPlan, params: dict[str, torch.Tensor], *, rank: int = 0, lr: float = 0.01,
-                 epilogue: str = "sgd", param_arena: bool = True, grads: str = "flat", group=None,
+                 epilogue: str = "sgd", param_arena: bool = True, grads: str = "bucket", group=None,
                  bootstrap: bool = True, engine: str = "auto"):
         if engine not in ("auto", "sm", "ce"):
             raise ValueError("engine must be 'auto', 'sm' or 'ce'")
@@ -200,6 +200,7 @@ class Aggregator:
         if self.param_arena:
             self._adopt_params()
         # Gradient storage:
+        #   "bucket" (default) zero-copy, see below
         #   "flat"   views into one flat buffer with the parameter arena's layout
         #            (bucket order, gradient_as_bucket_view style): the pack kernel
         #            gathers contiguous runs, host staging is one copy per group
@@ -375,11 +376,12 @@ class Aggregator:
 
     def step_host_flat(self, host_grads: torch.Tensor, host_params: torch.Tensor | None = None,
                        group_bytes: int = 16 << 20) -> int:
-        """step_host for flat pinned buffers in the arena layout (flat_layout()):
-        one H2D and one D2H cudaMemcpyAsync per group of buckets, overlapped
-        with the group's aggregation kernel."""
-        if self.grad_flat is None or not self.param_arena:
-            raise RuntimeError("step_host_flat needs grads='flat' and the parameter arena")
+        """step_host for flat pinned buffers in the parameter-arena layout
+        (flat_layout()): per group of buckets one H2D (grads="flat"; one per
+        bucket with grads="bucket") and one D2H cudaMemcpyAsync, overlapped with
+        the group's aggregation kernel."""
+        if self.grads not in ("flat", "bucket") or not self.param_arena:
+            raise RuntimeError("step_host_flat needs grads='flat' or 'bucket' and the parameter arena")
         cur = torch.cuda.current_stream(self.device)
         if not hasattr(self, "_h2d"):
             self._h2d = torch.cuda.Stream(device=self.device)
@@ -394,7 +396,12 @@ class Aggregator:
             last = self._live[j - 1].spec
             b = last.param_off // 4 + last.numel
             with torch.cuda.stream(h2d):
-                self.grad_flat[a:b].copy_(host_grads[a:b], non_blocking=True)
+                if self.grad_flat is not None:
+                    self.grad_flat[a:b].copy_(host_grads[a:b], non_blocking=True)
+                else:  # zero-copy: each bucket's gradients sit in its arena region
+                    for lv in self._live[i:j]:
+                        o = lv.spec.param_off // 4
+                        self._bucket_view(lv).copy_(host_grads[o:o + lv.spec.numel], non_blocking=True)
             cur.wait_stream(h2d)
             self._launch_range(i, j, cur.cuda_stream, N.MANY_FUSED, 0)
             launches += 1
@@ -404,6 +411,12 @@ class Aggregator:
                     host_params[a:b].copy_(pflat[a:b], non_blocking=True)
         cur.wait_stream(d2h)
         return launches
+
+    def _bucket_view(self, lv: _Live) -> torch.Tensor:
+        v = getattr(lv, "_view", None)
+        if v is None:
+            v = lv._view = self.ctx.arena_view(0, lv.spec.bucket_off, lv.spec.numel)
+        return v
 
     def step_host(self, host_grads: dict, host_params: dict | None = None, group_bytes: int = 16 << 20) -> int:
         """The plugin path with HOST buffers: pinned host gradients -> device,

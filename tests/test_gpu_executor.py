@@ -130,13 +130,14 @@ def test_step_host_pipelined_matches_sgd():
     agg.close()
 
 
-def test_step_host_flat_matches_sgd():
+@pytest.mark.parametrize("grads", ["bucket", "flat"])
+def test_step_host_flat_matches_sgd(grads):
     from paper_2004_14020_b200.executor import Aggregator
 
     lr = 0.1
     model = _tiny_model(4)
     plan, params = _plan_for(model)
-    agg = Aggregator(plan, params, lr=lr, epilogue="sgd")
+    agg = Aggregator(plan, params, lr=lr, epilogue="sgd", grads=grads)
     theta0 = {k: v.detach().cpu().clone().view(-1) for k, v in params.items()}
     hg = torch.zeros(plan.param_bytes // 4).pin_memory()
     hp = torch.zeros(plan.param_bytes // 4).pin_memory()
@@ -166,7 +167,7 @@ def test_tables_track_gradient_storage():
     agg.close()
 
 
-@pytest.mark.parametrize("grads", ["bucket", "own"])
+@pytest.mark.parametrize("grads", ["bucket", "flat", "own"])
 def test_gradient_storage_modes_match_sgd(grads):
     from paper_2004_14020_b200.executor import Aggregator
 
