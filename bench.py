@@ -454,36 +454,48 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
             p.data = p.data.clone()
             p.grad = p.grad.clone()
 
-    for engine in engines:
+    def run_engine(engine, cs, per_engine):
+        nonlocal gated
         agg = Aggregator(mplan, dict(ing.params), rank=rank, lr=LR, epilogue="sgd", grads=args.exposed_grads,
                          engine=engine)
-        if args.ce_min_mb is not None:
-            agg.ce_min_bytes = int(args.ce_min_mb * (1 << 20))
-        gated = agg.gate_forward(ing.modules)
+        try:
+            if args.ce_min_mb is not None:
+                agg.ce_min_bytes = int(args.ce_min_mb * (1 << 20))
+            gated = agg.gate_forward(ing.modules)
 
-        def caramel_step():
-            agg.zero_grad()
-            agg.begin_iteration()
-            fwd_bwd(model)
-            agg.finish_iteration(postpone=True)
+            def caramel_step():
+                agg.zero_grad()
+                agg.begin_iteration()
+                fwd_bwd(model)
+                agg.finish_iteration(postpone=True)
 
-        ks, ds = [], []
-        for _ in range(3):
-            c = timed(compute_only)
-            agg.attach_hooks()
-            k = timed(caramel_step)
+            ks, ds = [], []
+            for _ in range(3):
+                c = timed(compute_only)
+                agg.attach_hooks()
+                k = timed(caramel_step)
+                agg.detach_hooks()
+                cs.append(c)
+                ks.append(k)
+                ds.append(k - c)
+            # exposed = median over rounds of (round's Caramel - round's compute):
+            # paired rounds cancel slow clock / thermal drift between rounds
+            per_engine[engine] = (sorted(ks)[1], sorted(ds)[1])
+            agg.sync()
+            agg.status()
+        finally:
             agg.detach_hooks()
-            cs.append(c)
-            ks.append(k)
-            ds.append(k - c)
-        # exposed = median over rounds of (round's Caramel - round's compute):
-        # paired rounds cancel slow clock / thermal drift between rounds
-        per_engine[engine] = (sorted(ks)[1], sorted(ds)[1])
-        agg.sync()
-        agg.status()
-        detach_storage()
-        agg.close()
-        del agg
+            detach_storage()
+            agg.close()
+
+    errors = {}
+    for engine in engines:
+        try:
+            run_engine(engine, cs, per_engine)
+        except Exception as exc:  # recorded in the JSON line; the other engine still runs
+            errors[engine] = f"{type(exc).__name__}: {exc}"
+    if not per_engine:
+        raise RuntimeError(f"no engine completed: {errors}")
     c_ms = sorted(cs)[len(cs) // 2]
     best = min(per_engine, key=lambda e: per_engine[e][1])
     k_ms, k_exp = per_engine[best]
@@ -515,6 +527,7 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
     out = {"compute_ms": round(c_ms, 4), "caramel_ms": round(k_ms, 4),
            "caramel_exposed_ms": round(k_exp, 4), "engine": best,
            "engines": {e: {"ms": round(v[0], 4), "exposed_ms": round(v[1], 4)} for e, v in per_engine.items()},
+           "engine_errors": errors or None,
            "model": f"torchvision {args.model}, batch {B}/GPU, {size}x{size}, bf16 autocast, fp32 grads",
            "iters": K, "rounds": 3,
            "stat": "exposed = median over 3 rounds of (round time - paired compute-only round time)",
@@ -863,7 +876,10 @@ def run_caramel(args) -> int:
     # ---- config 5: bucket-size sweep vs NCCL (N > 1) --------------------------
     sweep = None
     if dist is not None and not args.no_sweep:
-        sweep = bucket_sweep(torch, dist, world, rank, dev)
+        try:
+            sweep = bucket_sweep(torch, dist, world, rank, dev)
+        except Exception as exc:  # recorded, never silently dropped
+            sweep = {"error": f"{type(exc).__name__}: {exc}"}
 
     # ---- exposed communication on the real model (T - C) --------------------
     exposed = None
@@ -875,7 +891,10 @@ def run_caramel(args) -> int:
         from paper_2004_14020_b200.costmodel import NetworkModel as _NM
 
         net = _NM(calibrated["latency_us"], calibrated["per_byte_us"]) if calibrated else None
-        exposed = measure_exposed(args, plan, ids, world, rank, dev, dist, network=net)
+        try:
+            exposed = measure_exposed(args, plan, ids, world, rank, dev, dist, network=net)
+        except Exception as exc:  # recorded, never silently dropped
+            exposed = {"error": f"{type(exc).__name__}: {exc}", "caramel_exposed_ms": None}
 
     # ---- CPU baseline (rank 0, N = 1 only) ----------------------------------
     cpu = None
