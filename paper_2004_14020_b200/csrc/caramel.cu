@@ -1560,10 +1560,18 @@ __device__ void grid_barrier(const Env& E, int me, int k, uint32_t S) {
 
 // items of my shard range [lo, hi): one edge item (scalar head + tail) and
 // vector items of 64 float4 over the 4-aligned interior
+// float4s per lane per item of the fused NVLink phase: about 8 loads in
+// flight per lane whatever p is (V * NP), at least 2
+template <int NP>
+struct FusedV { static constexpr int V = NP >= 4 ? 2 : 8 / NP; };
+
+// items of my shard range [lo, hi): one edge item (scalar head + tail) and
+// one per 32*V float4s of the 16-byte aligned interior
+template <int V>
 __device__ __forceinline__ uint32_t shard_items(uint64_t lo, uint64_t hi) {
   if (lo >= hi) return 0;
   const uint64_t a = (lo + 3) & ~3ull, e = hi & ~3ull;
-  return 1 + (e > a ? (uint32_t)(((e - a) / 4 + 63) / 64) : 0);
+  return 1 + (e > a ? (uint32_t)(((e - a) / 4 + 32 * V - 1) / (32 * V)) : 0);
 }
 
 struct FusedShared {
@@ -1630,7 +1638,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_shuffle_fused(const __grid_const
         for (int c = 0; c < B.depth; ++c) {
           uint64_t lo, hi;
           shard_bounds(B.numel, B.depth, E.world, c, me, lo, hi);
-          cnt += shard_items(lo, hi);
+          cnt += shard_items<FusedV<NP>::V>(lo, hi);
         }
       }
       uint32_t excl;
@@ -1662,7 +1670,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_shuffle_fused(const __grid_const
       uint64_t lo = 0, hi = 0;
       for (int c = 0; c < B.depth; ++c) {
         shard_bounds(B.numel, B.depth, E.world, c, me, lo, hi);
-        const uint32_t n = shard_items(lo, hi);
+        const uint32_t n = shard_items<FusedV<NP>::V>(lo, hi);
         if (li < n) break;
         li -= n;
       }
@@ -1693,38 +1701,33 @@ __global__ void __launch_bounds__(THREADS, 1) k_shuffle_fused(const __grid_const
         }
         continue;
       }
-      // vector item li-1: float4 [64 (li-1), 64 li) of the interior; lane does two
+      // vector item li-1: float4 [32V (li-1), 32V li) of the interior; lane
+      // does V of them (all V*NP loads issued before the first store)
+      constexpr int V = FusedV<NP>::V;
       const uint64_t nv = (e - a) / 4;
-      const uint64_t v0 = 64ull * (li - 1) + lane, v1 = v0 + 32;
-      const bool ok0 = v0 < nv, ok1 = v1 < nv;
-      const uint64_t x0 = a + 4 * v0, x1 = a + 4 * v1;
-      float4 p0[NP], p1[NP];
+      const uint64_t vb = 32ull * V * (li - 1) + lane;
+      float4 p[V][NP], t[V];
 #pragma unroll
-      for (int q = 0; q < NP; ++q) {
-        p0[q] = ok0 ? ld4(src[q] + x0) : make_float4(0.f, 0.f, 0.f, 0.f);
-        p1[q] = ok1 ? ld4(src[q] + x1) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      float4 t0 = make_float4(0.f, 0.f, 0.f, 0.f), t1 = t0;
-      if (sgd) {
-        if (arena) {
-          if (ok0) t0 = ld4(th + x0);
-          if (ok1) t1 = ld4(th + x1);
-        } else {
-          if (ok0) t0 = seg_ld4(tc, x0, 1);
-          if (ok1) t1 = seg_ld4(tc, x1, 1);
-        }
-      }
-      float4 s0 = p0[0], s1 = p1[0];
+      for (int v = 0; v < V; ++v) {
+        const uint64_t vi = vb + 32ull * v;
+        const bool ok = vi < nv;
+        const uint64_t x = a + 4 * vi;
 #pragma unroll
-      for (int q = 1; q < NP; ++q) {
-        s0 = add4(s0, p0[q]);
-        s1 = add4(s1, p1[q]);
+        for (int q = 0; q < NP; ++q) p[v][q] = ok ? ld4(src[q] + x) : make_float4(0.f, 0.f, 0.f, 0.f);
+        t[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (sgd && ok) t[v] = arena ? ld4(th + x) : seg_ld4(tc, x, 1);
       }
-      const float4 o0 = epi4(B.epilogue, s0, t0, B.scale, B.lr), o1 = epi4(B.epilogue, s1, t1, B.scale, B.lr);
 #pragma unroll
-      for (int q = 0; q < NP; ++q) {
-        if (ok0) st4(dst[q] + x0, o0);
-        if (ok1) st4(dst[q] + x1, o1);
+      for (int v = 0; v < V; ++v) {
+        const uint64_t vi = vb + 32ull * v;
+        if (vi >= nv) continue;
+        const uint64_t x = a + 4 * vi;
+        float4 sum = p[v][0];
+#pragma unroll
+        for (int q = 1; q < NP; ++q) sum = add4(sum, p[v][q]);
+        const float4 o = epi4(B.epilogue, sum, t[v], B.scale, B.lr);
+#pragma unroll
+        for (int q = 0; q < NP; ++q) st4(dst[q] + x, o);
       }
     }
   }
