@@ -217,6 +217,21 @@ int caramel_allreduce_ce(caramel_ctx* ctx, const caramel_bucket* host, int32_t c
                          uint32_t index0, uint32_t epoch, void* grad_stream, void* stream);
 /* 1 if caramel_allreduce_ce can run on this context, else 0. */
 int caramel_ce_available(caramel_ctx* ctx);
+/* Asynchronous caramel_allreduce_ce: validates, records "gradients ready" on
+ * grad_stream in the caller's stream order, and hands the call to the
+ * context's worker thread, which issues it (copies, stream memory ops, the
+ * reduce kernel) on `stream` -- the calling thread (autograd's) pays a few
+ * microseconds instead of the whole issue cost.  Calls are issued in
+ * submission order.  `done_event` (a cudaEvent_t, or NULL) is recorded on
+ * `stream` after the call.  Work submitted here is ordered on `stream` only
+ * after caramel_ce_flush returns: flush before enqueueing anything else on
+ * `stream` or waiting on it / on done_event.  Worker errors are reported by
+ * the next submit or flush. */
+int caramel_ce_submit(caramel_ctx* ctx, const caramel_bucket* host, int32_t count,
+                      uint32_t index0, uint32_t epoch, void* grad_stream, void* stream,
+                      void* done_event);
+/* Blocks until every submitted call has been issued to its streams. */
+int caramel_ce_flush(caramel_ctx* ctx);
 
 #ifdef __cplusplus
 }

@@ -101,6 +101,9 @@ SIGNATURES = {
     "caramel_allreduce_ce": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Bucket), ctypes.c_int32,
                                             ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p]),
     "caramel_ce_available": (ctypes.c_int, [ctypes.c_void_p]),
+    "caramel_ce_submit": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Bucket), ctypes.c_int32, ctypes.c_uint32,
+                                         ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "caramel_ce_flush": (ctypes.c_int, [ctypes.c_void_p]),
 }
 
 

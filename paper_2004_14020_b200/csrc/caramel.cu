@@ -27,6 +27,13 @@
 #include <string.h>
 #include <stdarg.h>
 
+#include <condition_variable>
+#include <deque>
+#include <new>
+#include <mutex>
+#include <thread>
+#include <vector>
+
 #include "../../include/caramel.h"
 
 #define THREADS 512
@@ -2046,6 +2053,15 @@ struct CeItem {
   float lr, scale;
 };
 
+#define CE_POOL 256  // gradient-ready events of submitted, not yet issued calls
+
+struct CeJob {
+  std::vector<caramel_bucket> buckets;
+  uint32_t index0, epoch;
+  cudaEvent_t grads, done;
+  cudaStream_t stream;
+};
+
 struct CeParams {
   const char* arena;  // my bucket arena (own gradients + staging slots)
   char* out;
@@ -2104,6 +2120,16 @@ struct caramel_ctx {
   bool ce_ready;
   cudaStream_t ce_send;  // reduce-scatter pushes + READY: never waits on a peer
   cudaEvent_t ce_grads;  // gradients produced (recorded on the caller's grad stream)
+  // asynchronous submission (caramel_ce_submit / caramel_ce_flush)
+  std::mutex ce_mu;
+  std::condition_variable ce_cv;
+  std::deque<CeJob> ce_jobs;
+  std::thread ce_worker;
+  bool ce_worker_started, ce_stop, ce_busy;
+  uint64_t ce_submitted, ce_consumed;
+  cudaEvent_t ce_pool[CE_POOL];
+  int ce_rc;
+  char ce_err[512];
 };
 
 struct Blob {
@@ -2217,7 +2243,7 @@ int caramel_init(int rank, int world, int nlocal, uint64_t arena_bytes, uint64_t
   if (nlocal != 1 && nlocal != world) return set_err(CARAMEL_EINVAL, "nlocal must be 1 or world");
   if (nlocal == world && rank != 0) return set_err(CARAMEL_EINVAL, "rank emulation requires rank 0");
   if (rank < 0 || rank >= world) return set_err(CARAMEL_EINVAL, "rank %d outside [0, %d)", rank, world);
-  caramel_ctx* c = (caramel_ctx*)calloc(1, sizeof(caramel_ctx));
+  caramel_ctx* c = new (std::nothrow) caramel_ctx();  // value-initialised: PODs zeroed
   if (!c) return set_err(CARAMEL_EINVAL, "out of host memory");
   c->rank = rank;
   c->world = world;
@@ -2328,6 +2354,16 @@ int caramel_set_timeout_ms(caramel_ctx* c, uint64_t ms) {
 
 int caramel_finalize(caramel_ctx* c) {
   if (!c) return 0;
+  if (c->ce_worker_started) {
+    {
+      std::lock_guard<std::mutex> lk(c->ce_mu);
+      c->ce_stop = true;
+    }
+    c->ce_cv.notify_all();
+    c->ce_worker.join();  // drains what was submitted
+    for (int i = 0; i < CE_POOL; ++i) cudaEventDestroy(c->ce_pool[i]);
+  }
+  cudaDeviceSynchronize();  // nothing in flight touches the arenas below
   for (int q = 0; q < MAXR; ++q) {
     if (c->opened[q]) {
       cudaIpcCloseMemHandle((void*)c->arena[q]);
@@ -2343,7 +2379,7 @@ int caramel_finalize(caramel_ctx* c) {
     cudaStreamDestroy(c->ce_send);
     cudaEventDestroy(c->ce_grads);
   }
-  free(c);
+  delete c;
   return 0;
 }
 
@@ -2690,14 +2726,13 @@ int caramel_ce_available(caramel_ctx* c) {
   return c && c->nlocal == 1 && c->world > 1 && ce_probe(c) ? 1 : 0;
 }
 
-int caramel_allreduce_ce(caramel_ctx* c, const caramel_bucket* host, int32_t count, uint32_t index0,
-                         uint32_t epoch, void* grad_stream, void* stream) {
+static int ce_validate(caramel_ctx* c, const caramel_bucket* host, int32_t count, uint32_t epoch) {
   if (!c || !host || count < 1) return set_err(CARAMEL_EINVAL, "allreduce_ce: null argument or empty list");
   if (c->nlocal != 1 || c->world < 2) return set_err(CARAMEL_ESTATE, "allreduce_ce: one rank per process, world >= 2");
   if (!c->imported) return set_err(CARAMEL_ESTATE, "peer arenas not mapped (call caramel_import)");
   if (epoch == 0) return set_err(CARAMEL_EINVAL, "allreduce_ce: epoch must be > 0");
   if (!ce_probe(c)) return set_err(CARAMEL_ESTATE, "allreduce_ce: device lacks 64-bit stream memory operations");
-  const int me = c->rank, p = c->world;
+  const int p = c->world;
   const int epi = host[0].epilogue;
   for (int i = 0; i < count; ++i) {
     const caramel_bucket& b = host[i];
@@ -2714,11 +2749,16 @@ int caramel_allreduce_ce(caramel_ctx* c, const caramel_bucket* host, int32_t cou
     if (b.numel && end > c->arena_bytes)
       return set_err(CARAMEL_EINVAL, "allreduce_ce: bucket + staging slots exceed the arena (size it with caramel_bucket_layout)");
   }
-  int rc = ce_setup(c);
-  if (rc) return rc;
+  return ce_setup(c);
+}
+
+// Enqueue one call's work (see the block comment above); `grads` is an event
+// recorded on the stream that produced the gradients.
+static int ce_enqueue(caramel_ctx* c, const caramel_bucket* host, int32_t count, uint32_t index0, uint32_t epoch,
+                      cudaEvent_t grads, cudaStream_t s) {
+  const int epi = host[0].epilogue;
   const bool sgd = epi == CARAMEL_EPI_SGD;
-  cudaStream_t s = (cudaStream_t)stream;
-  cudaStream_t gs = grad_stream ? (cudaStream_t)grad_stream : s;
+  const int me = c->rank, p = c->world;
   const uint64_t tag = ((uint64_t)epoch << 32) | (uint64_t)(index0 + (uint32_t)count);
   const uint64_t ready = c->arena_bytes + CE_FLAG_OFF, done = ready + 8 * MAXR;
   uint64_t peer_ready[MAXR], my_ready[MAXR], peer_done[MAXR], my_done[MAXR];
@@ -2734,8 +2774,8 @@ int caramel_allreduce_ce(caramel_ctx* c, const caramel_bucket* host, int32_t cou
   // 1. reduce-scatter: push my gradients of every peer's shard into that
   //    peer's staging slot for me, then READY -- on the send stream, which
   //    never waits on a peer (so READY can always go out)
-  CUDA_TRY(cudaEventRecord(c->ce_grads, gs));
-  CUDA_TRY(cudaStreamWaitEvent(c->ce_send, c->ce_grads, 0));
+  CUDA_TRY(cudaStreamWaitEvent(c->ce_send, grads, 0));
+  CUDA_TRY(cudaStreamWaitEvent(s, grads, 0));
   for (int r = 1; r < p; ++r) {
     const int q = (me + r) % p;
     const uint64_t k = (uint64_t)(me < q ? me : me - 1);  // my slot at q
@@ -2794,6 +2834,84 @@ int caramel_allreduce_ce(caramel_ctx* c, const caramel_bucket* host, int32_t cou
   }
   CU_TRY(ce_memops(s, false, peer_done, np_, tag));
   CU_TRY(ce_memops(s, true, my_done, np_, tag));
+  return 0;
+}
+
+int caramel_allreduce_ce(caramel_ctx* c, const caramel_bucket* host, int32_t count, uint32_t index0,
+                         uint32_t epoch, void* grad_stream, void* stream) {
+  int rc = ce_validate(c, host, count, epoch);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaEventRecord(c->ce_grads, grad_stream ? (cudaStream_t)grad_stream : s));
+  return ce_enqueue(c, host, count, index0, epoch, c->ce_grads, s);
+}
+
+// ---- asynchronous submission: a per-context worker thread issues the calls ----
+static void ce_worker_main(caramel_ctx* c) {
+  cudaSetDevice(c->device);
+  std::unique_lock<std::mutex> lk(c->ce_mu);
+  for (;;) {
+    c->ce_cv.wait(lk, [&] { return c->ce_stop || !c->ce_jobs.empty(); });
+    if (c->ce_jobs.empty()) return;  // stop requested and drained
+    CeJob job = std::move(c->ce_jobs.front());
+    c->ce_jobs.pop_front();
+    c->ce_busy = true;
+    lk.unlock();
+    int rc = c->ce_rc ? 0 : ce_enqueue(c, job.buckets.data(), (int32_t)job.buckets.size(), job.index0, job.epoch,
+                                       job.grads, job.stream);
+    if (!rc && job.done) {
+      cudaError_t e = cudaEventRecord(job.done, job.stream);
+      if (e != cudaSuccess) rc = set_err(CARAMEL_ECUDA, "cudaEventRecord(done): %s", cudaGetErrorString(e));
+    }
+    lk.lock();
+    if (rc && !c->ce_rc) {
+      c->ce_rc = rc;
+      snprintf(c->ce_err, sizeof(c->ce_err), "%s", caramel_last_error());
+    }
+    ++c->ce_consumed;
+    c->ce_busy = false;
+    c->ce_cv.notify_all();
+  }
+}
+
+int caramel_ce_submit(caramel_ctx* c, const caramel_bucket* host, int32_t count, uint32_t index0, uint32_t epoch,
+                      void* grad_stream, void* stream, void* done_event) {
+  int rc = ce_validate(c, host, count, epoch);
+  if (rc) return rc;
+  std::unique_lock<std::mutex> lk(c->ce_mu);
+  if (c->ce_rc) return set_err(c->ce_rc, "%s", c->ce_err);
+  if (!c->ce_worker_started) {
+    for (int i = 0; i < CE_POOL; ++i) CUDA_TRY(cudaEventCreateWithFlags(&c->ce_pool[i], cudaEventDisableTiming));
+    c->ce_worker = std::thread(ce_worker_main, c);
+    c->ce_worker_started = true;
+  }
+  // an event is reusable once the worker has issued the waits on it
+  c->ce_cv.wait(lk, [&] { return c->ce_submitted - c->ce_consumed < CE_POOL; });
+  cudaEvent_t ev = c->ce_pool[c->ce_submitted % CE_POOL];
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaEventRecord(ev, grad_stream ? (cudaStream_t)grad_stream : s));  // in the caller's stream order
+  CeJob job;
+  job.buckets.assign(host, host + count);
+  job.index0 = index0;
+  job.epoch = epoch;
+  job.grads = ev;
+  job.stream = s;
+  job.done = (cudaEvent_t)done_event;
+  c->ce_jobs.push_back(std::move(job));
+  ++c->ce_submitted;
+  c->ce_cv.notify_all();
+  return 0;
+}
+
+int caramel_ce_flush(caramel_ctx* c) {
+  if (!c) return set_err(CARAMEL_EINVAL, "null ctx");
+  std::unique_lock<std::mutex> lk(c->ce_mu);
+  c->ce_cv.wait(lk, [&] { return c->ce_jobs.empty() && !c->ce_busy; });
+  if (c->ce_rc) {
+    const int rc = c->ce_rc;
+    c->ce_rc = 0;
+    return set_err(rc, "%s", c->ce_err);
+  }
   return 0;
 }
 

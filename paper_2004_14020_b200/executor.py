@@ -140,6 +140,7 @@ class _Live:
     members: list[str]
     remaining: int = 0
     done: torch.cuda.Event | None = None
+    ce_done: torch.cuda.Event | None = None  # engine="ce": recorded by the library's worker
     gate_modules: list = field(default_factory=list)
 
 
@@ -236,6 +237,10 @@ class Aggregator:
         for lv in self._live:
             for pid in lv.members:
                 self._by_param[pid] = lv
+        if self.engine == "ce":
+            for lv in self._live:  # materialised now, recorded by the worker thread later
+                lv.ce_done = torch.cuda.Event()
+                lv.ce_done.record(self.comm_stream)
         self._next = 0
         self._hooks = []
         self.epoch = 0
@@ -295,7 +300,10 @@ class Aggregator:
 
     def refresh_tables(self) -> None:
         """Rebuild segment tables (after gradients were reallocated)."""
-        self._live = [self._make_live(lv.spec) for lv in self._live]
+        old = self._live
+        self._live = [self._make_live(lv.spec) for lv in old]
+        for a, b in zip(old, self._live):
+            b.ce_done = a.ce_done
         self._by_param = {pid: lv for lv in self._live for pid in lv.members}
         self._build_list()
 
@@ -500,7 +508,10 @@ class Aggregator:
     coalesce_ctas = 32  # grid of a coalesced launch: leave SMs to the backward pass
     #: engine="ce": buckets below this size still run on the SM kernels (their
     #: latency is lower and they hold SMs only for microseconds)
-    ce_min_bytes = 8 << 20
+    ce_min_bytes = 0
+    ce_tail_us = 150.0
+    ce_tail_frac = 0.02
+    _ce_tail = None
 
     def _comm_busy(self) -> bool:
         return self._last_done is not None and not self._last_done.query()
@@ -515,31 +526,7 @@ class Aggregator:
             return
         pending_bytes = 4 * (self._prefix[j] - self._prefix[self._next])
         if self.engine == "ce":
-            # one call per bucket: every rank must group the launch order into
-            # the same calls (a stream-memory-op wait stalls its hardware queue);
-            # the engine choice per bucket is by size, identical on every rank
-            cur = torch.cuda.current_stream(self.device)
-            self.comm_stream.wait_stream(cur)
-            k = self._next
-            while k < j:
-                if 4 * self._live[k].spec.numel >= self.ce_min_bytes:
-                    self._launch_ce(k, k + 1, self.comm_stream.cuda_stream, cur.cuda_stream)
-                    k += 1
-                    continue
-                e = k  # a run of small buckets: one SM list launch (per-bucket flags)
-                while e < j and 4 * self._live[e].spec.numel < self.ce_min_bytes:
-                    e += 1
-                if e - k == 1:
-                    self._launch(self._live[k], self.comm_stream.cuda_stream)
-                else:
-                    self._launch_range(k, e, self.comm_stream.cuda_stream, N.MANY_FLAGS, 0)
-                k = e
-            ev = torch.cuda.Event()  # the comm stream is FIFO: one event covers the run
-            ev.record(self.comm_stream)
-            for lv in self._live[self._next:j]:
-                lv.done = ev
-            self._last_done = ev
-            self._next = j
+            self._drain_ce(j)
             return
         if not force and self._comm_busy() and j - self._next < self.coalesce_buckets \
                 and pending_bytes < self.coalesce_bytes:
@@ -559,6 +546,53 @@ class Aggregator:
         self._last_done = ev
         self._next = j
 
+    def _ce_engine_of(self, k: int) -> str:
+        """Engine of bucket k under engine="ce" (a function of the plan only, so
+        identical on every rank): the copy engines, except buckets below
+        ce_min_bytes and the tail -- buckets the plan makes ready in the last
+        ce_tail_frac of the ready-time span (at least ce_tail_us), launched when
+        backward is (nearly) over and the SM kernels' lower latency wins."""
+        if self._ce_tail is None:
+            ready = [lv.spec.ready_time_us for lv in self._live]
+            lo, hi = min(ready), max(ready)
+            cut = hi - max(self.ce_tail_us, self.ce_tail_frac * (hi - lo))
+            self._ce_tail = {i for i, r in enumerate(ready) if r >= cut}
+        if k in self._ce_tail or 4 * self._live[k].spec.numel < self.ce_min_bytes:
+            return "sm"
+        return "ce"
+
+    def _drain_ce(self, j: int) -> None:
+        """engine="ce": one call per bucket (every rank groups the launch order
+        identically: a stream-memory-op wait stalls its hardware queue).  Copy
+        engine calls go to the library's worker thread (caramel_ce_submit), so
+        autograd's thread only records an event; SM-engine buckets are launched
+        here after a flush, which keeps the comm stream in launch order."""
+        cur = torch.cuda.current_stream(self.device)
+        s = self.comm_stream.cuda_stream
+        bsz = ctypes.sizeof(N.Bucket)
+        for k in range(self._next, j):
+            lv = self._live[k]
+            if self._ce_engine_of(k) == "ce":
+                host = ctypes.cast(ctypes.byref(self._host_list, k * bsz), ctypes.POINTER(N.Bucket))
+                done = lv.ce_done.cuda_event if lv.ce_done is not None else None
+                N.check(N.lib().caramel_ce_submit(self.ctx._ctx, host, 1, k, self._ce_epoch,
+                                                  ctypes.c_void_p(cur.cuda_stream), ctypes.c_void_p(s),
+                                                  ctypes.c_void_p(done)))
+                self.launches += 1
+                lv.done = lv.ce_done
+            else:
+                N.check(N.lib().caramel_ce_flush(self.ctx._ctx))
+                self.comm_stream.wait_stream(cur)
+                self._launch(lv, s)
+                ev = torch.cuda.Event()
+                ev.record(self.comm_stream)
+                lv.done = ev
+        self._next = j
+
+    def _ce_flush(self) -> None:
+        if self.engine == "ce":
+            N.check(N.lib().caramel_ce_flush(self.ctx._ctx))
+
     def finish_iteration(self, postpone: bool = False) -> None:
         """Launch whatever is still held back, then make the current stream
         wait for the buckets.  postpone=True executes the plan's postponed
@@ -566,6 +600,7 @@ class Aggregator:
         (FP_OVERLAP) are not waited for here but by the forward gate of the
         first module that reads one of their parameters (gate_forward)."""
         self._drain(force=True)
+        self._ce_flush()
         if self._next != len(self._live):
             missing = [lv.spec.group_id for lv in self._live[self._next:]]
             raise RuntimeError(f"buckets never became ready: {missing[:5]}")
@@ -625,6 +660,7 @@ class Aggregator:
 
     def sync(self) -> None:
         """Wait for everything, including postponed buckets (e.g. before evaluation)."""
+        self._ce_flush()
         cur = torch.cuda.current_stream(self.device)
         cur.wait_stream(self.comm_stream)
         for i in sorted(self._fp_pending):

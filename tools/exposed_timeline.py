@@ -159,6 +159,28 @@ def ce_timed(i, j, stream, grad_stream=None):
 
 
 agg._launch_ce = ce_timed
+drain_t = []
+orig_drain_ce = agg._drain_ce
+
+
+def drain_ce_timed(j):
+    t = time.perf_counter()
+    orig_drain_ce(j)
+    drain_t.append(time.perf_counter() - t)
+
+
+agg._drain_ce = drain_ce_timed
+hook_t = []
+orig_drain = agg._drain
+
+
+def drain_timed(force=False):
+    t = time.perf_counter()
+    orig_drain(force)
+    hook_t.append(time.perf_counter() - t)
+
+
+agg._drain = drain_timed
 agg.attach_hooks()
 
 
@@ -180,6 +202,8 @@ for _ in range(K):
 e = ev()
 torch.cuda.synchronize()
 host_k = sorted(host_bwd[-K:])[K // 2]
+drain_per_it = sum(drain_t[-K * 40:]) / K if drain_t else 0.0
+hooks_per_it = sum(hook_t) / (K + 5)
 launches.clear()
 m0, m1 = [], []
 caramel_iter(m0)
@@ -187,6 +211,7 @@ caramel_iter(m1)
 torch.cuda.synchronize()
 k_ms = s.elapsed_time(e) / K
 agg.detach_hooks()
+host_bwd.clear()
 for _ in range(3):
     compute_only()
 c = []
@@ -202,7 +227,8 @@ if rank == 0:
     print(f"{name} p={world} batch {B}: compute fwd {c[0].elapsed_time(c[1]):.3f} bwd {c[1].elapsed_time(c[2]):.3f}"
           f" ms; per-iteration compute {c_ms:.3f} caramel {k_ms:.3f} exposed {k_ms - c_ms:.3f} ms; gated {gated}")
     print(f"host time in backward(): with aggregation {1e3 * host_k:.3f} ms, compute only "
-          f"{1e3 * sorted(host_bwd[-K:])[K // 2]:.3f} ms")
+          f"{1e3 * sorted(host_bwd)[len(host_bwd) // 2]:.3f} ms; _drain per iteration {1e3 * hooks_per_it:.3f} ms "
+          f"(_drain_ce {1e3 * sum(drain_t) / (K + 7):.3f} ms)")
     print(f"network model {net.latency_us:.2f} us + {net.per_byte_us:.3e} us/B;"
           f" modelled exposed {art.transfer_schedule.added_iteration_time_us:.1f} us")
     for b in plan.buckets:
