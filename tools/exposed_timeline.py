@@ -51,10 +51,15 @@ def ev():
     return e
 
 
+host_fwd = []
+
+
 def fwd_bwd(marks):
     marks.append(ev())
+    t = time.perf_counter()
     with torch.autocast("cuda", dtype=torch.bfloat16):
         loss = torch.nn.functional.cross_entropy(model(x).float(), y)
+    host_fwd.append(time.perf_counter() - t)
     marks.append(ev())
     t = time.perf_counter()
     loss.backward()
@@ -202,6 +207,29 @@ for _ in range(K):
 e = ev()
 torch.cuda.synchronize()
 host_k = sorted(host_bwd[-K:])[K // 2]
+host_fk = sorted(host_fwd[-K:])[K // 2]
+
+
+def fwd_only():
+    with torch.no_grad(), torch.autocast("cuda", dtype=torch.bfloat16):
+        model(x)
+
+
+def time_fwd():
+    for _ in range(3):
+        fwd_only()
+    torch.cuda.synchronize()
+    a = ev()
+    for _ in range(K):
+        fwd_only()
+    b = ev()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / K
+
+
+caramel_iter([])
+torch.cuda.synchronize()
+fwd_after = time_fwd()
 drain_per_it = sum(drain_t[-K * 40:]) / K if drain_t else 0.0
 hooks_per_it = sum(hook_t) / (K + 5)
 launches.clear()
@@ -212,6 +240,7 @@ torch.cuda.synchronize()
 k_ms = s.elapsed_time(e) / K
 agg.detach_hooks()
 host_bwd.clear()
+host_fwd.clear()
 for _ in range(3):
     compute_only()
 c = []
@@ -223,7 +252,11 @@ for _ in range(K):
 e = ev()
 torch.cuda.synchronize()
 c_ms = s.elapsed_time(e) / K
+fwd_plain = time_fwd()
 if rank == 0:
+    print(f"no-grad forward: after aggregation iterations {fwd_after:.3f} ms, after compute-only {fwd_plain:.3f} ms; "
+          f"host time in forward: aggregation iterations {1e3 * host_fk:.3f} ms, compute only "
+          f"{1e3 * sorted(host_fwd)[len(host_fwd) // 2]:.3f} ms")
     print(f"{name} p={world} batch {B}: compute fwd {c[0].elapsed_time(c[1]):.3f} bwd {c[1].elapsed_time(c[2]):.3f}"
           f" ms; per-iteration compute {c_ms:.3f} caramel {k_ms:.3f} exposed {k_ms - c_ms:.3f} ms; gated {gated}")
     print(f"host time in backward(): with aggregation {1e3 * host_k:.3f} ms, compute only "
