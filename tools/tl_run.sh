@@ -1,8 +1,9 @@
 set -x
 export PYTHONUNBUFFERED=1
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29612 bench.py --gpus 2 > gpurun_out/b2.json 2> gpurun_out/b2.err
-for m in alexnet vgg16 inception_v3; do
-  B=64; [ $m = vgg16 ] && B=32
-  timeout 500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29612 bench.py --gpus 2 --model $m --batch $B --no-cpu-baseline --no-sweep > gpurun_out/m_${m}_n2.json 2> gpurun_out/m_${m}_n2.err
+timeout 900 python -m pytest tests/test_gpu_kernels.py -x -q > gpurun_out/tk.txt 2>&1
+CARAMEL_FUSED_CLAIM=2 timeout 900 python -m pytest tests/test_gpu_kernels.py -x -q > gpurun_out/tk2.txt 2>&1
+for c in 0 1 2 4; do
+CARAMEL_FUSED_CLAIM=$c CUDA_VISIBLE_DEVICES=0,1 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29612 tools/fused_breakdown.py > gpurun_out/fb2_c$c.txt 2>&1
+CARAMEL_FUSED_CLAIM=$c timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29612 tools/fused_breakdown.py > gpurun_out/fb4_c$c.txt 2>&1
 done
 echo done
