@@ -292,6 +292,48 @@ def time_kernel_gated(agg, torch, reps=20):
     return ts[len(ts) // 2]  # ms, median launch
 
 
+def pack_unpack_bw(torch, tensors, dev, peak_gbs, reps=20):
+    """K1 / K4 standalone (pack/unpack GB/s against HBM): every
+    gradient of the set as its own allocation (161 tensors for resnet50),
+    gathered into one bucket by caramel_pack and scattered back by
+    caramel_unpack.  Algorithmic bytes 2 x 4 x elements (read + write);
+    median of `reps` launches, CUDA events on the launching stream."""
+    import ctypes
+
+    from paper_2004_14020_b200 import _native as N
+    from paper_2004_14020_b200 import comm
+
+    grads = [torch.randn(max(1, t.numel), device=dev) for t in tensors]
+    n = sum(g.numel() for g in grads)
+    bucket = torch.empty(n, device=dev)
+    segs = comm.segments_for(grads)
+    table = comm.segment_table([segs], dev)
+    st = torch.cuda.current_stream().cuda_stream
+
+    def med(fn):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        fn()
+        torch.cuda._sleep(int(20e6))
+        for a, b in evs:
+            a.record()
+            fn()
+            b.record()
+        torch.cuda.synchronize()
+        ts = sorted(a.elapsed_time(b) for a, b in evs)
+        return ts[len(ts) // 2]
+
+    pk = med(lambda: comm.pack(table, len(segs), n, bucket.data_ptr(), st))
+    up = med(lambda: comm.unpack(table, len(segs), n, bucket.data_ptr(), False, st))
+    ok = all(torch.equal(g, bucket[o.offset:o.offset + o.numel]) for g, o in zip(grads, segs))
+    alg = 8 * n
+    return {"members": len(grads), "bytes": 4 * n, "alg_bytes_per_launch": alg,
+            "pack_ms": round(pk, 4), "pack_gbs": round(alg / (pk * 1e-3) / 1e9, 1),
+            "pack_frac": round(alg / (pk * 1e-3) / 1e9 / peak_gbs, 4),
+            "unpack_ms": round(up, 4), "unpack_gbs": round(alg / (up * 1e-3) / 1e9, 1),
+            "unpack_frac": round(alg / (up * 1e-3) / 1e9 / peak_gbs, 4), "peak_gbs": peak_gbs,
+            "round_trip_exact": bool(ok), "kernels": "k_pack / k_unpack (caramel.cu)"}
+
+
 def nccl_baseline(torch, dist, params, grads_dev, world, steps, warmup, bucket_bytes=25 << 20):
     """Plain bucketed NCCL all-reduce (DDP-style 25 MiB buckets in reverse
     parameter order) + SGD update with torch ops: the compared baseline."""
@@ -896,6 +938,15 @@ def run_caramel(args) -> int:
         except Exception as exc:  # recorded, never silently dropped
             exposed = {"error": f"{type(exc).__name__}: {exc}", "caramel_exposed_ms": None}
 
+    # ---- K1 / K4 standalone vs HBM --------------------------------
+    hbm_peak = 6650.0
+    if (ROOT / "MEASURED_PEAKS.json").exists():
+        hbm_peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs") or hbm_peak
+    try:
+        packbw = pack_unpack_bw(torch, tensors, dev, hbm_peak)
+    except Exception as exc:  # recorded, never silently dropped
+        packbw = {"error": f"{type(exc).__name__}: {exc}"}
+
     # ---- CPU baseline (rank 0, N = 1 only) ----------------------------------
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -937,6 +988,7 @@ def run_caramel(args) -> int:
         "bucket_sweep": sweep,
         vkey: variant,
         "calibrated_network_model": calibrated,
+        "pack_unpack": packbw,
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,

@@ -560,14 +560,14 @@ __device__ __forceinline__ void walk(uint64_t lo, uint64_t hi, FV fv, FS fs) {
 // ---------------------------------------------------------------------------
 // K1 / K4 standalone: pack and unpack
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(THREADS) k_pack(const caramel_segment* segs, int nseg,
+__global__ void __launch_bounds__(THREADS, 4) k_pack(const caramel_segment* segs, int nseg,
                                                   uint64_t numel, float* bucket) {
   uint64_t lo, hi;
   tile_of(0, numel, gridDim.x, blockIdx.x, lo, hi);
   pack_range(segs, nseg, bucket, lo, hi, g_tab);
 }
 
-__global__ void __launch_bounds__(THREADS) k_unpack(const caramel_segment* segs, int nseg,
+__global__ void __launch_bounds__(THREADS, 4) k_unpack(const caramel_segment* segs, int nseg,
                                                     uint64_t numel, const float* bucket,
                                                     int to_param) {
   uint64_t lo, hi;
@@ -2405,9 +2405,21 @@ int caramel_finalize(caramel_ctx* c) {
   return 0;
 }
 
-static int grid_for(uint64_t numel) {
+// One full wave: SMs x resident CTAs of `fn` (592 CTAs at 3 resident per SM
+// left a 148-CTA second wave: 47.5 -> measured below)
+static int grid_for(uint64_t numel, const void* fn) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms < 1) sms = 148;
+  }
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, THREADS, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
   uint64_t g = (numel + (uint64_t)THREADS * 16 - 1) / ((uint64_t)THREADS * 16);
-  if (g > 148 * 4) g = 148 * 4;
+  const uint64_t cap = (uint64_t)sms * per_sm;
+  if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (int)g;
 }
@@ -2416,7 +2428,7 @@ int caramel_pack(const caramel_segment* segs, int32_t nseg, uint64_t numel, floa
   if (!segs || nseg < 1 || !bucket) return set_err(CARAMEL_EINVAL, "pack: null table or bucket");
   if (((uintptr_t)bucket) & 15) return set_err(CARAMEL_EINVAL, "pack: bucket must be 16-byte aligned");
   if (numel == 0) return 0;
-  k_pack<<<grid_for(numel), THREADS, 0, (cudaStream_t)stream>>>(segs, nseg, numel, bucket);
+  k_pack<<<grid_for(numel, (const void*)k_pack), THREADS, 0, (cudaStream_t)stream>>>(segs, nseg, numel, bucket);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -2426,7 +2438,7 @@ int caramel_unpack(const caramel_segment* segs, int32_t nseg, uint64_t numel, co
   if (!segs || nseg < 1 || !bucket) return set_err(CARAMEL_EINVAL, "unpack: null table or bucket");
   if (((uintptr_t)bucket) & 15) return set_err(CARAMEL_EINVAL, "unpack: bucket must be 16-byte aligned");
   if (numel == 0) return 0;
-  k_unpack<<<grid_for(numel), THREADS, 0, (cudaStream_t)stream>>>(segs, nseg, numel, bucket, to_param ? 1 : 0);
+  k_unpack<<<grid_for(numel, (const void*)k_unpack), THREADS, 0, (cudaStream_t)stream>>>(segs, nseg, numel, bucket, to_param ? 1 : 0);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
