@@ -200,12 +200,22 @@ def caramel_iter(marks):
 for _ in range(5):
     caramel_iter([])
 torch.cuda.synchronize()
-K = 20
-s = ev()
-for _ in range(K):
-    caramel_iter([])
-e = ev()
-torch.cuda.synchronize()
+K = int(os.environ.get("ITERS", "20"))
+
+
+def clk(cs):
+    sm = sorted(float(l.split(",")[1]) for l in cs.lines if len(l.split(",")) >= 9)
+    pw = sorted(float(l.split(",")[3]) for l in cs.lines if len(l.split(",")) >= 9)
+    rs = sorted({l.split(",")[4].strip() for l in cs.lines if len(l.split(",")) >= 9})
+    return (sm[len(sm) // 2] if sm else None, pw[len(pw) // 2] if pw else None, rs)
+
+
+with bench.ClockSampler(local) as cs_k:
+    s = ev()
+    for _ in range(K):
+        caramel_iter([])
+    e = ev()
+    torch.cuda.synchronize()
 host_k = sorted(host_bwd[-K:])[K // 2]
 host_fk = sorted(host_fwd[-K:])[K // 2]
 
@@ -246,14 +256,16 @@ for _ in range(3):
 c = []
 fwd_bwd(c)
 torch.cuda.synchronize()
-s = ev()
-for _ in range(K):
-    compute_only()
-e = ev()
-torch.cuda.synchronize()
+with bench.ClockSampler(local) as cs_c:
+    s = ev()
+    for _ in range(K):
+        compute_only()
+    e = ev()
+    torch.cuda.synchronize()
 c_ms = s.elapsed_time(e) / K
 fwd_plain = time_fwd()
 if rank == 0:
+    print(f"clocks (sm MHz, power W, reasons): aggregation {clk(cs_k)}, compute only {clk(cs_c)}")
     print(f"no-grad forward: after aggregation iterations {fwd_after:.3f} ms, after compute-only {fwd_plain:.3f} ms; "
           f"host time in forward: aggregation iterations {1e3 * host_fk:.3f} ms, compute only "
           f"{1e3 * sorted(host_fwd)[len(host_fwd) // 2]:.3f} ms")
