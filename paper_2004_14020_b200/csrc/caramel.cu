@@ -86,6 +86,12 @@ __device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
 
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
+__device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ void st_u64_relaxed_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -1542,8 +1548,11 @@ __device__ void grid_barrier(const Env& E, int me, int k, uint32_t S) {
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t* mine = sync_words(E, me);
-    fence_acq_rel_sys();
-    const uint32_t old = atomicAdd(mine + 16 + k, 1u);
+    // arrive with a gpu-scope release (covers this CTA's writes through the
+    // bar.sync above); the last arriver acquires every arrival, and its
+    // sys-scope fence before the remote flag stores makes all of them visible
+    // to the peers (causality is transitive across the two scopes)
+    const uint32_t old = atom_add_acq_rel_gpu(mine + 16 + k, 1u);
     if (old == gridDim.x - 1) {
       atomicExch(mine + 16 + k, 0u);
       if (k == 0) atomicAdd(mine, 1u);  // launch sequence: everybody has read it

@@ -1,6 +1,6 @@
 set -x
 export PYTHONUNBUFFERED=1
-T="timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29611"
-ITERS=60 MODEL=vgg16 BATCH=32 ENGINE=ce $T tools/exposed_timeline.py > gpurun_out/tl4_vgg_ce.txt 2>&1
-ITERS=60 MODEL=vgg16 BATCH=32 ENGINE=sm $T tools/exposed_timeline.py > gpurun_out/tl4_vgg_sm.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/tests4.txt 2>&1
+CUDA_VISIBLE_DEVICES=0,1 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29612 tools/fused_breakdown.py > gpurun_out/fb2.txt 2>&1
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29612 tools/fused_breakdown.py > gpurun_out/fb4.txt 2>&1
 echo done
