@@ -80,6 +80,9 @@ gated = agg.gate_forward(ing.modules)
 cap = int(os.environ.get("HOOK_CTAS", "0"))
 if "CE_MIN" in os.environ:
     agg.ce_min_bytes = int(os.environ["CE_MIN"])
+if "TAIL_US" in os.environ:
+    agg.ce_tail_us = float(os.environ["TAIL_US"])
+    agg.ce_tail_frac = float(os.environ.get("TAIL_FRAC", "0"))
 if cap:
     agg.coalesce_ctas = cap
 launches = []
