@@ -217,19 +217,26 @@ int caramel_allreduce_ce(caramel_ctx* ctx, const caramel_bucket* host, int32_t c
                          uint32_t index0, uint32_t epoch, void* grad_stream, void* stream);
 /* 1 if caramel_allreduce_ce can run on this context, else 0. */
 int caramel_ce_available(caramel_ctx* ctx);
-/* Asynchronous caramel_allreduce_ce: validates, records "gradients ready" on
- * grad_stream in the caller's stream order, and hands the call to the
- * context's worker thread, which issues it (copies, stream memory ops, the
- * reduce kernel) on `stream` -- the calling thread (autograd's) pays a few
- * microseconds instead of the whole issue cost.  Calls are issued in
- * submission order.  `done_event` (a cudaEvent_t, or NULL) is recorded on
- * `stream` after the call.  Work submitted here is ordered on `stream` only
- * after caramel_ce_flush returns: flush before enqueueing anything else on
- * `stream` or waiting on it / on done_event.  Worker errors are reported by
- * the next submit or flush. */
+/* Engines of caramel_ce_submit. */
+#define CARAMEL_ENGINE_CE 0  /* caramel_allreduce_ce                                  */
+#define CARAMEL_ENGINE_SM 1  /* caramel_allreduce[_update] per bucket, epoch 0 (device counter) */
+
+/* Asynchronous launch: validates, records "gradients ready" on grad_stream in
+ * the caller's stream order, and hands the call to the context's worker
+ * thread, which issues it on `stream` -- the calling thread (autograd's) pays
+ * a few microseconds instead of the whole issue cost.  CARAMEL_ENGINE_CE
+ * issues caramel_allreduce_ce(host, count, index0, epoch); CARAMEL_ENGINE_SM
+ * launches the SM kernel of each bucket with the device epoch counter
+ * (caramel_epoch_advance on `stream` once per iteration).  Calls are issued in
+ * submission order, so both engines can share `stream` in launch order.
+ * `done_event` (a cudaEvent_t, or NULL) is recorded on `stream` after the
+ * call.  Work submitted here is ordered on `stream` only after
+ * caramel_ce_flush returns: flush before enqueueing anything else on `stream`
+ * or waiting on it / on done_event.  Worker errors are reported by the next
+ * submit or flush. */
 int caramel_ce_submit(caramel_ctx* ctx, const caramel_bucket* host, int32_t count,
-                      uint32_t index0, uint32_t epoch, void* grad_stream, void* stream,
-                      void* done_event);
+                      uint32_t index0, uint32_t epoch, int32_t engine, void* grad_stream,
+                      void* stream, void* done_event);
 /* Blocks until every submitted call has been issued to its streams. */
 int caramel_ce_flush(caramel_ctx* ctx);
 

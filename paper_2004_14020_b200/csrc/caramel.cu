@@ -2088,6 +2088,7 @@ struct CeItem {
 
 struct CeJob {
   std::vector<caramel_bucket> buckets;
+  int engine;  // CARAMEL_ENGINE_CE / CARAMEL_ENGINE_SM
   uint32_t index0, epoch;
   cudaEvent_t grads, done;
   cudaStream_t stream;
@@ -2907,8 +2908,17 @@ static void ce_worker_main(caramel_ctx* c) {
     c->ce_jobs.pop_front();
     c->ce_busy = true;
     lk.unlock();
-    int rc = c->ce_rc ? 0 : ce_enqueue(c, job.buckets.data(), (int32_t)job.buckets.size(), job.index0, job.epoch,
-                                       job.grads, job.stream);
+    int rc = 0;
+    if (!c->ce_rc) {
+      if (job.engine == CARAMEL_ENGINE_CE) {
+        rc = ce_enqueue(c, job.buckets.data(), (int32_t)job.buckets.size(), job.index0, job.epoch, job.grads,
+                        job.stream);
+      } else {  // the SM kernels, one launch per bucket, device epoch counter
+        cudaError_t e = cudaStreamWaitEvent(job.stream, job.grads, 0);
+        if (e != cudaSuccess) rc = set_err(CARAMEL_ECUDA, "cudaStreamWaitEvent: %s", cudaGetErrorString(e));
+        for (size_t i = 0; !rc && i < job.buckets.size(); ++i) rc = launch(c, &job.buckets[i], 0, job.stream);
+      }
+    }
     if (!rc && job.done) {
       cudaError_t e = cudaEventRecord(job.done, job.stream);
       if (e != cudaSuccess) rc = set_err(CARAMEL_ECUDA, "cudaEventRecord(done): %s", cudaGetErrorString(e));
@@ -2925,8 +2935,17 @@ static void ce_worker_main(caramel_ctx* c) {
 }
 
 int caramel_ce_submit(caramel_ctx* c, const caramel_bucket* host, int32_t count, uint32_t index0, uint32_t epoch,
-                      void* grad_stream, void* stream, void* done_event) {
-  int rc = ce_validate(c, host, count, epoch);
+                      int32_t engine, void* grad_stream, void* stream, void* done_event) {
+  if (engine != CARAMEL_ENGINE_CE && engine != CARAMEL_ENGINE_SM)
+    return set_err(CARAMEL_EINVAL, "ce_submit: unknown engine %d", engine);
+  int rc = 0;
+  if (engine == CARAMEL_ENGINE_CE) {
+    rc = ce_validate(c, host, count, epoch);
+  } else {
+    if (!c || !host || count < 1) return set_err(CARAMEL_EINVAL, "ce_submit: null argument or empty list");
+    if (!c->imported) return set_err(CARAMEL_ESTATE, "peer arenas not mapped (call caramel_import)");
+    for (int i = 0; i < count && !rc; ++i) rc = validate_bucket(c, &host[i]);
+  }
   if (rc) return rc;
   std::unique_lock<std::mutex> lk(c->ce_mu);
   if (c->ce_rc) return set_err(c->ce_rc, "%s", c->ce_err);
@@ -2942,6 +2961,7 @@ int caramel_ce_submit(caramel_ctx* c, const caramel_bucket* host, int32_t count,
   CUDA_TRY(cudaEventRecord(ev, grad_stream ? (cudaStream_t)grad_stream : s));  // in the caller's stream order
   CeJob job;
   job.buckets.assign(host, host + count);
+  job.engine = engine;
   job.index0 = index0;
   job.epoch = epoch;
   job.grads = ev;

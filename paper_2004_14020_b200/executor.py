@@ -563,30 +563,21 @@ class Aggregator:
 
     def _drain_ce(self, j: int) -> None:
         """engine="ce": one call per bucket (every rank groups the launch order
-        identically: a stream-memory-op wait stalls its hardware queue).  Copy
-        engine calls go to the library's worker thread (caramel_ce_submit), so
-        autograd's thread only records an event; SM-engine buckets are launched
-        here after a flush, which keeps the comm stream in launch order."""
-        cur = torch.cuda.current_stream(self.device)
+        identically: a stream-memory-op wait stalls its hardware queue).  Both
+        engines' calls go to the library's worker thread (caramel_ce_submit),
+        which issues them on the comm stream in launch order, so autograd's
+        thread only records an event per bucket and never waits."""
+        cur = torch.cuda.current_stream(self.device).cuda_stream
         s = self.comm_stream.cuda_stream
         bsz = ctypes.sizeof(N.Bucket)
         for k in range(self._next, j):
             lv = self._live[k]
-            if self._ce_engine_of(k) == "ce":
-                host = ctypes.cast(ctypes.byref(self._host_list, k * bsz), ctypes.POINTER(N.Bucket))
-                done = lv.ce_done.cuda_event if lv.ce_done is not None else None
-                N.check(N.lib().caramel_ce_submit(self.ctx._ctx, host, 1, k, self._ce_epoch,
-                                                  ctypes.c_void_p(cur.cuda_stream), ctypes.c_void_p(s),
-                                                  ctypes.c_void_p(done)))
-                self.launches += 1
-                lv.done = lv.ce_done
-            else:
-                N.check(N.lib().caramel_ce_flush(self.ctx._ctx))
-                self.comm_stream.wait_stream(cur)
-                self._launch(lv, s)
-                ev = torch.cuda.Event()
-                ev.record(self.comm_stream)
-                lv.done = ev
+            eng = N.ENGINE_CE if self._ce_engine_of(k) == "ce" else N.ENGINE_SM
+            host = ctypes.cast(ctypes.byref(self._host_list, k * bsz), ctypes.POINTER(N.Bucket))
+            N.check(N.lib().caramel_ce_submit(self.ctx._ctx, host, 1, k, self._ce_epoch, eng, ctypes.c_void_p(cur),
+                                              ctypes.c_void_p(s), ctypes.c_void_p(lv.ce_done.cuda_event)))
+            self.launches += 1
+            lv.done = lv.ce_done
         self._next = j
 
     def _ce_flush(self) -> None:
