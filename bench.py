@@ -38,7 +38,7 @@ NVLINK_MODEL = (10.0, 1.0 / 460e3)      # latency us, us/B (SURVEY §8a "NVLink-
 REDUCE_MODEL = (400.0, 10.0)            # CLI defaults (cli.py:102-105); only shapes the modelled times
 NVLINK_PEAK_GBS = 770.0                 # B200_PROFILING.md measured peer copy per direction (fallback)
 NVLINK_NOMINAL_GBS = 900.0
-E2E_GROUP = 16 << 20                    # host-path pipelining granularity (H2D / kernel / D2H per group)
+E2E_GROUP = int(float(os.environ.get("CARAMEL_E2E_GROUP_MB", "16")) * (1 << 20))  # host-path pipelining granularity
 LR = 0.1
 MODEL_INDEX = {"vgg16": 0, "resnet50": 1, "inception_v3": 2, "alexnet": 3}
 

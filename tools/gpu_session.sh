@@ -3,9 +3,7 @@
 #   /usr/local/graft/bin/gpurun --gpus N -- "bash tools/gpu_session.sh"
 set -x
 export PYTHONUNBUFFERED=1
-timeout 600 python -m pytest tests/test_multigpu.py -x -q > gpurun_out/mg4.txt 2>&1
-for m in alexnet vgg16; do
-  B=64; [ $m = vgg16 ] && B=32
-  timeout 500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29612 bench.py --gpus 4 --model $m --batch $B --no-cpu-baseline --no-sweep > gpurun_out/m_${m}_n4.json 2> gpurun_out/m_${m}_n4.err
+for g in 6 8 12 16 24 32; do
+CARAMEL_E2E_GROUP_MB=$g timeout 300 python bench.py --no-exposed --no-cpu-baseline --steps 10 > gpurun_out/e2e_$g.json 2>/dev/null
 done
 echo done
