@@ -1867,7 +1867,7 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // world == 1, every bucket CARAMEL_F_FLAT + PACK + PARAM_ARENA + SGD:
 // theta[b] <- theta[b] - lr * (grad[b] * scale), tile by tile.
 template <int TT, int TS>
-__global__ void __launch_bounds__(TMA_THREADS, 1) k_local_flat_tma(const __grid_constant__ MParams P) {
+__global__ void __launch_bounds__(TMA_THREADS, 2) k_local_flat_tma(const __grid_constant__ MParams P) {
   extern __shared__ __align__(128) unsigned char dyn_smem[];
   TmaSmem<TT, TS>& S = *reinterpret_cast<TmaSmem<TT, TS>*>(dyn_smem);
   const Env E = P.env;
@@ -2655,21 +2655,24 @@ int caramel_allreduce_many(caramel_ctx* c, const caramel_bucket* host, int32_t c
     // tile geometry (floats x stages), measured on resnet50 (82 -> 88% of HBM):
     // 4096x6 5.35 TB/s, 5120x5 5.55, 6144x4 5.54, 8192x3 5.76 -- per-tile
     // overhead (mbarrier wait, CTA barrier, the issuing thread's bookkeeping)
-    // outweighs the deeper prefetch; CARAMEL_TMA=4096x6 selects the old one
+    // outweighs the deeper prefetch; two CTAs of 16 KB x 3 per SM (4096x3x2)
+    // tie with 8192x3 at 5.75 TB/s.  CARAMEL_TMA=4096x6 / 4096x3x2 select those
     static int variant = -1;
     if (variant < 0) {
       const char* e = getenv("CARAMEL_TMA");
-      variant = (e && !strcmp(e, "4096x6")) ? 1 : 0;
+      variant = (e && !strcmp(e, "4096x6")) ? 1 : (e && !strcmp(e, "4096x3x2")) ? 2 : 0;
     }
     void (*fn)(MParams) = k_local_flat_tma<8192, 3>;
     size_t smem = sizeof(TmaSmem<8192, 3>);
+    int per_sm = 1;
     if (variant == 1) { fn = k_local_flat_tma<4096, 6>; smem = sizeof(TmaSmem<4096, 6>); }
-    static bool attr[2] = {false, false};
+    if (variant == 2) { fn = k_local_flat_tma<4096, 3>; smem = sizeof(TmaSmem<4096, 3>); per_sm = 2; }
+    static bool attr[3] = {false, false, false};
     if (!attr[variant]) {
       CUDA_TRY(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr[variant] = true;
     }
-    fn<<<dim3(c->sms, 1), TMA_THREADS, smem, (cudaStream_t)stream>>>(P);
+    fn<<<dim3(c->sms * per_sm, 1), TMA_THREADS, smem, (cudaStream_t)stream>>>(P);
     CUDA_TRY(cudaGetLastError());
     return 0;
   }
