@@ -66,8 +66,11 @@ static int set_err(int code, const char* fmt, ...) {
 // device helpers
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint64_t split_at(uint64_t n, uint64_t parts, uint64_t i) {
-  // floor(i * n / parts): the integer chunk/shard rule
-  return (n * i) / parts;
+  // floor(i * n / parts): the integer chunk/shard rule;
+  // 32-bit division when the product fits (the common case, and a fraction of
+  // the cost of the 64-bit division routine the fused kernel ran per item)
+  const uint64_t x = n * i;
+  return x <= 0xffffffffull ? (uint64_t)((uint32_t)x / (uint32_t)parts) : x / parts;
 }
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
@@ -658,11 +661,16 @@ __host__ __device__ __forceinline__ uint64_t ll_region_bytes(uint64_t numel, int
   return ll_out_off(numel) + 8 * numel * (1 + (uint64_t)world);
 }
 
+// x / d for the chunk/shard rule: 32-bit division when x fits (exact either way)
+__host__ __device__ __forceinline__ uint64_t div_u64(uint64_t x, uint32_t d) {
+  return x <= 0xffffffffull ? (uint64_t)((uint32_t)x / d) : x / d;
+}
+
 __host__ __device__ __forceinline__ void shard_bounds(uint64_t n, int k, int p, int c, int s, uint64_t& lo,
                                                       uint64_t& hi) {
-  const uint64_t c0 = (n * (uint64_t)c) / k, m = (n * (uint64_t)(c + 1)) / k - c0;
-  lo = c0 + (m * (uint64_t)s) / p;
-  hi = c0 + (m * (uint64_t)(s + 1)) / p;
+  const uint64_t c0 = div_u64(n * (uint64_t)c, (uint32_t)k), m = div_u64(n * (uint64_t)(c + 1), (uint32_t)k) - c0;
+  lo = c0 + div_u64(m * (uint64_t)s, (uint32_t)p);
+  hi = c0 + div_u64(m * (uint64_t)(s + 1), (uint32_t)p);
 }
 
 

@@ -3,8 +3,7 @@
 #   /usr/local/graft/bin/gpurun --gpus N -- "bash tools/gpu_session.sh"
 set -x
 export PYTHONUNBUFFERED=1
-for v in 8192x3 4096x3x2 8192x3 4096x3x2; do
-CARAMEL_TMA=$v timeout 300 python bench.py --no-exposed --no-cpu-baseline --no-zero-copy --steps 50 > gpurun_out/tma_$v.json 2>/dev/null
-python -c "import json; d=json.loads(open('gpurun_out/tma_$v.json').read().strip().splitlines()[-1]); print('$v', d['ms_per_step'], d['roofline']['achieved'], d['roofline']['frac'])" >> gpurun_out/tma_sweep.txt
-done
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/tests4.txt 2>&1
+CUDA_VISIBLE_DEVICES=0,1 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29612 tools/fused_breakdown.py > gpurun_out/fb2.txt 2>&1
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29612 tools/fused_breakdown.py > gpurun_out/fb4.txt 2>&1
 echo done
