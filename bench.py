@@ -583,15 +583,18 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
     return out
 
 
-SWEEP_SIZES = (4096, 65536, 1 << 20, 4 << 20, 16 << 20, 64 << 20, 256 << 20)
+SWEEP_SIZES = tuple(4096 * 4 ** i for i in range(10))  # 4 KiB .. 1 GiB
+SWEEP_DEPTHS = (1, 2, 4, 8)
 
 
-def bucket_sweep(torch, dist, world, rank, dev, iters=20):
-    """Config 5: one bucket of S bytes, adaptive depth from the NVLink model,
-    two-shot over NVLink (caramel_allreduce, packed input, result in place)
-    vs torch.distributed.all_reduce (NCCL) on the same bytes.  `iters` calls
-    captured in a CUDA graph (both sides; host launch cost excluded), replayed
-    between two CUDA events, max over ranks; bus GB/s = 2(p-1)/p*S/t."""
+def bucket_sweep(torch, dist, world, rank, dev, iters=20, network=None):
+    """Config 5: one bucket of S bytes (4 KiB * 4^i up to 1 GiB), adaptive depth
+    from the calibrated network model (else the NVLink model), two-shot over
+    NVLink (caramel_allreduce, packed input, result in place) vs
+    torch.distributed.all_reduce (NCCL) on the same bytes, plus fixed depths
+    1/2/4/8 from 1 MiB up.  `iters` calls captured in a CUDA graph (both
+    sides; host launch cost excluded), replayed between two CUDA events, max
+    over ranks; bus GB/s = 2(p-1)/p*S/t."""
     import ctypes
 
     from paper_2004_14020_b200 import _native as N
@@ -599,7 +602,7 @@ def bucket_sweep(torch, dist, world, rank, dev, iters=20):
     from paper_2004_14020_b200.collective import adaptive_depth
     from paper_2004_14020_b200.costmodel import NetworkModel, batching_threshold
 
-    thr = batching_threshold(NetworkModel(*NVLINK_MODEL))
+    thr = batching_threshold(network or NetworkModel(*NVLINK_MODEL))
     big = max(SWEEP_SIZES)
     region = max(N.bucket_layout(big // 4, d, N.SHUFFLE, world)[1] for d in (1, 8))
     region = (region + (1 << 20)) // (1 << 20) * (1 << 20)
@@ -670,6 +673,20 @@ def bucket_sweep(torch, dist, world, rank, dev, iters=20):
         row = {"bytes": size, "depth": depth, "caramel_us": round(us_c, 2),
                "caramel_bus_gbs": round(bus / us_c, 1), "nccl_us": round(us_n, 2),
                "nccl_bus_gbs": round(bus / us_n, 1), "graphed": [gc, gn]}
+        if size >= (1 << 20):
+            fixed = {}
+            for d in SWEEP_DEPTHS:
+                cd, _, _ = N.bucket_layout(n, d, N.SHUFFLE, world)
+                bd = comm.make_bucket(n, 0, region + k * (1 << 20), depth=d, pattern=N.SHUFFLE,
+                                      epilogue=N.EPI_SUM, flags=0, ctas=cd)
+
+                def fixed_call(st=None, bd=bd):
+                    st = st or stream
+                    N.check(N.lib().caramel_epoch_advance(ctx._ctx, ctypes.c_void_p(st.cuda_stream)))
+                    ctx.allreduce(bd, 0, st.cuda_stream)
+
+                fixed[str(d)] = round(timed(fixed_call)[0], 2)
+            row["fixed_depth_us"] = fixed
         if size >= (1 << 20) and ce_ctx:
             # the copy-engine two-shot (eager: its host-side tags cannot replay)
             for key, c in ce_ctx.items():
@@ -919,7 +936,10 @@ def run_caramel(args) -> int:
     sweep = None
     if dist is not None and not args.no_sweep:
         try:
-            sweep = bucket_sweep(torch, dist, world, rank, dev)
+            from paper_2004_14020_b200.costmodel import NetworkModel as _NMs
+
+            sweep = bucket_sweep(torch, dist, world, rank, dev,
+                                 network=_NMs(calibrated["latency_us"], calibrated["per_byte_us"]) if calibrated else None)
         except Exception as exc:  # recorded, never silently dropped
             sweep = {"error": f"{type(exc).__name__}: {exc}"}
 
