@@ -640,7 +640,7 @@ __host__ __device__ __forceinline__ uint64_t out_region_elems(uint64_t numel) {
 // word, two one-way NVLink hops per bucket.  Region: [float bucket | LL out
 // (numel x 8 B) | LL in (p slots x numel x 8 B)].  Chosen from numel alone, so
 // every rank and every launch kind agrees.
-#define LL_MAX_ELEMS 16384
+#define LL_MAX_ELEMS 65536  // 256 KB: LL 21.6 vs flags 23.0 us at 256 KB (p=4); CARAMEL_LL_MAX overrides
 // LL cutoff in elements: compile-time default, CARAMEL_LL_MAX overrides it at
 // library load (host layout and device kernels read the same value; every
 // rank must use the same setting, like every other layout parameter)

@@ -111,6 +111,19 @@ def test_shuffle_sum_bitexact(p, depth):
     assert_bitexact(run_emulated(N.SHUFFLE, p, depth, SHAPES_RAGGED, N.EPI_SUM))
 
 
+# 16K-64K elements: the upper range of the LL (flag-in-word) protocol
+SHAPES_MID = [(128, 300), (3,), (7, 1111), (1,)]         # 46,181 elements
+SHAPES_LL_EDGE = [(65536,)]                                # exactly the LL cutoff
+
+
+@pytest.mark.parametrize("shapes", ["mid", "edge"])
+@pytest.mark.parametrize("p", [2, 4, 8])
+def test_shuffle_mid_size_buckets_bitexact(shapes, p):
+    N, _ = _native()
+    sh = SHAPES_MID if shapes == "mid" else SHAPES_LL_EDGE
+    assert_bitexact(run_emulated(N.SHUFFLE, p, 1, sh, N.EPI_SGD, epochs=3))
+
+
 @pytest.mark.parametrize("pattern", ["ring", "hd", "shuffle"])
 @pytest.mark.parametrize("p", [2, 4, 8])
 def test_patterns_sgd_fused_update_bitexact(pattern, p):
