@@ -3,7 +3,7 @@
 #   /usr/local/graft/bin/gpurun --gpus N -- "bash tools/gpu_session.sh"
 set -x
 export PYTHONUNBUFFERED=1
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/final_tests1.txt 2>&1
-timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final_smoke1.txt 2>&1
-timeout 600 python bench.py > gpurun_out/final_b1b.json 2> gpurun_out/final_b1b.err
+timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_executor.py -x -q > gpurun_out/tk.txt 2>&1
+timeout 300 python tools/prof_pack.py > gpurun_out/pack.txt 2>&1
+timeout 300 python tools/prof_pack.py >> gpurun_out/pack.txt 2>&1
 echo done
