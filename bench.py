@@ -40,6 +40,13 @@ NVLINK_PEAK_GBS = 770.0                 # B200_PROFILING.md measured peer copy p
 NVLINK_NOMINAL_GBS = 900.0
 E2E_GROUP = int(float(os.environ.get("CARAMEL_E2E_GROUP_MB", "16")) * (1 << 20))  # host-path pipelining granularity
 LR = 0.1
+ROUNDS = 5  # paired (compute-only, aggregation) rounds of the exposed-communication measurement
+
+
+def _median(xs):
+    v = sorted(xs)
+    n = len(v)
+    return v[n // 2] if n % 2 else 0.5 * (v[n // 2 - 1] + v[n // 2])
 MODEL_INDEX = {"vgg16": 0, "resnet50": 1, "inception_v3": 2, "alexnet": 3}
 
 
@@ -473,8 +480,13 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
     for p in model.parameters():
         p.grad = torch.zeros_like(p)
 
+    # every arm zeroes its gradients the same way: one _foreach_zero_ over the
+    # gradient list (a per-parameter zero_() loop would cost the compute-only
+    # arm ~160-290 extra launches and bias T - C low)
+    grads_c = [p.grad for p in model.parameters()]
+
     def compute_only():
-        model.zero_grad(set_to_none=False)
+        torch._foreach_zero_(grads_c)
         fwd_bwd(model)
 
     ing, art, mplan, net = ingested_plan(args, model, compute_only, world, dist, dev, network)
@@ -489,12 +501,6 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
     if args.exposed_engine != "both":
         engines = [args.exposed_engine]
     cs, per_engine, gated = [], {}, 0
-
-    def detach_storage():
-        # give the model its own storage back before an Aggregator's arenas go
-        for p in model.parameters():
-            p.data = p.data.clone()
-            p.grad = p.grad.clone()
 
     def run_engine(engine, cs, per_engine):
         nonlocal gated
@@ -512,7 +518,7 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
                 agg.finish_iteration(postpone=True)
 
             ks, ds = [], []
-            for _ in range(3):
+            for _ in range(ROUNDS):
                 c = timed(compute_only)
                 agg.attach_hooks()
                 k = timed(caramel_step)
@@ -522,13 +528,12 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
                 ds.append(k - c)
             # exposed = median over rounds of (round's Caramel - round's compute):
             # paired rounds cancel slow clock / thermal drift between rounds
-            per_engine[engine] = (sorted(ks)[1], sorted(ds)[1])
+            per_engine[engine] = (_median(ks), _median(ds), min(ds), max(ds))
             agg.sync()
             agg.status()
         finally:
-            agg.detach_hooks()
-            detach_storage()
-            agg.close()
+            agg.close()  # hands the model torch-owned storage back
+            grads_c[:] = [p.grad for p in model.parameters()]
 
     errors = {}
     for engine in engines:
@@ -538,9 +543,9 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
             errors[engine] = f"{type(exc).__name__}: {exc}"
     if not per_engine:
         raise RuntimeError(f"no engine completed: {errors}")
-    c_ms = sorted(cs)[len(cs) // 2]
+    c_ms = _median(cs)
     best = min(per_engine, key=lambda e: per_engine[e][1])
-    k_ms, k_exp = per_engine[best]
+    k_ms, k_exp = per_engine[best][:2]
     torch.cuda.empty_cache()
 
     nccl_ms = nccl_exp = None
@@ -551,35 +556,47 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
         ddp = DDP(m2, device_ids=[dev.index], bucket_cap_mb=25, gradient_as_bucket_view=True)
         opt = torch.optim.SGD(m2.parameters(), lr=LR)
 
+        for p in m2.parameters():
+            p.grad = torch.zeros_like(p)
+        fwd_bwd(ddp)  # the first backward settles DDP's gradient bucket views
+        grads_d = [p.grad for p in m2.parameters()]
+
         def ddp_step():
-            opt.zero_grad(set_to_none=False)
+            torch._foreach_zero_(grads_d)
             fwd_bwd(ddp)
             opt.step()
 
         ns, nd = [], []
-        for _ in range(3):
+        for _ in range(ROUNDS):
             c = timed(compute_only)
             n = timed(ddp_step)
             ns.append(n)
             nd.append(n - c)
-        nccl_ms, nccl_exp = sorted(ns)[1], sorted(nd)[1]
+        nccl_ms, nccl_exp = _median(ns), _median(nd)
+        nccl_spread = [round(min(nd), 4), round(max(nd), 4)]
         del ddp, m2, opt
         torch.cuda.empty_cache()
     del model
-    out = {"compute_ms": round(c_ms, 4), "caramel_ms": round(k_ms, 4),
+    out = {"compute_ms": round(c_ms, 4), "compute_spread_ms": [round(min(cs), 4), round(max(cs), 4)],
+           "caramel_ms": round(k_ms, 4),
            "caramel_exposed_ms": round(k_exp, 4), "engine": best,
-           "engines": {e: {"ms": round(v[0], 4), "exposed_ms": round(v[1], 4)} for e, v in per_engine.items()},
+           "engines": {e: {"ms": round(v[0], 4), "exposed_ms": round(v[1], 4),
+                           "exposed_spread_ms": [round(v[2], 4), round(v[3], 4)]} for e, v in per_engine.items()},
            "engine_errors": errors or None,
+           "negative_median_is_error": k_exp < 0,
            "model": f"torchvision {args.model}, batch {B}/GPU, {size}x{size}, bf16 autocast, fp32 grads",
-           "iters": K, "rounds": 3,
-           "stat": "exposed = median over 3 rounds of (round time - paired compute-only round time)",
+           "iters": K, "rounds": ROUNDS,
+           "zero_grad": "torch._foreach_zero_ over the gradient list in every arm (C, Caramel, DDP)",
+           "stat": f"exposed = median over {ROUNDS} rounds of (round time - paired compute-only round time); "
+                   "spread = [min, max] over the rounds; a negative median is a measurement error, not a result",
            "grads": args.exposed_grads,
            "plan": {"source": "ingested model DAG (measured, min of 5 runs, max over ranks)",
                     "network_model": [round(net.latency_us, 3), net.per_byte_us], "reduce_model": list(B200_REDUCE_MODEL),
                     "buckets": len(mplan.buckets), "placements": placements, "gated_modules": gated,
                     "modelled_exposed_us": round(art.transfer_schedule.added_iteration_time_us, 1)}}
     if nccl_ms is not None:
-        out.update({"nccl_ddp_ms": round(nccl_ms, 4), "nccl_ddp_exposed_ms": round(nccl_exp, 4)})
+        out.update({"nccl_ddp_ms": round(nccl_ms, 4), "nccl_ddp_exposed_ms": round(nccl_exp, 4),
+                    "nccl_ddp_exposed_spread_ms": nccl_spread})
     return out
 
 

@@ -131,9 +131,18 @@ int caramel_import(caramel_ctx* ctx, const void* blobs);
 /* Device addresses of local rank `lr`'s arenas (lr < nlocal). */
 int caramel_arena(caramel_ctx* ctx, int lr, uint64_t* bucket_arena,
                   uint64_t* param_arena);
-/* Watchdog state: 0, or CARAMEL_ETIMEOUT if a flag wait timed out since the
- * last call (synchronizes the device; clears the word). */
+/* Watchdog state: 0, or CARAMEL_ETIMEOUT if a cross-rank flag wait ever
+ * exceeded the watchdog (synchronizes the device).  A timeout POISONS the
+ * context: the waiting CTAs leave their kernel before any further store (no
+ * epilogue writes a result computed from inputs that never arrived), every
+ * later launch exits at entry, and the status stays set -- finalize the
+ * context and bootstrap a new one.  The reference's analogue is its plan
+ * consistency checks raising DeadlockDetected (sim.py:136-153). */
 int caramel_status(caramel_ctx* ctx);
+/* Same state without synchronizing: reads a host-mapped mirror of the status
+ * word that the device writes when the watchdog fires (cheap enough to call
+ * once per iteration). */
+int caramel_poll(caramel_ctx* ctx);
 int caramel_set_timeout_ms(caramel_ctx* ctx, uint64_t ms);
 int caramel_finalize(caramel_ctx* ctx);
 

@@ -134,6 +134,20 @@ def np_allreduce(pattern: int, bufs: list[np.ndarray], k: int, epi: int = EPI_SU
     return out
 
 
+def np_shuffle_lean(bufs: list[np.ndarray], epi: int = EPI_SUM, scale: float = 1.0, lr: float = 0.0,
+                    theta: np.ndarray | None = None) -> np.ndarray:
+    """np_allreduce(SHUFFLE, ...) without its per-worker copies, for buckets of
+    hundreds of MB at p = 8.  In the two-shot pattern every element is reduced
+    once, by its shard owner, in ascending rank order (collective.py:12-13,
+    98-100), so the values do not depend on the chunk/shard bounds and the
+    bucket can be summed whole: acc = g0; acc += g1; ... (each += is one fp32
+    rounding, the same as (acc + g).astype(float32))."""
+    acc = np.array(bufs[0], dtype=np.float32, copy=True)
+    for b in bufs[1:]:
+        np.add(acc, b, out=acc)
+    return np_epilogue(epi, acc, theta, scale, lr)
+
+
 # ---------------------------------------------------------------------------
 # C restatement (ctypes)
 # ---------------------------------------------------------------------------

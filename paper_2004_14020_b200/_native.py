@@ -85,6 +85,7 @@ SIGNATURES = {
     "caramel_arena": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64),
                                      ctypes.POINTER(ctypes.c_uint64)]),
     "caramel_status": (ctypes.c_int, [ctypes.c_void_p]),
+    "caramel_poll": (ctypes.c_int, [ctypes.c_void_p]),
     "caramel_set_timeout_ms": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64]),
     "caramel_finalize": (ctypes.c_int, [ctypes.c_void_p]),
     "caramel_pack": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64, ctypes.c_void_p,

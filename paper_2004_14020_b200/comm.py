@@ -127,7 +127,12 @@ class Context:
         return _view_fp32(base + byte_off, numel)
 
     def status(self) -> None:
+        """Raise CaramelError if a flag wait ever timed out (synchronizes)."""
         N.check(self._lib.caramel_status(self._ctx))
+
+    def poll(self) -> None:
+        """Same check without synchronizing (host-mapped status word)."""
+        N.check(self._lib.caramel_poll(self._ctx))
 
     def set_timeout_ms(self, ms: int) -> None:
         N.check(self._lib.caramel_set_timeout_ms(self._ctx, ms))

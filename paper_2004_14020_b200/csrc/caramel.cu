@@ -595,9 +595,34 @@ struct Env {
   uint32_t epoch;         // 0: read *epoch_dev (graph-replayable launches)
   const uint32_t* epoch_dev;
   uint64_t timeout_ns;
-  int* status;
+  int* status;            // device status word: 0, or CARAMEL_ETIMEOUT (sticky: the context is poisoned)
+  int* hstatus;           // host-mapped mirror of *status (caramel_poll reads it without a sync)
   uint64_t sync_off;      // library sync words, past the user part of every arena
 };
+
+// ---- watchdog / abort ---------------------------------------------------------
+// A flag wait that exceeds the watchdog poisons the context: the status word
+// is set (device + host-mapped mirror) and every CTA that was waiting, or that
+// starts afterwards, leaves the kernel before its next store -- no epilogue
+// ever writes a result computed from inputs that had not arrived.
+__device__ __forceinline__ bool poisoned(const Env& E) { return *reinterpret_cast<volatile int*>(E.status) != 0; }
+
+__device__ __noinline__ void raise_timeout(const Env& E) {
+  atomicExch(E.status, CARAMEL_ETIMEOUT);
+  if (E.hstatus) {
+    *reinterpret_cast<volatile int*>(E.hstatus) = CARAMEL_ETIMEOUT;
+    __threadfence_system();
+  }
+}
+
+// every thread of the CTA calls: leaves the kernel (all threads together) if
+// any thread's wait failed.  `exit` after a CTA-uniform barrier result.
+__device__ __forceinline__ void cta_abort_if(int failed) {
+  if (__syncthreads_or(failed)) asm volatile("exit;");
+}
+
+// CTA-uniform entry check of the kernels that wait on peers
+__device__ __forceinline__ void cta_enter(const Env& E) { cta_abort_if(threadIdx.x == 0 && poisoned(E)); }
 
 struct KParams {          // one bucket
   Env env;
@@ -701,25 +726,33 @@ struct Ctx {
     __syncthreads();
     if ((int)threadIdx.x < world) st_release_sys(flag(threadIdx.x, c, slot, me), epoch);
   }
-  __device__ __forceinline__ void spin(const uint32_t* f, uint32_t want) const {
-    if (ld_acquire_sys(f) >= want) return;
+  // false: the watchdog fired (or the context is already poisoned)
+  __device__ __forceinline__ bool spin(const uint32_t* f, uint32_t want) const {
+    if (ld_acquire_sys(f) >= want) return true;
     uint64_t t0 = globaltimer();
     uint32_t spins = 0;
     while (ld_acquire_sys(f) < want) {
-      if ((++spins & 1023u) == 0 && globaltimer() - t0 > E->timeout_ns) {
-        atomicExch(E->status, CARAMEL_ETIMEOUT);
-        break;
+      if ((++spins & 1023u) == 0) {
+        if (poisoned(*E)) return false;
+        if (globaltimer() - t0 > E->timeout_ns) {
+          raise_timeout(*E);
+          return false;
+        }
       }
     }
+    return true;
   }
-  // every thread calls; waits until each src's flag (in my block) reaches `want`
+  // every thread calls; waits until each src's flag (in my block) reaches
+  // `want`; the whole CTA leaves the kernel if a wait failed
   __device__ __forceinline__ void wait_from(int c, int slot, const int* srcs, int nsrc, uint32_t want) const {
-    if ((int)threadIdx.x < nsrc) spin(flag(me, c, slot, srcs[threadIdx.x]), want);
-    __syncthreads();
+    int bad = 0;
+    if ((int)threadIdx.x < nsrc) bad = !spin(flag(me, c, slot, srcs[threadIdx.x]), want);
+    cta_abort_if(bad);
   }
   __device__ __forceinline__ void wait_all(int c, int slot, uint32_t want) const {
-    if ((int)threadIdx.x < world) spin(flag(me, c, slot, threadIdx.x), want);
-    __syncthreads();
+    int bad = 0;
+    if ((int)threadIdx.x < world) bad = !spin(flag(me, c, slot, threadIdx.x), want);
+    cta_abort_if(bad);
   }
 };
 
@@ -1259,19 +1292,27 @@ __device__ __forceinline__ uint64_t ll_pack(uint32_t epoch, float v) {
   return ((uint64_t)epoch << 32) | (uint64_t)__float_as_uint(v);
 }
 
-// spin until the LL word carries `epoch`; returns its value
-__device__ __forceinline__ float ll_wait(const uint64_t* p, uint32_t epoch, const Env& E) {
+// spin until the LL word carries `epoch`; returns its value.  On a watchdog
+// timeout (or a poisoned context) sets `bad`: the caller stores nothing
+// derived from this value.
+__device__ __forceinline__ float ll_wait(const uint64_t* p, uint32_t epoch, const Env& E, int& bad) {
   uint64_t w = ld_u64_relaxed_sys(p);
-  if ((uint32_t)(w >> 32) != epoch) {
+  if ((uint32_t)(w >> 32) != epoch && !bad) {
     const uint64_t t0 = globaltimer();
     uint32_t spins = 0;
     do {
       w = ld_u64_relaxed_sys(p);
-      if ((++spins & 1023u) == 0 && globaltimer() - t0 > E.timeout_ns) {
-        atomicExch(E.status, CARAMEL_ETIMEOUT);
-        break;
+      if ((++spins & 1023u) == 0) {
+        if (poisoned(E)) { bad = 1; break; }
+        if (globaltimer() - t0 > E.timeout_ns) {
+          raise_timeout(E);
+          bad = 1;
+          break;
+        }
       }
     } while ((uint32_t)(w >> 32) != epoch);
+  } else if ((uint32_t)(w >> 32) != epoch) {
+    bad = 1;
   }
   return __uint_as_float((uint32_t)w);
 }
@@ -1314,6 +1355,7 @@ __device__ void phase_ll_reduce(const BucketRun& R) {
   const float* th = R.theta_flat();
   const bool sgd = R.B->epilogue == CARAMEL_EPI_SGD;
   const uint32_t ep = R.X.epoch;
+  int bad = 0;
   for (int c = 0; c < R.B->depth; ++c) {
     if (!R.mine(c)) continue;
     uint64_t lo, hi;
@@ -1334,9 +1376,10 @@ __device__ void phase_ll_reduce(const BucketRun& R) {
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
           float v = __uint_as_float((uint32_t)w[u][q]);
-          if ((uint32_t)(w[u][q] >> 32) != ep) v = ll_wait(ll_in(R, me, q) + x, ep, *R.E);
+          if ((uint32_t)(w[u][q] >> 32) != ep) v = ll_wait(ll_in(R, me, q) + x, ep, *R.E, bad);
           acc = q == 0 ? v : __fadd_rn(acc, v);
         }
+        if (bad) continue;  // an input never arrived: store nothing derived from it
         const float t = sgd ? (th ? ld1(th + x) : seg_ld1(tc, x, 1)) : 0.f;
         const uint64_t o = ll_pack(ep, epi1(R.B->epilogue, acc, t, R.B->scale, R.B->lr));
 #pragma unroll
@@ -1358,6 +1401,7 @@ __device__ void phase_ll_finish(const BucketRun& R) {
   const uint64_t* in = ll_out(R, me);
   const uint32_t ep = R.X.epoch;
   const uint64_t T = blockDim.x;
+  int bad = 0;
   for (int c = 0; c < R.B->depth; ++c)
     for (int s = 0; s < p && R.mine(c); ++s) {
       uint64_t lo, hi;
@@ -1371,7 +1415,8 @@ __device__ void phase_ll_finish(const BucketRun& R) {
           const uint64_t x = x0 + u * T;
           if (x >= hi) break;
           float v = __uint_as_float((uint32_t)w[u]);
-          if ((uint32_t)(w[u] >> 32) != ep) v = ll_wait(in + x, ep, *R.E);
+          if ((uint32_t)(w[u] >> 32) != ep) v = ll_wait(in + x, ep, *R.E, bad);
+          if (bad) continue;
           if (unpack) seg_st1(uc, x, which, v);
           else st1(res + x, v);
         }
@@ -1457,6 +1502,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_collective(const __grid_constant
   // local copies: the phases hold pointers to these, and generic pointers to
   // kernel parameters are not valid across real device-function calls
   const Env E = P.env;
+  cta_enter(E);
   const caramel_bucket B = P.b;
   run_bucket<PAT, NP>(E, B, lr_idx, launch_epoch(E), blockIdx.x);
 }
@@ -1554,6 +1600,7 @@ __device__ __forceinline__ uint32_t* sync_words(const Env& E, int rank) {
 // every rank; everybody waits for all ranks' flags.
 __device__ void grid_barrier(const Env& E, int me, int k, uint32_t S) {
   __syncthreads();
+  int bad = 0;
   if (threadIdx.x == 0) {
     uint32_t* mine = sync_words(E, me);
     // arrive with a gpu-scope release (covers this CTA's writes through the
@@ -1568,20 +1615,24 @@ __device__ void grid_barrier(const Env& E, int me, int k, uint32_t S) {
       fence_acq_rel_sys();
       for (int q = 0; q < E.world; ++q) st_relaxed_sys(sync_words(E, q) + 64 + k * MAXR + me, S + 1);
     }
-    for (int q = 0; q < E.world; ++q) {
+    for (int q = 0; q < E.world && !bad; ++q) {
       const uint32_t* f = mine + 64 + k * MAXR + q;
       if (ld_acquire_sys(f) >= S + 1) continue;
       const uint64_t t0 = globaltimer();
       uint32_t spins = 0;
       while (ld_acquire_sys(f) < S + 1) {
-        if ((++spins & 1023u) == 0 && globaltimer() - t0 > E.timeout_ns) {
-          atomicExch(E.status, CARAMEL_ETIMEOUT);
-          break;
+        if ((++spins & 1023u) == 0) {
+          if (poisoned(E)) { bad = 1; break; }
+          if (globaltimer() - t0 > E.timeout_ns) {
+            raise_timeout(E);
+            bad = 1;
+            break;
+          }
         }
       }
     }
   }
-  __syncthreads();
+  cta_abort_if(bad);
 }
 
 // items of my shard range [lo, hi): one edge item (scalar head + tail) and
@@ -1608,6 +1659,7 @@ template <int NP>
 __global__ void __launch_bounds__(THREADS, 1) k_shuffle_fused(const __grid_constant__ MParams P) {
   __shared__ FusedShared sh;
   const Env E = P.env;
+  cta_enter(E);
   const int lr_idx = blockIdx.y;
   const int me = E.rank_base + lr_idx;
   const uint32_t S = *reinterpret_cast<volatile uint32_t*>(sync_words(E, me));
@@ -1988,6 +2040,7 @@ template <int PAT, int NP>
 __global__ void __launch_bounds__(THREADS, 1) k_collective_many(const __grid_constant__ MParams P) {
   const int lr_idx = blockIdx.y;
   const Env E = P.env;  // local copy: phases keep pointers to it
+  cta_enter(E);
   const uint32_t epoch = launch_epoch(E);
   const int G = gridDim.x;
   // bucket i occupies CTAs base_i .. base_i + ctas_i - 1 (mod G), base_i being
@@ -2156,6 +2209,8 @@ struct caramel_ctx {
   bool imported;
   bool opened[MAXR];
   int* status;
+  int* hstatus;      // host-mapped mirror of *status (pinned host memory)
+  int* hstatus_dev;  // its device address
   uint32_t* epoch_dev;
   uint64_t timeout_ns;
   // copy-engine two-shot (caramel_allreduce_ce), created on first use
@@ -2313,6 +2368,9 @@ int caramel_init(int rank, int world, int nlocal, uint64_t arena_bytes, uint64_t
   if ((e = cudaMalloc(&c->status, 2 * sizeof(int))) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "cudaMalloc status: %s", cudaGetErrorString(e)); goto fail; }
   if ((e = cudaMemset(c->status, 0, 2 * sizeof(int))) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "memset: %s", cudaGetErrorString(e)); goto fail; }
   c->epoch_dev = reinterpret_cast<uint32_t*>(c->status + 1);
+  if ((e = cudaHostAlloc((void**)&c->hstatus, sizeof(int), cudaHostAllocMapped)) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "cudaHostAlloc status: %s", cudaGetErrorString(e)); goto fail; }
+  *(volatile int*)c->hstatus = 0;
+  if ((e = cudaHostGetDevicePointer((void**)&c->hstatus_dev, c->hstatus, 0)) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "cudaHostGetDevicePointer: %s", cudaGetErrorString(e)); goto fail; }
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "sync: %s", cudaGetErrorString(e)); goto fail; }
   c->imported = (nlocal == world);
   *out = c;
@@ -2375,17 +2433,25 @@ int caramel_arena(caramel_ctx* c, int lr, uint64_t* bucket_arena, uint64_t* para
   return 0;
 }
 
+static int poisoned_err(const caramel_ctx* c, int s) {
+  return set_err(s, "a cross-rank flag wait exceeded the %llu ms watchdog; the context is poisoned (every "
+                    "later launch exits before storing anything): finalize it and re-bootstrap",
+                 (unsigned long long)(c->timeout_ns / 1000000ull));
+}
+
 int caramel_status(caramel_ctx* c) {
   if (!c) return set_err(CARAMEL_EINVAL, "null ctx");
   CUDA_TRY(cudaDeviceSynchronize());
   int s = 0;
   CUDA_TRY(cudaMemcpy(&s, c->status, sizeof(int), cudaMemcpyDeviceToHost));
-  if (s) {
-    CUDA_TRY(cudaMemset(c->status, 0, sizeof(int)));
-    return set_err(s, "a cross-rank flag wait exceeded the %llu ms watchdog",
-                   (unsigned long long)(c->timeout_ns / 1000000ull));
-  }
-  return 0;
+  if (!s && c->hstatus) s = *(volatile int*)c->hstatus;
+  return s ? poisoned_err(c, s) : 0;  // sticky: the flags of a timed-out context are out of step
+}
+
+int caramel_poll(caramel_ctx* c) {
+  if (!c) return set_err(CARAMEL_EINVAL, "null ctx");
+  const int s = c->hstatus ? *(volatile int*)c->hstatus : 0;
+  return s ? poisoned_err(c, s) : 0;
 }
 
 int caramel_set_timeout_ms(caramel_ctx* c, uint64_t ms) {
@@ -2417,6 +2483,7 @@ int caramel_finalize(caramel_ctx* c) {
     if (c->param_local[i]) cudaFree(c->param_local[i]);
   }
   if (c->status) cudaFree(c->status);
+  if (c->hstatus) cudaFreeHost(c->hstatus);
   if (c->ce_ready) {
     cudaStreamDestroy(c->ce_send);
     cudaEventDestroy(c->ce_grads);
@@ -2555,20 +2622,41 @@ static void fill_env(const caramel_ctx* c, Env& E, uint32_t epoch) {
   E.epoch_dev = c->epoch_dev;
   E.timeout_ns = c->timeout_ns;
   E.status = c->status;
+  E.hstatus = c->hstatus_dev;
   E.sync_off = c->arena_bytes;
 }
 
+}  // extern "C"
+
 // rank emulation: all ranks' CTAs spin on each other, so they must be
 // co-resident -- a cooperative launch guarantees it or fails
-static int coop_launch(const caramel_ctx* c, const void* fn, dim3 grid, void** args, void* stream) {
+// Also used for k_shuffle_fused with one rank per process: its grid barriers
+// need every CTA resident, which only a cooperative launch guarantees (other
+// kernels -- backward, NCCL -- may hold SMs).  cudaLaunchKernelEx with the
+// cooperative attribute is capturable in a CUDA graph.
+template <class Params>
+static int coop_launch(const caramel_ctx* c, void (*fn)(Params), dim3 grid, const Params& P, void* stream) {
   int per_sm = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, THREADS, 0));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, THREADS, 0));
   if ((uint64_t)per_sm * c->sms < (uint64_t)grid.x * grid.y)
-    return set_err(CARAMEL_EINVAL, "emulated launch of %u x %u CTAs exceeds co-residency (%d per SM)", grid.x,
+    return set_err(CARAMEL_EINVAL, "cooperative launch of %u x %u CTAs exceeds co-residency (%d per SM)", grid.x,
                    grid.y, per_sm);
-  CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, dim3(THREADS), args, 0, (cudaStream_t)stream));
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, P));
   return 0;
 }
+
+extern "C" {
 
 static int launch(caramel_ctx* c, const caramel_bucket* b, uint32_t epoch, void* stream) {
   if (!c || !b) return set_err(CARAMEL_EINVAL, "null argument");
@@ -2585,10 +2673,7 @@ static int launch(caramel_ctx* c, const caramel_bucket* b, uint32_t epoch, void*
   else if (b->pattern == CARAMEL_RING) fn = pick_np<CARAMEL_RING>(c->world);
   else fn = pick_np<CARAMEL_HD>(c->world);
   dim3 grid(b->ctas, c->nlocal);
-  if (c->nlocal > 1) {
-    void* args[] = {(void*)&P};
-    return coop_launch(c, (const void*)fn, grid, args, stream);
-  }
+  if (c->nlocal > 1) return coop_launch(c, fn, grid, P, stream);
   fn<<<grid, THREADS, 0, (cudaStream_t)stream>>>(P);
   CUDA_TRY(cudaGetLastError());
   return 0;
@@ -2705,10 +2790,9 @@ int caramel_allreduce_many(caramel_ctx* c, const caramel_bucket* host, int32_t c
     gmax = tiled && ctas < need ? need : ctas;
   }
   dim3 grid(gmax, c->nlocal);
-  if (c->nlocal > 1) {
-    void* args[] = {(void*)&P};
-    return coop_launch(c, (const void*)fn, grid, args, stream);
-  }
+  // grid barriers (fused) or rank emulation: every CTA must be resident
+  const bool fused = pattern == CARAMEL_SHUFFLE && mode == CARAMEL_MANY_FUSED && c->world > 1;
+  if (c->nlocal > 1 || fused) return coop_launch(c, fn, grid, P, stream);
   fn<<<grid, THREADS, 0, (cudaStream_t)stream>>>(P);
   CUDA_TRY(cudaGetLastError());
   return 0;

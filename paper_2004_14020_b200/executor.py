@@ -43,6 +43,17 @@ from .transfer import PlacementKind
 
 PATTERN_CODE = {Pattern.RING: N.RING, Pattern.HALVING_DOUBLING: N.HD, Pattern.SHUFFLE: N.SHUFFLE}
 ALIGN = 256
+#: the copy-engine engine's stream-memory-op waits stall their hardware queue;
+#: with fewer queues than streams a wait can stall the backward pass too
+CE_MIN_CONNECTIONS = 16
+
+
+def ce_connections_ok() -> bool:
+    """True if CUDA_DEVICE_MAX_CONNECTIONS gives every stream its own queue."""
+    try:
+        return int(os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS", "8")) >= CE_MIN_CONNECTIONS
+    except ValueError:
+        return False
 
 
 def _align(x: int, a: int = ALIGN) -> int:
@@ -194,10 +205,16 @@ class Aggregator:
             self.ctx.bootstrap(group)
         if engine == "ce" and not N.lib().caramel_ce_available(self.ctx._ctx):
             raise RuntimeError("engine='ce': this device lacks 64-bit stream memory operations")
+        if engine == "ce" and not ce_connections_ok():
+            raise RuntimeError(f"engine='ce' needs CUDA_DEVICE_MAX_CONNECTIONS >= {CE_MIN_CONNECTIONS} in the "
+                               "environment before CUDA initialises: a stream-memory-op wait stalls its hardware "
+                               "queue, and with shared queues it can stall the backward pass behind a peer")
         if engine == "auto":
-            ok = grads == "bucket" and self.world > 1 and plan.pattern == N.SHUFFLE
+            ok = grads == "bucket" and self.world > 1 and plan.pattern == N.SHUFFLE and ce_connections_ok()
             engine = "ce" if ok and N.lib().caramel_ce_available(self.ctx._ctx) else "sm"
         self.engine = engine
+        self._group = group
+        self._engines_checked = not (self.world > 1 and bootstrap)
         if self.param_arena:
             self._adopt_params()
         # Gradient storage:
@@ -490,6 +507,8 @@ class Aggregator:
         """Arm every bucket for one backward pass (gradients must be zeroed in
         place -- Aggregator.zero_grad(), or zero_grad(set_to_none=False) -- so
         the segment tables stay valid)."""
+        if not self._engines_checked:
+            self._check_engines()
         for lv in self._live:
             lv.remaining = len(lv.members)
         self._next = 0
@@ -546,6 +565,31 @@ class Aggregator:
         self._last_done = ev
         self._next = j
 
+    def engine_assignment(self) -> list[str]:
+        """Engine of every bucket in launch order (overlapped mode)."""
+        if self.engine != "ce":
+            return ["sm"] * len(self._live)
+        return [self._ce_engine_of(k) for k in range(len(self._live))]
+
+    def _check_engines(self) -> None:
+        """All-gather the per-bucket engine assignment (and the knobs that
+        decide it) once, before the first overlapped iteration: a bucket run by
+        the copy-engine protocol on one rank and by the SM flag protocol on
+        another would hang, so a mismatch raises instead."""
+        import torch.distributed as dist
+
+        doc = json.dumps({"plan": self.plan.digest(), "engine": self.engine,
+                          "assignment": self.engine_assignment(),
+                          "knobs": [self.ce_min_bytes, self.ce_tail_us, self.ce_tail_frac,
+                                    self.coalesce_buckets, self.coalesce_bytes, self.coalesce_ctas]})
+        mine = hashlib.sha256(doc.encode()).hexdigest()
+        allv: list = [None] * self.world
+        dist.all_gather_object(allv, mine, group=self._group)
+        if len(set(allv)) != 1:
+            raise RuntimeError("ranks disagree on the engine of some bucket (engine, ce_min_bytes, ce_tail_* "
+                               "or coalescing knobs differ): the flag protocols would deadlock")
+        self._engines_checked = True
+
     def _ce_engine_of(self, k: int) -> str:
         """Engine of bucket k under engine="ce" (a function of the plan only, so
         identical on every rank): the copy engines, except buckets below
@@ -592,6 +636,7 @@ class Aggregator:
         first module that reads one of their parameters (gate_forward)."""
         self._drain(force=True)
         self._ce_flush()
+        self.ctx.poll()  # host-mapped watchdog word: raises if a wait ever timed out (no sync)
         if self._next != len(self._live):
             missing = [lv.spec.group_id for lv in self._live[self._next:]]
             raise RuntimeError(f"buckets never became ready: {missing[:5]}")
@@ -666,8 +711,26 @@ class Aggregator:
     def status(self) -> None:
         self.ctx.status()
 
+    def release_storage(self) -> None:
+        """Give every parameter and gradient torch-owned storage again (values
+        kept): the arenas they point into are freed by close()."""
+        torch.cuda.current_stream(self.device).wait_stream(self.comm_stream)
+        for p in self.params.values():
+            if self.param_arena:
+                p.data = p.data.clone()
+            if p.grad is not None and self.grads in ("bucket", "flat"):
+                p.grad = p.grad.clone()
+        self.grad_flat = None
+
     def close(self) -> None:
+        """Detach hooks, hand parameters/gradients back to torch-owned storage
+        and free the arenas.  The model stays usable (e.g. state_dict())."""
+        if self.ctx._ctx is None:
+            return
         self.detach_hooks()
+        self._ce_flush()
+        self.release_storage()
+        torch.cuda.synchronize(self.device)
         self.ctx.close()
 
 

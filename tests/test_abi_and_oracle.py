@@ -177,3 +177,17 @@ def test_lowering_is_rank_invariant_and_covers_the_plan():
         # regions never overlap
         spans = sorted((b.bucket_off, b.flag_off) for b in plan.buckets)
         assert all(a[1] <= b[0] for a, b in zip(spans, spans[1:]))
+
+
+def test_lean_shuffle_oracle_equals_the_chunked_restatement():
+    """np_shuffle_lean (used for the BASELINE-size GPU parity tests) is the
+    chunked two-shot restatement without copies: equal bit for bit."""
+    rng = np.random.default_rng(42)
+    for p in (2, 3, 8):
+        for n, k in ((1, 1), (1000, 3), (4097, 8)):
+            bufs = [rng.standard_normal(n).astype(np.float32) for _ in range(p)]
+            theta = rng.standard_normal(n).astype(np.float32)
+            for epi in (O.EPI_SUM, O.EPI_SCALE, O.EPI_SGD):
+                want = O.np_allreduce(O.SHUFFLE, bufs, k, epi, 1.0 / p, 0.1, theta)
+                got = O.np_shuffle_lean(bufs, epi, 1.0 / p, 0.1, theta)
+                assert np.array_equal(got.view(np.uint32), want.view(np.uint32))

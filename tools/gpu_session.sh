@@ -1,9 +1,12 @@
 #!/bin/bash
 # Scratch GPU session driven through gpurun during development (rewritten per experiment):
 #   /usr/local/graft/bin/gpurun --gpus N -- "bash tools/gpu_session.sh"
-set -x
 export PYTHONUNBUFFERED=1
-for i in 1 2 3; do
-timeout 600 python -m pytest tests/test_multigpu.py -x -q > gpurun_out/mg_rep$i.txt 2>&1; echo "rep $i rc=$?"
-done
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=index,name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
+nvidia-smi topo -m >> gpurun_out/smi.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -x --durations=25 > gpurun_out/gputest.txt 2>&1; echo "gputest rc=$?"
+tail -5 gpurun_out/gputest.txt
+timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_n1.json 2> gpurun_out/bench_n1.err; echo "bench n1 rc=$?"
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 20 --warmup 5 > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err; echo "bench n2 rc=$?"
 echo done
