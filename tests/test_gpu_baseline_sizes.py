@@ -52,7 +52,11 @@ def _plan(model: str, p: int):
                        SimConfig(workers=max(2, p), network=NetworkModel(*NVLINK_MODEL),
                                  reduce=ReduceModel(400.0, 10.0)))
     numels = {gradsets.param_id(i, len(tensors)): t.numel for i, t in enumerate(tensors)}
-    return lower(art, numels, p, Pattern.SHUFFLE)
+    # all p emulated ranks' CTAs must be co-resident under the cooperative
+    # launch (the list kernels run one 512-thread CTA per SM): at most 148/p
+    # CTAs per rank.  Tile counts are a launch parameter; the element
+    # ownership (chunk/shard rule) does not depend on them.
+    return lower(art, numels, p, Pattern.SHUFFLE, max_ctas=148 // p)
 
 
 def _device_list(descs, dev):
@@ -158,7 +162,7 @@ def run_single(numel: int, p: int, depth: int, pattern: int, epochs: int = 2, ep
 
     dev = torch.device("cuda:0")
     ctas, bbytes, _ = N.bucket_layout(numel, depth, pattern, p)
-    ctas = min(ctas, max(1, 256 // p))  # co-resident under the cooperative (emulated) launch
+    ctas = min(ctas, 148 // p)  # co-resident under the cooperative (emulated) launch: one CTA per SM
     fbytes = N.flag_bytes_for(depth, ctas, pattern, p)
     flag_off = (bbytes + 255) // 256 * 256
     sgd = epi == O.EPI_SGD

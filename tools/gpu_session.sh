@@ -3,10 +3,11 @@
 #   /usr/local/graft/bin/gpurun --gpus N -- "bash tools/gpu_session.sh"
 export PYTHONUNBUFFERED=1
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=index,name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
-nvidia-smi topo -m >> gpurun_out/smi.txt 2>&1
-timeout 1500 python -m pytest tests -m gpu -q -x --durations=25 > gpurun_out/gputest.txt 2>&1; echo "gputest rc=$?"
-tail -5 gpurun_out/gputest.txt
-timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_n1.json 2> gpurun_out/bench_n1.err; echo "bench n1 rc=$?"
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 20 --warmup 5 > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err; echo "bench n2 rc=$?"
+run_sweep() {  # $1 = tag, $2 = library
+  CARAMEL_LIB=$2 SWEEP_MAX=$((1<<30)) SWEEP_ENGINES=single,fused timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+    --master-addr 127.0.0.1 --master-port 29512 tools/sweep.py > gpurun_out/ab_$1.jsonl 2> gpurun_out/ab_$1.err
+  echo "sweep $1 rc=$?"
+}
+run_sweep old tools/libcaramel_r01.so
+run_sweep new paper_2004_14020_b200/csrc/libcaramel_b200.so
 echo done
