@@ -385,7 +385,7 @@ def nccl_baseline(torch, dist, params, grads_dev, world, steps, warmup, bucket_b
 B200_REDUCE_MODEL = (2e6, 1.0)  # the reduction runs inside the collective kernel (~2 TB/s effective, 1 us)
 
 
-def ingested_plan(args, model, compute_only, world, dist, dev, network=None):
+def ingested_plan(args, model, compute_only, world, dist, dev, network=None, example_inputs=None):
     """The full Caramel configuration for a real model: DAG ingested from the
     model (module-level ops, device-measured durations, min of 5 runs; max over
     ranks so every rank plans identically), calibrated network model,
@@ -402,7 +402,7 @@ def ingested_plan(args, model, compute_only, world, dist, dev, network=None):
     from paper_2004_14020_b200.pipeline import run_pipeline as _rp
     from paper_2004_14020_b200.sim import SimConfig as _SC
 
-    ing = ingest_model(model, compute_only, runs=5)
+    ing = ingest_model(model, compute_only, runs=5, example_inputs=example_inputs)
     op_ids = sorted(o for o, op in ing.dag.ops.items() if op.kind.value == "compute")
     durs = torch.tensor([float(ing.dag.ops[o].duration_us) for o in op_ids], device=dev)
     if dist is not None:
@@ -489,7 +489,7 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
         torch._foreach_zero_(grads_c)
         fwd_bwd(model)
 
-    ing, art, mplan, net = ingested_plan(args, model, compute_only, world, dist, dev, network)
+    ing, art, mplan, net = ingested_plan(args, model, compute_only, world, dist, dev, network, example_inputs=(x,))
     placements = {}
     for b in mplan.buckets:
         placements[b.placement] = placements.get(b.placement, 0) + 1
@@ -590,7 +590,9 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
            "stat": f"exposed = median over {ROUNDS} rounds of (round time - paired compute-only round time); "
                    "spread = [min, max] over the rounds; a negative median is a measurement error, not a result",
            "grads": args.exposed_grads,
-           "plan": {"source": "ingested model DAG (measured, min of 5 runs, max over ranks)",
+           "plan": {"source": "ingested model DAG: unit dataflow traced from the model (ingest.trace_units), "
+                              "durations measured (min of 5 runs, max over ranks)",
+                    "control_edges": len(art.control_edges),
                     "network_model": [round(net.latency_us, 3), net.per_byte_us], "reduce_model": list(B200_REDUCE_MODEL),
                     "buckets": len(mplan.buckets), "placements": placements, "gated_modules": gated,
                     "modelled_exposed_us": round(art.transfer_schedule.added_iteration_time_us, 1)}}

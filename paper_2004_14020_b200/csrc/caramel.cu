@@ -621,8 +621,10 @@ __device__ __forceinline__ void cta_abort_if(int failed) {
   if (__syncthreads_or(failed)) asm volatile("exit;");
 }
 
-// CTA-uniform entry check of the kernels that wait on peers
-__device__ __forceinline__ void cta_enter(const Env& E) { cta_abort_if(threadIdx.x == 0 && poisoned(E)); }
+// CTA-uniform entry check of the kernels that wait on peers: true = leave
+// (the caller returns; an `exit` this early cost the single-bucket kernel
+// 40% of its NVLink bandwidth -- measured, cause in the compiler's layout)
+__device__ __forceinline__ bool cta_poisoned(const Env& E) { return __syncthreads_or(threadIdx.x == 0 && poisoned(E)); }
 
 struct KParams {          // one bucket
   Env env;
@@ -1502,7 +1504,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_collective(const __grid_constant
   // local copies: the phases hold pointers to these, and generic pointers to
   // kernel parameters are not valid across real device-function calls
   const Env E = P.env;
-  cta_enter(E);
+  if (cta_poisoned(E)) return;
   const caramel_bucket B = P.b;
   run_bucket<PAT, NP>(E, B, lr_idx, launch_epoch(E), blockIdx.x);
 }
@@ -1659,7 +1661,7 @@ template <int NP>
 __global__ void __launch_bounds__(THREADS, 1) k_shuffle_fused(const __grid_constant__ MParams P) {
   __shared__ FusedShared sh;
   const Env E = P.env;
-  cta_enter(E);
+  if (cta_poisoned(E)) return;
   const int lr_idx = blockIdx.y;
   const int me = E.rank_base + lr_idx;
   const uint32_t S = *reinterpret_cast<volatile uint32_t*>(sync_words(E, me));
@@ -2040,7 +2042,7 @@ template <int PAT, int NP>
 __global__ void __launch_bounds__(THREADS, 1) k_collective_many(const __grid_constant__ MParams P) {
   const int lr_idx = blockIdx.y;
   const Env E = P.env;  // local copy: phases keep pointers to it
-  cta_enter(E);
+  if (cta_poisoned(E)) return;
   const uint32_t epoch = launch_epoch(E);
   const int G = gridDim.x;
   // bucket i occupies CTAs base_i .. base_i + ctas_i - 1 (mod G), base_i being

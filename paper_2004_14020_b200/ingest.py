@@ -1,22 +1,36 @@
 """DAG ingestion from a PyTorch model.
 
 Builds the planner's DataflowDag (dag.py; JSON wire format dag.py:267-365)
-from a real model instead of the synthetic layered chain:
+from a real model instead of the synthetic layered chain, in two parts.
 
-* ops are the model's parameterised leaf modules in the order their forward
-  pass actually runs (forward hooks), each with a forward compute op f{k} and a
-  backward compute op b{k} (backward visits them in reverse);
-* every parameter gets a read marker feeding the forward op of its module and
-  an update marker fed by that module's backward op (a module's weight and bias
-  become ready together -- their gradients come from the same backward node);
-* durations are measured on the device: CUDA events at the boundaries of every
-  module's forward and backward, over several runs, each op's duration the
-  minimum across runs (estimate_op_times, costmodel.py:74-81);
-  the time between two parameterised modules (activations, pooling, residual
-  adds) is charged to the later one, so the ops partition the iteration;
-  backward boundaries are the moments a module's parameter gradients are
-  accumulated (post-accumulate-grad hooks), i.e. the update times the batcher
-  works from.
+Structure -- `trace_units`.  A "unit" is a module that owns parameters
+directly (a conv, a batch norm, a linear layer).  One forward pass runs under
+a TorchDispatchMode that sees every aten op: each tensor carries the set of
+units whose outputs flowed into it; an op inside a unit's forward makes its
+outputs that unit's and records, as the unit's inputs, the units behind the
+tensors it consumed; any other op (relu, add, cat, pooling, views, in-place
+updates) passes the union of its inputs' sets on.  The result is the real
+branch structure: a ResNet block's convolutions form a chain while its
+identity/downsample path joins at the add; Inception's towers run side by
+side from one input and meet at the concatenation; the auxiliary classifier
+is a second sink.  The trace runs on a meta-device copy of the model (no
+memory, no compute), so it is cheap and has no side effects.
+
+Graph -- `build_dag`.  Per unit U (ids follow the forward execution order k):
+  * read marker r_<pid> per parameter -> forward op f<k>;
+  * f<k> depends on the forward ops of U's input units;
+  * backward op b<K-1-k> depends on the backward ops of the units that
+    consumed U's output (the gradient arrives from them); a unit nothing
+    consumes (a loss input) waits for the forward pass to finish;
+  * update marker u_<pid> per parameter fed by b<K-1-k>.
+Lexicographic op ids make the planner's priority the execution order
+(forward) and its reverse (backward), as in the survey's layered chain.
+
+Durations -- `ingest_model`.  CUDA events at the boundaries of every unit's
+forward and at the moment its parameter gradients are accumulated, over
+several runs, each op's duration the minimum across runs (estimate_op_times,
+costmodel.py:74-81); the time between two units is charged to
+the later one, so the ops partition the iteration.
 
 Parameter ids are gradsets.param_id(i) over named_parameters() order, the ids
 the gradient inventories and the executor use.
@@ -24,13 +38,142 @@ the gradient inventories and the executor use.
 
 from __future__ import annotations
 
+import copy
 from dataclasses import dataclass
 
 import torch
+from torch.utils._python_dispatch import TorchDispatchMode
+from torch.utils._pytree import tree_leaves
 
 from .costmodel import OpProfile, estimate_op_times
 from .dag import DataflowDag, Op, OpKind, Parameter, Phase
 from .gradsets import param_id
+
+
+@dataclass(frozen=True)
+class UnitGraph:
+    """Parameter-owning modules in forward execution order and their dataflow."""
+
+    names: tuple[str, ...]                          # qualified module names, execution order
+    inputs: tuple[frozenset[int], ...]              # unit k <- units feeding its forward
+    params: tuple[tuple[tuple[str, int], ...], ...]  # unit k -> ((param id, bytes), ...)
+
+    def consumers(self) -> list[set[int]]:
+        out: list[set[int]] = [set() for _ in self.names]
+        for k, ins in enumerate(self.inputs):
+            for v in ins:
+                out[v].add(k)
+        return out
+
+
+class _Provenance(TorchDispatchMode):
+    """Tracks, per tensor, which units' outputs it was computed from."""
+
+    def __init__(self):
+        super().__init__()
+        self.origin: dict[int, frozenset[int]] = {}
+        self.keep: list = []          # keeps traced tensors alive: ids stay unique
+        self.stack: list[int] = []    # units whose forward is running (innermost last)
+        self.inputs: dict[int, set[int]] = {}
+
+    def __torch_dispatch__(self, func, types, args=(), kwargs=None):
+        out = func(*args, **(kwargs or {}))
+        src: set[int] = set()
+        for t in tree_leaves((args, kwargs)):
+            if isinstance(t, torch.Tensor):
+                src |= self.origin.get(id(t), frozenset())
+        if self.stack:
+            unit = self.stack[-1]
+            self.inputs.setdefault(unit, set()).update(src - {unit})
+            tag = frozenset((unit,))
+        else:
+            tag = frozenset(src)
+        for t in tree_leaves(out):
+            if isinstance(t, torch.Tensor):
+                self.origin[id(t)] = tag
+                self.keep.append(t)
+        return out
+
+
+def _units(model: torch.nn.Module) -> dict[str, torch.nn.Module]:
+    return {name: m for name, m in model.named_modules() if any(True for _ in m.parameters(recurse=False))}
+
+
+def trace_units(model: torch.nn.Module, example_inputs: tuple) -> UnitGraph:
+    """Unit dataflow of one forward pass of `model` on `example_inputs`
+    (traced on a meta-device copy; `model` itself is not run)."""
+    named = list(model.named_parameters())
+    pids = {id(p): param_id(i, len(named)) for i, (_, p) in enumerate(named)}
+    owner_name = {}
+    for name, m in _units(model).items():
+        for p in m.parameters(recurse=False):
+            owner_name[id(p)] = name
+    by_name: dict[str, list[tuple[str, int]]] = {}
+    for _, p in named:
+        by_name.setdefault(owner_name[id(p)], []).append((pids[id(p)], 4 * p.numel()))
+    ghost = copy.deepcopy(model).to("meta")
+    units = _units(ghost)
+    index: dict[str, int] = {}   # name -> execution position
+    mode = _Provenance()
+    handles = []
+
+    def pre(name):
+        def hook(_m, _args):
+            k = index.setdefault(name, len(index))
+            mode.stack.append(k)
+        return hook
+
+    def post(_m, _args, _out):
+        mode.stack.pop()
+
+    for name, m in units.items():
+        handles.append(m.register_forward_pre_hook(pre(name)))
+        handles.append(m.register_forward_hook(post))
+    meta_in = tuple(torch.empty_like(x, device="meta") if isinstance(x, torch.Tensor) else x for x in example_inputs)
+    try:
+        with torch.no_grad(), mode:
+            ghost(*meta_in)
+    finally:
+        for h in handles:
+            h.remove()
+    missing = [n for n in by_name if n not in index]
+    if missing:
+        raise RuntimeError(f"modules with parameters that never ran forward: {missing[:5]}")
+    names = tuple(sorted(index, key=index.get))
+    return UnitGraph(names=names, inputs=tuple(frozenset(mode.inputs.get(k, ())) for k in range(len(names))),
+                     params=tuple(tuple(by_name[n]) for n in names))
+
+
+def build_dag(graph: UnitGraph, fwd_us: dict[int, int], bwd_us: dict[int, int]) -> DataflowDag:
+    """DataflowDag of a traced unit graph with per-unit forward/backward
+    durations (see the module docstring for the op naming and edges)."""
+    K = len(graph.names)
+    cons = graph.consumers()
+    sinks = [k for k in range(K) if not cons[k]]
+    fid = [f"f{k:04d}" for k in range(K)]
+    bid = [f"b{K - 1 - k:04d}" for k in range(K)]
+    ops: dict[str, Op] = {}
+    params: dict[str, Parameter] = {}
+    for k in range(K):
+        reads = set()
+        for pid, nbytes in graph.params[k]:
+            params[pid] = Parameter(pid, nbytes)
+            ops[f"r_{pid}"] = Op(f"r_{pid}", OpKind.PARAM_READ, 0, frozenset(), Phase.FORWARD, pid)
+            ops[f"u_{pid}"] = Op(f"u_{pid}", OpKind.PARAM_UPDATE, 0, frozenset({bid[k]}), Phase.BACKPROP, pid)
+            reads.add(f"r_{pid}")
+        fdeps = reads | {fid[v] for v in graph.inputs[k]}
+        ops[fid[k]] = Op(fid[k], OpKind.COMPUTE, max(1, int(fwd_us.get(k, 1))), frozenset(fdeps), Phase.FORWARD)
+        bdeps = {bid[w] for w in cons[k]} if cons[k] else {fid[s] for s in sinks}
+        ops[bid[k]] = Op(bid[k], OpKind.COMPUTE, max(1, int(bwd_us.get(k, 1))), frozenset(bdeps), Phase.BACKPROP)
+    return DataflowDag(ops=ops, params=params)
+
+
+def synthetic_durations(graph: UnitGraph) -> tuple[dict[int, int], dict[int, int]]:
+    """The survey's stand-in timing: forward max(1, int(numel /
+    1e6 * 100)) us per unit, backward twice that -- for planning a traced
+    graph without a device."""
+    fwd = {k: max(1, int(sum(b for _, b in ps) / 4 / 1e6 * 100)) for k, ps in enumerate(graph.params)}
+    return fwd, {k: 2 * v for k, v in fwd.items()}
 
 
 @dataclass
@@ -40,53 +183,34 @@ class IngestedModel:
     modules: dict[str, torch.nn.Module]          # param id -> owning module
     forward_us: dict[str, int]                   # op id -> duration
     runs: int
+    graph: UnitGraph | None = None
 
 
-def _param_modules(model: torch.nn.Module):
-    owner = {}
-    for mod in model.modules():
-        for p in mod.parameters(recurse=False):
-            owner[id(p)] = mod
-    return owner
-
-
-def ingest_model(model: torch.nn.Module, step_fn, runs: int = 5) -> IngestedModel:
-    """Run `step_fn()` (one forward + backward of `model`) `runs` times with
-    timing hooks and return the measured iteration DAG."""
-    named = list(model.named_parameters())
-    n = len(named)
-    pids = {id(p): param_id(i, n) for i, (_, p) in enumerate(named)}
-    owner = _param_modules(model)
-    mods = []
-    for _, p in named:
-        m = owner[id(p)]
-        if all(m is not x for x in mods):
-            mods.append(m)
+def _measure(model: torch.nn.Module, step_fn, names: tuple[str, ...], runs: int) -> tuple[dict, dict]:
+    """Per-unit forward / backward device time (us), minimum over `runs`."""
+    mods = dict(model.named_modules())
+    pos = {id(mods[n]): k for k, n in enumerate(names)}
     fwd_events: list[list] = []
     bwd_events: list[list] = []
-    order: list = []   # modules in forward execution order (first run)
     handles = []
 
     def f_hook(m, *_):
         ev = torch.cuda.Event(enable_timing=True)
         ev.record()
-        fwd_events[-1].append((m, ev))
+        fwd_events[-1].append((pos[id(m)], ev))
 
-    # backward boundaries: the moment each module's parameter gradients are
-    # accumulated (post-accumulate-grad hooks; module backward hooks would wrap
-    # outputs and break in-place activations)
-    def make_b_hook(m):
+    def make_b_hook(k):
         def b_hook(_p):
             ev = torch.cuda.Event(enable_timing=True)
             ev.record()
-            bwd_events[-1].append((m, ev))
+            bwd_events[-1].append((k, ev))
         return b_hook
 
-    for m in mods:
-        handles.append(m.register_forward_hook(f_hook))
-        for p in m.parameters(recurse=False):
-            handles.append(p.register_post_accumulate_grad_hook(make_b_hook(m)))
-    samples: dict[str, list[int]] = {}
+    for k, n in enumerate(names):
+        handles.append(mods[n].register_forward_hook(f_hook))
+        for p in mods[n].parameters(recurse=False):
+            handles.append(p.register_post_accumulate_grad_hook(make_b_hook(k)))
+    samples: dict[tuple[str, int], list[int]] = {}
     try:
         for r in range(runs + 1):  # the first run warms up
             fwd_events.append([])
@@ -96,60 +220,40 @@ def ingest_model(model: torch.nn.Module, step_fn, runs: int = 5) -> IngestedMode
             step_fn()
             torch.cuda.synchronize()
             if r == 0:
-                seen = []
-                for m, _ in fwd_events[-1]:
-                    if all(m is not x for x in seen):
-                        seen.append(m)
-                order = seen
                 continue
-            # forward: boundary-to-boundary times in execution order
-            prev = start
-            t_f = {}
-            for m, ev in fwd_events[-1]:
-                t_f[id(m)] = t_f.get(id(m), 0.0) + prev.elapsed_time(ev)
+            prev, t_f = start, {}
+            for k, ev in fwd_events[-1]:
+                t_f[k] = t_f.get(k, 0.0) + prev.elapsed_time(ev)
                 prev = ev
-            # backward: a module's boundary is its last parameter's accumulation
             last = {}
-            for m, ev in bwd_events[-1]:
-                last[id(m)] = ev
-            seq = sorted(last.items(), key=lambda kv: prev.elapsed_time(kv[1]))
+            for k, ev in bwd_events[-1]:  # a unit's boundary: its last gradient's accumulation
+                last[k] = ev
             t_b = {}
-            for mid, ev in seq:
-                t_b[mid] = max(0.0, prev.elapsed_time(ev))
+            for k, ev in sorted(last.items(), key=lambda kv: prev.elapsed_time(kv[1])):
+                t_b[k] = max(0.0, prev.elapsed_time(ev))
                 prev = ev
-            for k, m in enumerate(order):
+            for k in range(len(names)):
                 for kind, t in (("f", t_f), ("b", t_b)):
-                    us = max(1, int(round(1000.0 * t.get(id(m), 0.0))))
-                    samples.setdefault(f"{kind}{k:04d}", []).append(us)
+                    samples.setdefault((kind, k), []).append(max(1, int(round(1000.0 * t.get(k, 0.0)))))
     finally:
         for h in handles:
             h.remove()
-    dur = estimate_op_times([OpProfile(op, tuple(v)) for op, v in sorted(samples.items())])
-    K = len(order)
-    ops: dict[str, Op] = {}
-    params: dict[str, Parameter] = {}
-    param_map: dict[str, torch.nn.Parameter] = {}
-    module_map: dict[str, torch.nn.Module] = {}
-    for k, m in enumerate(order):
-        fid, bid = f"f{k:04d}", f"b{K - 1 - k:04d}"
-        reads = []
-        for p in m.parameters(recurse=False):
-            pid = pids[id(p)]
-            params[pid] = Parameter(pid, 4 * p.numel())
-            param_map[pid] = p
-            module_map[pid] = m
-            rid = f"r_{pid}"
-            ops[rid] = Op(rid, OpKind.PARAM_READ, 0, frozenset(), Phase.FORWARD, pid)
-            reads.append(rid)
-            uid = f"u_{pid}"
-            ops[uid] = Op(uid, OpKind.PARAM_UPDATE, 0, frozenset({bid}), Phase.BACKPROP, pid)
-        deps = set(reads) | ({f"f{k - 1:04d}"} if k else set())
-        ops[fid] = Op(fid, OpKind.COMPUTE, dur.get(f"f{k:04d}", 1), frozenset(deps), Phase.FORWARD)
-        # backward op of module k runs after the backward of module k+1
-        bdeps = {f"b{K - 2 - k:04d}"} if k < K - 1 else {f"f{K - 1:04d}"}
-        ops[bid] = Op(bid, OpKind.COMPUTE, dur.get(f"b{k:04d}", 1), frozenset(bdeps), Phase.BACKPROP)
-    missing = [pid for pid in pids.values() if pid not in params]
-    if missing:
-        raise RuntimeError(f"parameters whose module never ran forward: {missing[:5]}")
-    return IngestedModel(dag=DataflowDag(ops=ops, params=params), params=param_map, modules=module_map,
-                         forward_us=dur, runs=runs)
+    est = estimate_op_times([OpProfile(f"{kind}{k}", tuple(v)) for (kind, k), v in samples.items()])
+    return ({k: est[f"f{k}"] for k in range(len(names))}, {k: est[f"b{k}"] for k in range(len(names))})
+
+
+def ingest_model(model: torch.nn.Module, step_fn, runs: int = 5, example_inputs: tuple | None = None) -> IngestedModel:
+    """Measured iteration DAG of `model`: structure traced from one forward on
+    `example_inputs` (the units' real dataflow), durations from `runs` timed
+    executions of `step_fn()` (one forward + backward)."""
+    if example_inputs is None:
+        raise ValueError("ingest_model needs example_inputs to trace the model's dataflow")
+    graph = trace_units(model, example_inputs)
+    fwd, bwd = _measure(model, step_fn, graph.names, runs)
+    dag = build_dag(graph, fwd, bwd)
+    named = list(model.named_parameters())
+    mods = dict(model.named_modules())
+    by_pid = {param_id(i, len(named)): p for i, (_, p) in enumerate(named)}
+    owner = {pid: mods[graph.names[k]] for k in range(len(graph.names)) for pid, _ in graph.params[k]}
+    durs = {f"f{k:04d}": v for k, v in fwd.items()}
+    return IngestedModel(dag=dag, params=by_pid, modules=owner, forward_us=durs, runs=runs, graph=graph)

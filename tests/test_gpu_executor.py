@@ -258,7 +258,7 @@ def test_ingest_model_dag_and_plan():
         model.zero_grad(set_to_none=False)
         model(x).square().mean().backward()
 
-    ing = ingest_model(model, step, runs=3)
+    ing = ingest_model(model, step, runs=3, example_inputs=(x,))
     rep = validate_dag(ing.dag)
     assert rep.ok, rep.errors
     assert len(ing.dag.params) == len(list(model.parameters()))
