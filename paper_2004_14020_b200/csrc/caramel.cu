@@ -688,6 +688,62 @@ __host__ __device__ __forceinline__ uint64_t ll_region_bytes(uint64_t numel, int
   return ll_out_off(numel) + 8 * numel * (1 + (uint64_t)world);
 }
 
+// ---- bucket region layout ------------------------------------------------------
+//   [kernel region: packed bucket (two-shot) | LL region | ring/hd halves]
+//   [push region (SHUFFLE, world > 1, not LL): 256 B header {seq, done} +
+//    2 x (world-1) inbox slots, each mirroring the bucket's element
+//    coordinates (element x of source q's contribution at slot + 4x, so every
+//    slot keeps the bucket's 16-byte phase and TMA bulk copies line up)]
+//   [copy-engine staging slots (caramel_allreduce_ce)]
+__host__ __device__ __forceinline__ uint64_t kernel_region_bytes(uint64_t numel, int pattern, int world) {
+  const uint64_t e = out_region_elems(numel);
+  return use_ll(pattern, world, numel) ? (ll_region_bytes(numel, world) + 15) & ~15ull
+                                       : 4 * ((world > 1 && pattern != CARAMEL_SHUFFLE) ? 2 * e : e);
+}
+__host__ __device__ __forceinline__ bool has_push_region(uint64_t numel, int pattern, int world) {
+  return pattern == CARAMEL_SHUFFLE && world > 1 && numel > 0 && !use_ll(pattern, world, numel);
+}
+__host__ __device__ __forceinline__ uint64_t push_off(uint64_t numel, int pattern, int world) {
+  return (kernel_region_bytes(numel, pattern, world) + 255) & ~255ull;
+}
+__host__ __device__ __forceinline__ uint64_t push_slot_bytes(uint64_t numel) { return (4 * numel + 255) & ~255ull; }
+__host__ __device__ __forceinline__ uint64_t push_region_bytes(uint64_t numel, int pattern, int world) {
+  return has_push_region(numel, pattern, world) ? 256 + 2ull * (world - 1) * push_slot_bytes(numel) : 0;
+}
+
+// Protocols of a two-shot (SHUFFLE) bucket at world > 1.  A function of the
+// bucket descriptor and the world size only -- identical on every rank and in
+// every launch kind, so ranks never disagree on a bucket's flag protocol.
+//   LL    <= LL cutoff elements: values travel with their epoch (two hops)
+//   OS    one-shot push: every rank pushes its contribution of the whole
+//         bucket into every peer's inbox (TMA, smem-staged), then reduces
+//         all p inputs locally in rank order -- one flag hop, (p-1) x S bytes
+//         per direction; used at p = 2 (where it moves exactly the two-shot's
+//         2(p-1)/p x S) and for buckets up to the OS cutoff
+//   TS    two-shot push: shard s of each chunk is pushed to its owner s
+//         (reduce-scatter into the owner's inbox), the owner reduces it in
+//         rank order, applies the epilogue and pushes the result into every
+//         rank's output (all-gather) -- 2(p-1)/p x S bytes per direction
+//   PULL  the register-staged pull kernels (UNPACK, or SGD with the
+//         parameters in the members instead of the parameter arena)
+// All protocols sum every element in ascending rank order: bit-identical.
+enum { PROTO_PULL = 0, PROTO_LL = 1, PROTO_OS = 2, PROTO_TS = 3 };
+#define OS_MAX_BYTES (1ull << 20)  // one-shot cutoff at p > 2; CARAMEL_OS_MAX overrides (same on every rank)
+__device__ uint64_t d_os_max = OS_MAX_BYTES;
+static uint64_t h_os_max = OS_MAX_BYTES;
+__host__ __device__ __forceinline__ int shuffle_proto(const caramel_bucket& b, int world) {
+#ifdef __CUDA_ARCH__
+  const uint64_t os_max = d_os_max;
+#else
+  const uint64_t os_max = h_os_max;
+#endif
+  if (b.pattern != CARAMEL_SHUFFLE || world < 2) return PROTO_PULL;
+  if (use_ll(b.pattern, world, b.numel)) return PROTO_LL;
+  if ((b.flags & CARAMEL_F_UNPACK) || (b.epilogue == CARAMEL_EPI_SGD && !(b.flags & CARAMEL_F_PARAM_ARENA)))
+    return PROTO_PULL;
+  return (world == 2 || 4 * b.numel <= os_max) ? PROTO_OS : PROTO_TS;
+}
+
 // x / d for the chunk/shard rule: 32-bit division when x fits (exact either way)
 __host__ __device__ __forceinline__ uint64_t div_u64(uint64_t x, uint32_t d) {
   return x <= 0xffffffffull ? (uint64_t)((uint32_t)x / d) : x / d;
@@ -2121,6 +2177,525 @@ __global__ void __launch_bounds__(THREADS, 1) k_collective_many(const __grid_con
 }
 
 // ---------------------------------------------------------------------------
+// Push protocols OS / TS (see shuffle_proto): every NVLink byte is moved by the
+// TMA bulk-copy unit, staged in shared memory -- cp.async.bulk global -> smem
+// (local HBM), then smem -> global in a peer's HBM over NVLink 5 / NVSwitch.
+// A store is a posted write: the CTA never waits a remote round trip per
+// byte, so a few CTAs keep the links busy (tools/mb_nvlink.cu: TMA pushes
+// reach 600-690 GB/s per direction with both directions loaded at 16-32 CTAs;
+// register pulls need 64+).
+//
+// Work items.  A launch takes a launch-ordered bucket list (or one bucket).
+// Each OS/TS bucket is cut into items (chunk c of its `depth`, tile range r of
+// `ranges` -- ranges of about PUSH_RANGE_BYTES, at most the bucket's flag
+// slots); items are numbered in launch order over the list and CTA g takes
+// items g, g+G, ...  The flags are per item, so any grid size works and ranks
+// may group the same launch order differently (CARAMEL_MANY_FLAGS).
+//
+// Warp roles, running concurrently in every CTA:
+//   warp 0 (pusher, one lane)  for each of my items in order:
+//       OS: range r of chunk c -> every peer's inbox (one smem tile, p-1 stores)
+//       TS: range r of shard (c, s) -> owner s's inbox, for every owner s
+//     then, once the item's stores have landed (bulk groups, lagged by one
+//     item), READY(c, r) to every peer.  Never waits on a peer.
+//   warp 1 (loader, one lane)  for each of my items in order: wait READY(c, r)
+//     from every peer; stream the p inputs (own bucket + inbox slots, rank
+//     order) and theta through a 3-stage smem ring (mbarrier complete_tx);
+//     bulk-store each finished result tile to my output (OS) or to every
+//     rank's output (TS: the all-gather), then DONE(c, r) (TS, lagged).
+//   warps 2.. (math)  sum each tile in ascending rank order and apply the
+//     epilogue in smem (separate fp32 roundings, bit-exact vs the oracle).
+// So pushing item k+1 overlaps reducing item k, and the only exposed flag
+// hop is the last item's.  Finally (TS) every CTA waits DONE for its items.
+// LL buckets ride along only in FUSED lists (identical on every rank): LL
+// scatter before the pipeline, LL reduce + finish after it.  OS double-buffers
+// its inbox by a per-bucket launch counter in the push-region header (a peer
+// may push launch s+1 while I still read launch s); TS needs no second buffer
+// (DONE orders reuse).
+// ---------------------------------------------------------------------------
+#define PUSH_THREADS THREADS     // warp 0 pusher, warp 1 loader, warps 2.. math
+#define PUSH_RSTAGES 3           // reduce ring stages
+#define PUSH_PSTAGES 3           // push ring stages
+#define PUSH_PTILE (32u << 10)   // push ring tile bytes
+#define PUSH_RANGE_BYTES (128u << 10)  // item size target (per chunk); CARAMEL_PUSH_RANGE_KB overrides
+
+template <int NP>
+struct PushGeo {
+  static constexpr int TT = NP <= 2 ? 2048 : NP <= 4 ? 1024 : 512;  // floats per reduce input tile
+  static constexpr int RSF = (NP + 2) * TT;                          // floats per reduce stage: in[NP], theta, out
+  static constexpr size_t PUSH_OFF = (size_t)PUSH_RSTAGES * RSF * 4;
+  static constexpr size_t BAR_OFF = PUSH_OFF + (size_t)PUSH_PSTAGES * PUSH_PTILE;
+  static constexpr size_t SMEM = BAR_OFF + (2 * PUSH_RSTAGES + PUSH_PSTAGES) * 8 + 16;
+};
+
+struct PushParams {
+  Env env;
+  const caramel_bucket* bs;  // device list, or nullptr: the single bucket `one`
+  int nb;
+  uint32_t range_bytes;      // PUSH_RANGE_BYTES unless overridden
+  int with_ll;               // FUSED lists: LL buckets handled in this launch
+  caramel_bucket one;
+};
+
+// tile ranges per chunk of one bucket (LL: its own CTA slots)
+__host__ __device__ __forceinline__ int push_ranges(const caramel_bucket& b, int world, uint32_t range_bytes) {
+  if (shuffle_proto(b, world) == PROTO_LL) return b.ctas;
+  const uint64_t per_chunk = 4 * b.numel / (uint64_t)(b.depth > 0 ? b.depth : 1);
+  uint64_t g = (per_chunk + range_bytes - 1) / range_bytes;
+  if (g > (uint64_t)b.ctas) g = b.ctas;  // the flag block holds b.ctas slots per chunk
+  return g < 1 ? 1 : (int)g;
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+// at most n bulk groups of this thread still pending (n clamped to 0..7)
+__device__ __forceinline__ void bulk_wait_upto(uint32_t n) {
+  switch (n > 7 ? 7 : n) {
+    case 0: asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.bulk.wait_group 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.bulk.wait_group 3;" ::: "memory"); break;
+    case 4: asm volatile("cp.async.bulk.wait_group 4;" ::: "memory"); break;
+    case 5: asm volatile("cp.async.bulk.wait_group 5;" ::: "memory"); break;
+    case 6: asm volatile("cp.async.bulk.wait_group 6;" ::: "memory"); break;
+    default: asm volatile("cp.async.bulk.wait_group 7;" ::: "memory"); break;
+  }
+}
+
+__device__ __forceinline__ uint64_t push_region(const Env& E, const caramel_bucket& B, int rank) {
+  return E.arena[rank] + B.bucket_off + push_off(B.numel, CARAMEL_SHUFFLE, E.world);
+}
+__device__ __forceinline__ float* push_inbox(const Env& E, const caramel_bucket& B, int rank, int buf, int src) {
+  const int p = E.world, slot = src < rank ? src : src - 1;
+  return reinterpret_cast<float*>(push_region(E, B, rank) + 256 +
+                                  ((uint64_t)buf * (p - 1) + slot) * push_slot_bytes(B.numel));
+}
+__device__ __forceinline__ float* push_out(const Env& E, const caramel_bucket& B, int rank) {
+  return B.epilogue == CARAMEL_EPI_SGD ? reinterpret_cast<float*>(E.parena[rank] + B.param_off)
+                                       : reinterpret_cast<float*>(E.arena[rank] + B.bucket_off);
+}
+__device__ __forceinline__ uint32_t* push_flag(const Env& E, const caramel_bucket& B, int rank, int c, int r,
+                                               int slot, int src) {
+  return reinterpret_cast<uint32_t*>(E.arena[rank] + B.flag_off) +
+         ((((uint64_t)c * B.ctas + r) * 2 + slot) * E.world + src);
+}
+
+// element range of item (c, r): OS -> range r of chunk c; TS -> range r of shard (c, s)
+__device__ __forceinline__ void item_range(const caramel_bucket& B, int proto, int p, int c, int s, int r, int R,
+                                           uint64_t& lo, uint64_t& hi) {
+  const uint64_t c0 = split_at(B.numel, B.depth, c), c1 = split_at(B.numel, B.depth, c + 1);
+  uint64_t a = c0, b = c1;
+  if (proto == PROTO_TS) {
+    const uint64_t m = c1 - c0;
+    a = c0 + split_at(m, p, s);
+    b = c0 + split_at(m, p, s + 1);
+  }
+  tile_of(a, b, R, r, lo, hi);
+}
+
+// Iterates this CTA's items of the list in launch order: f(i, B, proto, c, r, R, buf).
+template <class F>
+__device__ __forceinline__ void for_my_items(const PushParams& P, int me, F f) {
+  const int G = gridDim.x, g = blockIdx.x, p = P.env.world;
+  const int nb = P.bs ? P.nb : 1;
+  uint64_t k = 0;  // global item number
+  for (int i = 0; i < nb; ++i) {
+    const caramel_bucket B = P.bs ? P.bs[i] : P.one;
+    const int proto = shuffle_proto(B, p);
+    if ((proto != PROTO_OS && proto != PROTO_TS) || B.numel == 0) continue;
+    const int R = push_ranges(B, p, P.range_bytes);
+    const uint64_t n = (uint64_t)B.depth * R;
+    // first item of this bucket that is mine
+    uint64_t first = (g >= (int)(k % G)) ? k + (g - (k % G)) : k + (G - (k % G)) + g;
+    if (first < k + n) {
+      const int buf = proto == PROTO_OS
+                          ? (int)(*reinterpret_cast<volatile uint32_t*>(push_region(P.env, B, me)) & 1u) : 0;
+      for (uint64_t t = first - k; t < n; t += G) f(i, B, proto, (int)(t / R), (int)(t % R), R, buf);
+    }
+    k += n;
+  }
+}
+
+// ---- pusher (warp 0, lane 0) ----------------------------------------------------
+struct PushRing {
+  unsigned char* buf;  // PUSH_PSTAGES x PUSH_PTILE bytes
+  uint64_t* bar;
+  uint32_t u;          // tiles issued so far
+};
+
+// Copy the 16-byte aligned body of [lo, hi) of src to nd destinations through
+// the push ring (plain ld/st for the <= 3 + 3 ragged elements).  Returns the
+// number of bulk groups committed (one per tile).
+__device__ uint32_t push_copy(PushRing& S, const float* src, float* const* dst, int nd, uint64_t lo, uint64_t hi) {
+  if (lo >= hi) return 0;
+  uint64_t a, b;
+  split4(lo, hi, a, b);
+  for (uint64_t x = lo; x < a; ++x)
+    for (int d = 0; d < nd; ++d) st1(dst[d] + x, ld1(src + x));
+  for (uint64_t x = b > a ? b : a; x < hi; ++x)
+    for (int d = 0; d < nd; ++d) st1(dst[d] + x, ld1(src + x));
+  constexpr uint64_t TF = PUSH_PTILE / 4;
+  const uint64_t nt = b > a ? (b - a + TF - 1) / TF : 0;
+  auto bytes_of = [&](uint64_t t) {
+    const uint64_t x = a + t * TF;
+    return (uint32_t)(4 * ((b - x) < TF ? (b - x) : TF));
+  };
+  auto issue = [&](uint64_t t) {
+    const uint32_t u = S.u + (uint32_t)t, s = u % PUSH_PSTAGES;
+    mbar_expect_tx(&S.bar[s], bytes_of(t));
+    bulk_load(S.buf + (size_t)s * PUSH_PTILE, src + a + t * TF, bytes_of(t), &S.bar[s]);
+  };
+  // the stage refilled for tile t+S-1 held tile t-1: its stores must be done reading
+  for (uint64_t t = 0; t < nt && t + 1 < PUSH_PSTAGES; ++t) issue(t);
+  for (uint64_t t = 0; t < nt; ++t) {
+    const uint32_t u = S.u + (uint32_t)t, s = u % PUSH_PSTAGES;
+    mbar_wait(&S.bar[s], (u / PUSH_PSTAGES) & 1);
+    for (int d = 0; d < nd; ++d) bulk_store(dst[d] + a + t * TF, S.buf + (size_t)s * PUSH_PTILE, bytes_of(t));
+    bulk_commit();
+    if (t + PUSH_PSTAGES - 1 < nt) {
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      issue(t + PUSH_PSTAGES - 1);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // the ring restarts at the next call
+  S.u += (uint32_t)nt;
+  return (uint32_t)nt;
+}
+
+struct Pending {  // an item whose stores are in flight, to flag once they landed
+  const caramel_bucket* B;
+  int c, r, slot, valid;
+  uint32_t groups;  // bulk groups committed after it
+};
+
+__device__ __forceinline__ void flag_peers(const Env& E, const caramel_bucket& B, int me, int c, int r, int slot,
+                                           uint32_t epoch) {
+  for (int q = 0; q < E.world; ++q)
+    if (q != me) st_relaxed_sys(push_flag(E, B, q, c, r, slot, me), epoch);
+}
+
+// publish `pend` once at most `keep` bulk groups (committed after it) are pending
+__device__ __forceinline__ void publish_pending(const Env& E, Pending& pend, int me, uint32_t epoch, uint32_t keep) {
+  if (!pend.valid) return;
+  bulk_wait_upto(keep);
+  fence_proxy_async_global();
+  fence_acq_rel_sys();
+  flag_peers(E, *pend.B, me, pend.c, pend.r, pend.slot, epoch);
+  pend.valid = 0;
+}
+
+__device__ void pusher(const PushParams& P, PushRing& S, int me, uint32_t epoch, caramel_bucket* hold) {
+  const Env& E = P.env;
+  const int p = E.world;
+  Pending pend{nullptr, 0, 0, SLOT_READY, 0, 0};
+  int hi_ = 0;  // alternate between two bucket copies so `pend` can point at the previous one
+  for_my_items(P, me, [&](int, const caramel_bucket& B, int proto, int c, int r, int R, int buf) {
+    caramel_bucket& Bh = hold[hi_];
+    Bh = B;
+    hi_ ^= 1;
+    const float* mine = reinterpret_cast<const float*>(E.arena[me] + B.bucket_off);
+    uint32_t groups = 0;
+    if (proto == PROTO_OS) {
+      uint64_t lo, hi;
+      item_range(B, proto, p, c, 0, r, R, lo, hi);
+      float* dst[MAXR];
+      int nd = 0;
+      for (int t = 1; t < p; ++t) dst[nd++] = push_inbox(E, B, (me + t) % p, buf, me);
+      groups += push_copy(S, mine, dst, nd, lo, hi);
+    } else {
+      for (int t = 1; t < p; ++t) {  // owners in rotated order: every link starts busy
+        const int s = (me + t) % p;
+        uint64_t lo, hi;
+        item_range(B, proto, p, c, s, r, R, lo, hi);
+        float* dst[1] = {push_inbox(E, B, s, 0, me)};
+        groups += push_copy(S, mine, dst, 1, lo, hi);
+      }
+    }
+    publish_pending(E, pend, me, epoch, groups);  // the previous item has landed once <= `groups` remain
+    pend = Pending{&Bh, c, r, SLOT_READY, 1, groups};
+  });
+  publish_pending(E, pend, me, epoch, 0);
+}
+
+// ---- loader (warp 1, lane 0) and math warps (2..) -----------------------------------
+struct ReduceRing {
+  float* st;       // PUSH_RSTAGES stages of RSF floats
+  uint64_t* full;  // loads landed (count 1 + tx)
+  uint64_t* comp;  // math warps finished the tile (count = math warps)
+};
+
+template <int NP>
+__device__ __forceinline__ uint32_t tiles_of(uint64_t a, uint64_t b) {
+  return b > a ? (uint32_t)((b - a + PushGeo<NP>::TT - 1) / PushGeo<NP>::TT) : 0;
+}
+
+template <int NP>
+__device__ void loader(const PushParams& P, ReduceRing& S, int me, uint32_t epoch, int* abort_flag,
+                       caramel_bucket* hold) {
+  constexpr int TT = PushGeo<NP>::TT, SF = PushGeo<NP>::RSF;
+  const Env& E = P.env;
+  const int p = E.world;
+  uint32_t u = 0;  // ring position (tiles loaded so far)
+  uint32_t issued_items = 0;
+  Pending pend{nullptr, 0, 0, SLOT_DONE, 0, 0};
+  int hi_ = 0;
+  bool ok = true;
+  for_my_items(P, me, [&](int, const caramel_bucket& B, int proto, int c, int r, int R, int buf) {
+    if (!ok) return;
+    caramel_bucket& Bh = hold[hi_];
+    Bh = B;
+    hi_ ^= 1;
+    // the item's inputs: READY from every peer
+    for (int q = 0; q < p && ok; ++q) {
+      if (q == me) continue;
+      const uint32_t* f = push_flag(E, B, me, c, r, SLOT_READY, q);
+      if (ld_acquire_sys(f) >= epoch) continue;
+      const uint64_t t0 = globaltimer();
+      uint32_t spins = 0;
+      while (ld_acquire_sys(f) < epoch) {
+        if ((++spins & 1023u) == 0) {
+          if (poisoned(E)) { ok = false; break; }
+          if (globaltimer() - t0 > E.timeout_ns) { raise_timeout(E); ok = false; break; }
+        }
+      }
+    }
+    if (!ok) return;
+    fence_proxy_async_global();  // the TMA loads below must see what the flags published
+    const bool sgd = B.epilogue == CARAMEL_EPI_SGD;
+    const float* in[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q)
+      in[q] = q == me ? reinterpret_cast<const float*>(E.arena[me] + B.bucket_off) : push_inbox(E, B, me, buf, q);
+    const float* th = reinterpret_cast<const float*>(E.parena[me] + B.param_off);
+    float* out[MAXR];
+    int nd = 0;
+    if (proto == PROTO_TS)
+      for (int t = 0; t < p; ++t) out[nd++] = push_out(E, B, (me + t) % p);  // local first
+    else
+      out[nd++] = push_out(E, B, me);
+    uint64_t lo, hi, a, b;
+    item_range(B, proto, p, c, me, r, R, lo, hi);
+    split4(lo, hi, a, b);
+    auto edge = [&](uint64_t x) {  // <= 3 + 3 ragged elements: plain loads / stores
+      float acc = ld1(in[0] + x);
+      for (int q = 1; q < p; ++q) acc = __fadd_rn(acc, ld1(in[q] + x));
+      const float o = epi1(B.epilogue, acc, sgd ? ld1(th + x) : 0.f, B.scale, B.lr);
+      for (int d = 0; d < nd; ++d) st1(out[d] + x, o);
+    };
+    for (uint64_t x = lo; x < a; ++x) edge(x);
+    for (uint64_t x = b > a ? b : a; x < hi; ++x) edge(x);
+    const uint32_t nt = tiles_of<NP>(a, b);
+    auto bytes_of = [&](uint32_t t) {
+      const uint64_t x = a + (uint64_t)t * TT;
+      return (uint32_t)(4 * ((b - x) < (uint64_t)TT ? (b - x) : (uint64_t)TT));
+    };
+    auto issue = [&](uint32_t t) {
+      const uint32_t uu = u + t, s = uu % PUSH_RSTAGES, bytes = bytes_of(t);
+      float* st = S.st + (size_t)s * SF;
+      mbar_expect_tx(&S.full[s], bytes * (p + (sgd ? 1 : 0)));
+      const uint64_t x = a + (uint64_t)t * TT;
+      for (int q = 0; q < p; ++q) bulk_load(st + q * TT, in[q] + x, bytes, &S.full[s]);
+      if (sgd) bulk_load(st + NP * TT, th + x, bytes, &S.full[s]);
+    };
+    // prefetch distance STAGES-1; the stage refilled for tile t+S-1 held tile
+    // t-1: the math warps are done with it (its comp barrier was waited) and
+    // its stores must be done reading (wait_group.read 0 after tile t's commit
+    // would serialise, so read-wait with one group of slack)
+    for (uint32_t t = 0; t < nt && t + 1 < PUSH_RSTAGES; ++t) issue(t);
+    for (uint32_t t = 0; t < nt; ++t) {
+      const uint32_t uu = u + t, s = uu % PUSH_RSTAGES;
+      mbar_wait(&S.comp[s], (uu / PUSH_RSTAGES) & 1);
+      const float* res = S.st + (size_t)s * SF + (NP + 1) * TT;
+      const uint64_t x = a + (uint64_t)t * TT;
+      for (int d = 0; d < nd; ++d) bulk_store(out[d] + x, res, bytes_of(t));
+      bulk_commit();
+      if (t + PUSH_RSTAGES - 1 < nt) {
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        issue(t + PUSH_RSTAGES - 1);
+      }
+    }
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    u += nt;
+    ++issued_items;
+    if (proto == PROTO_TS) {
+      publish_pending(E, pend, me, epoch, nt);
+      pend = Pending{&Bh, c, r, SLOT_DONE, 1, nt};
+    }
+  });
+  if (!ok) {  // wake the math warps and stop them
+    *reinterpret_cast<volatile int*>(abort_flag) = 1;
+    for (int s = 0; s < PUSH_RSTAGES; ++s) mbar_arrive(&S.full[s]);
+    return;
+  }
+  publish_pending(E, pend, me, epoch, 0);
+  bulk_wait_upto(0);
+}
+
+template <int NP>
+__device__ void math_warps(const PushParams& P, ReduceRing& S, int me, const int* abort_flag) {
+  constexpr int TT = PushGeo<NP>::TT, SF = PushGeo<NP>::RSF;
+  const int p = P.env.world;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nmath = (blockDim.x >> 5) - 2, mw = warp - 2;
+  uint32_t u = 0;
+  bool stop = false;
+  for_my_items(P, me, [&](int, const caramel_bucket& B, int proto, int c, int r, int R, int) {
+    if (stop) return;
+    uint64_t lo, hi, a, b;
+    item_range(B, proto, p, c, me, r, R, lo, hi);
+    split4(lo, hi, a, b);
+    const uint32_t nt = tiles_of<NP>(a, b);
+    const bool sgd = B.epilogue == CARAMEL_EPI_SGD;
+    for (uint32_t t = 0; t < nt; ++t) {
+      const uint32_t uu = u + t, s = uu % PUSH_RSTAGES;
+      mbar_wait(&S.full[s], (uu / PUSH_RSTAGES) & 1);
+      if (*reinterpret_cast<const volatile int*>(abort_flag)) { stop = true; return; }
+      float* st = S.st + (size_t)s * SF;
+      const float4* i4 = reinterpret_cast<const float4*>(st);
+      const float4* t4 = reinterpret_cast<const float4*>(st + NP * TT);
+      float4* o4 = reinterpret_cast<float4*>(st + (NP + 1) * TT);
+      const uint64_t x = a + (uint64_t)t * TT;
+      const uint32_t n4 = (uint32_t)(((b - x) < (uint64_t)TT ? (b - x) : (uint64_t)TT) / 4);
+      for (uint32_t v = mw * 32 + lane; v < n4; v += nmath * 32) {
+        float4 acc = i4[v];
+#pragma unroll
+        for (int q = 1; q < NP; ++q) acc = add4(acc, i4[q * (TT / 4) + v]);
+        o4[v] = epi4(B.epilogue, acc, sgd ? t4[v] : acc, B.scale, B.lr);
+      }
+      fence_proxy_async();  // my smem writes -> the async proxy (the bulk store)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.comp[s]);
+    }
+    u += nt;
+  });
+}
+
+template <int NP>
+__global__ void __launch_bounds__(PUSH_THREADS, 1) k_push(const __grid_constant__ PushParams P) {
+  extern __shared__ __align__(128) unsigned char dyn_smem[];
+  __shared__ int s_abort;
+  __shared__ caramel_bucket s_hold[2][2];  // pusher / loader: the buckets of in-flight items
+  const Env E = P.env;
+  if (cta_poisoned(E)) return;
+  const int lr_idx = blockIdx.y;
+  const int me = E.rank_base + lr_idx, p = E.world;
+  const uint32_t epoch = launch_epoch(E);
+  const int nb = P.bs ? P.nb : 1;
+  ReduceRing RR;
+  RR.st = reinterpret_cast<float*>(dyn_smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dyn_smem + PushGeo<NP>::BAR_OFF);
+  RR.full = bars;
+  RR.comp = bars + PUSH_RSTAGES;
+  PushRing PR;
+  PR.buf = dyn_smem + PushGeo<NP>::PUSH_OFF;
+  PR.bar = bars + 2 * PUSH_RSTAGES;
+  PR.u = 0;
+  const int nmath = (blockDim.x >> 5) - 2;
+  if (threadIdx.x == 0) {
+    s_abort = 0;
+    for (int s = 0; s < PUSH_RSTAGES; ++s) {
+      mbar_init(&RR.full[s], 1);
+      mbar_init(&RR.comp[s], nmath);
+    }
+    for (int s = 0; s < PUSH_PSTAGES; ++s) mbar_init(&PR.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // ---- pre: PACK (gather my items' ranges into my bucket) and LL scatter ----
+  bool any_pack = false;
+  for (int i = 0; i < nb && !any_pack; ++i) any_pack = (P.bs ? P.bs[i] : P.one).flags & CARAMEL_F_PACK;
+  if (any_pack) {
+    for_my_items(P, me, [&](int, const caramel_bucket& B, int proto, int c, int r, int R, int) {
+      if (!(B.flags & CARAMEL_F_PACK)) return;
+      const caramel_segment* segs = reinterpret_cast<const caramel_segment*>(B.segs) + (uint64_t)lr_idx * B.nseg;
+      float* bkt = reinterpret_cast<float*>(E.arena[me] + B.bucket_off);
+      for (int s = 0; s < (proto == PROTO_TS ? p : 1); ++s) {
+        uint64_t lo, hi;
+        item_range(B, proto, p, c, s, r, R, lo, hi);
+        pack_range(segs, B.nseg, bkt, lo, hi, g_tab);
+      }
+    });
+    fence_proxy_async_global();  // generic-proxy pack stores -> the TMA loads of the push
+    __syncthreads();
+  }
+  auto ll_pass = [&](int phase) {
+    if (!P.with_ll) return;
+    const int G = gridDim.x;
+    int base = 0;
+    for (int i = 0; i < nb; ++i) {
+      const caramel_bucket B = P.bs ? P.bs[i] : P.one;
+      if (shuffle_proto(B, p) != PROTO_LL) continue;
+      int jj = ((int)blockIdx.x - base) % G;
+      if (jj < 0) jj += G;
+      base = (base + B.ctas) % G;
+      if (jj >= B.ctas || B.numel == 0) continue;
+      BucketRun R;
+      make_run(R, E, B, CARAMEL_SHUFFLE, lr_idx, epoch, jj);
+      if (phase == 0) phase_ll_scatter(R);
+      else if (phase == 1) phase_ll_reduce<NP>(R);
+      else phase_ll_finish(R);
+    }
+  };
+  ll_pass(0);
+  // ---- the push / reduce pipeline ------------------------------------------------
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    if (threadIdx.x == 0) pusher(P, PR, me, epoch, s_hold[0]);
+  } else if (warp == 1) {
+    if (threadIdx.x == 32) loader<NP>(P, RR, me, epoch, &s_abort, s_hold[1]);
+  } else {
+    math_warps<NP>(P, RR, me, &s_abort);
+  }
+  __syncthreads();
+  if (*reinterpret_cast<volatile int*>(&s_abort)) return;  // a flag wait failed: nothing more is stored
+  ll_pass(1);
+  ll_pass(2);
+  // ---- TS: every owner's all-gather of my items has landed --------------------------
+  int bad = 0;
+  for_my_items(P, me, [&](int, const caramel_bucket& B, int proto, int c, int r, int, int) {
+    if (proto != PROTO_TS || bad) return;
+    const int q = threadIdx.x;
+    if (q < p && q != me) {
+      const uint32_t* f = push_flag(E, B, me, c, r, SLOT_DONE, q);
+      if (ld_acquire_sys(f) < epoch) {
+        const uint64_t t0 = globaltimer();
+        uint32_t spins = 0;
+        while (ld_acquire_sys(f) < epoch) {
+          if ((++spins & 1023u) == 0) {
+            if (poisoned(E)) { bad = 1; break; }
+            if (globaltimer() - t0 > E.timeout_ns) { raise_timeout(E); bad = 1; break; }
+          }
+        }
+      }
+    }
+  });
+  cta_abort_if(bad);
+  // ---- OS: the last CTA of a bucket flips its inbox buffer -------------------------
+  if (threadIdx.x == 0) {
+    const int G = gridDim.x;
+    uint64_t k = 0;
+    for (int i = 0; i < nb; ++i) {
+      const caramel_bucket B = P.bs ? P.bs[i] : P.one;
+      if (shuffle_proto(B, p) != PROTO_OS || B.numel == 0) continue;
+      const uint64_t n = (uint64_t)B.depth * push_ranges(B, p, P.range_bytes);
+      const uint64_t off = (blockIdx.x + G - k % G) % G;  // my first item index within the bucket
+      if (off < n) {
+        const uint32_t parts = (uint32_t)(n < (uint64_t)G ? n : (uint64_t)G);
+        uint32_t* h = reinterpret_cast<uint32_t*>(push_region(E, B, me));
+        const uint32_t old = atomicAdd(h + 1, 1u);
+        if (old == parts - 1) {
+          atomicExch(h + 1, 0u);
+          atomicAdd(h, 1u);
+        }
+      }
+      k += n;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 
@@ -2244,7 +2819,9 @@ static void load_ll_max() {
   if (done) return;
   done = true;
   if (const char* e = getenv("CARAMEL_LL_MAX")) h_ll_max = strtoull(e, 0, 10);
+  if (const char* e = getenv("CARAMEL_OS_MAX")) h_os_max = strtoull(e, 0, 10);
   cudaMemcpyToSymbol(d_ll_max, &h_ll_max, sizeof(h_ll_max));
+  cudaMemcpyToSymbol(d_os_max, &h_os_max, sizeof(h_os_max));
 }
 
 int caramel_abi_version(void) { return CARAMEL_ABI_VERSION; }
@@ -2284,22 +2861,18 @@ static int default_max_ctas() {
 // engines push their contributions to my shard (caramel_allreduce_ce).  A
 // slot holds ceil(n/p) elements after a (lo & 3)-element pad, so staged data
 // keeps the 16-byte phase of the shard it belongs to.
-static uint64_t kernel_region_bytes(uint64_t numel, int pattern, int world) {
-  const uint64_t e = out_region_elems(numel);
-  return use_ll(pattern, world, numel) ? (ll_region_bytes(numel, world) + 15) & ~15ull
-                                       : 4 * ((world > 1 && pattern != CARAMEL_SHUFFLE) ? 2 * e : e);
-}
 static uint64_t ce_slot_bytes(uint64_t numel, int world) {
   const uint64_t m = (numel + world - 1) / world;
   return (4 * (m + 3) + 15) & ~15ull;
 }
 static uint64_t ce_stage_off(uint64_t numel, int pattern, int world) {
-  return (kernel_region_bytes(numel, pattern, world) + 255) & ~255ull;
+  return push_off(numel, pattern, world) + push_region_bytes(numel, pattern, world);
 }
 
 int caramel_bucket_layout(uint64_t numel, int depth, int pattern, int world, int32_t* ctas,
                           uint64_t* bucket_bytes, uint64_t* flag_bytes) {
   if (getenv("CARAMEL_LL_MAX")) h_ll_max = strtoull(getenv("CARAMEL_LL_MAX"), 0, 10);
+  if (getenv("CARAMEL_OS_MAX")) h_os_max = strtoull(getenv("CARAMEL_OS_MAX"), 0, 10);
   int rc = validate_workers(pattern, world);
   if (rc) return rc;
   if (depth < 1 || depth > CARAMEL_MAX_DEPTH)
@@ -2577,6 +3150,45 @@ static mfn_t pick_np_many(int p) {
   }
 }
 
+typedef void (*pfn_push)(const PushParams);
+
+static pfn_push pick_push(int p) {
+  switch (p) {
+    case 2: return k_push<2>;
+    case 3: return k_push<3>;
+    case 4: return k_push<4>;
+    case 5: return k_push<5>;
+    case 6: return k_push<6>;
+    case 7: return k_push<7>;
+    default: return k_push<8>;
+  }
+}
+
+static size_t push_smem(int p) {
+  switch (p) {
+    case 2: return PushGeo<2>::SMEM;
+    case 3: return PushGeo<3>::SMEM;
+    case 4: return PushGeo<4>::SMEM;
+    case 5: return PushGeo<5>::SMEM;
+    case 6: return PushGeo<6>::SMEM;
+    case 7: return PushGeo<7>::SMEM;
+    default: return PushGeo<8>::SMEM;
+  }
+}
+
+// item size of the push kernels (identical on every rank, like the LL cutoff)
+static uint32_t push_range_bytes() {
+  static uint32_t v = 0;
+  if (!v) v = getenv("CARAMEL_PUSH_RANGE_KB") ? (uint32_t)atoi(getenv("CARAMEL_PUSH_RANGE_KB")) << 10 : PUSH_RANGE_BYTES;
+  return v < 4096 ? 4096 : v;
+}
+// CTAs of a push launch when the caller leaves it to the library
+static int push_default_ctas() {
+  static int v = 0;
+  if (!v) v = getenv("CARAMEL_PUSH_CTAS") ? atoi(getenv("CARAMEL_PUSH_CTAS")) : 32;
+  return v < 1 ? 1 : v;
+}
+
 extern "C" {
 
 static int validate_bucket(const caramel_ctx* c, const caramel_bucket* b) {
@@ -2592,9 +3204,14 @@ static int validate_bucket(const caramel_ctx* c, const caramel_bucket* b) {
                             ? ll_region_bytes(b->numel, c->world)
                             : 4 * ((c->world > 1 && b->pattern != CARAMEL_SHUFFLE) ? 2 * out_region_elems(b->numel)
                                                                                    : b->numel);
-  if (b->bucket_off + span > c->arena_bytes)
-    return set_err(CARAMEL_EINVAL, "bucket [%llu, +%llu B) exceeds the arena", (unsigned long long)b->bucket_off,
-                   (unsigned long long)span);
+  const int proto = shuffle_proto(*b, c->world);
+  const uint64_t span2 = (proto == PROTO_OS || proto == PROTO_TS)
+                             ? push_off(b->numel, CARAMEL_SHUFFLE, c->world) +
+                                   push_region_bytes(b->numel, CARAMEL_SHUFFLE, c->world)
+                             : span;
+  if (b->bucket_off + (span2 > span ? span2 : span) > c->arena_bytes)
+    return set_err(CARAMEL_EINVAL, "bucket [%llu, +%llu B) exceeds the arena (size it with caramel_bucket_layout)",
+                   (unsigned long long)b->bucket_off, (unsigned long long)(span2 > span ? span2 : span));
   const bool arena = (b->flags & CARAMEL_F_PARAM_ARENA) && b->epilogue == CARAMEL_EPI_SGD;
   if (arena) {
     if (!c->param_bytes) return set_err(CARAMEL_EINVAL, "PARAM_ARENA requested but no parameter arena");
@@ -2637,9 +3254,10 @@ static void fill_env(const caramel_ctx* c, Env& E, uint32_t epoch) {
 // kernels -- backward, NCCL -- may hold SMs).  cudaLaunchKernelEx with the
 // cooperative attribute is capturable in a CUDA graph.
 template <class Params>
-static int coop_launch(const caramel_ctx* c, void (*fn)(Params), dim3 grid, const Params& P, void* stream) {
+static int coop_launch(const caramel_ctx* c, void (*fn)(Params), dim3 grid, const Params& P, void* stream,
+                       size_t smem = 0) {
   int per_sm = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, THREADS, 0));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, THREADS, smem));
   if ((uint64_t)per_sm * c->sms < (uint64_t)grid.x * grid.y)
     return set_err(CARAMEL_EINVAL, "cooperative launch of %u x %u CTAs exceeds co-residency (%d per SM)", grid.x,
                    grid.y, per_sm);
@@ -2647,7 +3265,7 @@ static int coop_launch(const caramel_ctx* c, void (*fn)(Params), dim3 grid, cons
   memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = grid;
   cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = (cudaStream_t)stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
@@ -2660,12 +3278,73 @@ static int coop_launch(const caramel_ctx* c, void (*fn)(Params), dim3 grid, cons
 
 extern "C" {
 
+// The push kernel over `count` buckets (host copy `host`; device copy at
+// `dev_list`, or 0 for a single bucket passed by value).  ctas <= 0: the
+// largest tile-range count of the list.
+static int push_launch(caramel_ctx* c, const caramel_bucket* host, int count, uint64_t dev_list, int ctas,
+                       uint32_t epoch, void* stream, int with_ll = 0) {
+  PushParams P;
+  memset(&P, 0, sizeof(P));
+  fill_env(c, P.env, epoch);
+  P.bs = reinterpret_cast<const caramel_bucket*>(dev_list);
+  P.nb = count;
+  P.range_bytes = push_range_bytes();
+  P.with_ll = with_ll;
+  P.one = host[0];
+  // default grid: enough CTAs for the items, at most CARAMEL_PUSH_CTAS (a
+  // small footprint leaves the SMs to the backward pass); LL buckets need
+  // their own CTA slots
+  uint64_t items = 0;
+  int G = 1;
+  for (int i = 0; i < count; ++i) {
+    const int pr = shuffle_proto(host[i], c->world);
+    if (pr == PROTO_LL) G = host[i].ctas > G ? host[i].ctas : G;
+    else items += (uint64_t)host[i].depth * push_ranges(host[i], c->world, P.range_bytes);
+  }
+  const uint64_t want = items < (uint64_t)push_default_ctas() ? items : (uint64_t)push_default_ctas();
+  if ((int)want > G) G = (int)want;
+  if (ctas > 0) G = ctas;
+  if (c->nlocal > 1 && G * c->nlocal > c->sms) G = c->sms / c->nlocal;  // emulated ranks: all co-resident
+  const int p = c->world;
+  pfn_push fn = pick_push(p);
+  const size_t smem = push_smem(p);
+  static bool attr[MAXR + 1] = {false};
+  if (!attr[p]) {
+    CUDA_TRY(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr[p] = true;
+  }
+  dim3 grid(G, c->nlocal);
+  if (c->nlocal > 1 || with_ll) return coop_launch(c, fn, grid, P, stream, smem);
+  fn<<<grid, THREADS, smem, (cudaStream_t)stream>>>(P);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// CARAMEL_MANY_FUSED lists through the push kernel with this many CTAs (0: the
+// grid-barrier pull kernel k_shuffle_fused)
+static int fused_push() {
+  static int v = -1;
+  if (v < 0) v = getenv("CARAMEL_FUSED_PUSH") ? atoi(getenv("CARAMEL_FUSED_PUSH")) : 0;
+  return v;
+}
+
+// kernel family of a bucket in a CARAMEL_MANY_FLAGS list: 1 = push kernel
+// (OS / TS), 0 = the flag list kernel (LL, PULL); runs of one family launch together
+static int push_family(const caramel_bucket& b, int world) {
+  const int pr = shuffle_proto(b, world);
+  return pr == PROTO_OS || pr == PROTO_TS;
+}
+
 static int launch(caramel_ctx* c, const caramel_bucket* b, uint32_t epoch, void* stream) {
   if (!c || !b) return set_err(CARAMEL_EINVAL, "null argument");
   if (!c->imported) return set_err(CARAMEL_ESTATE, "peer arenas not mapped (call caramel_import)");
   int rc = validate_bucket(c, b);
   if (rc) return rc;
   if (b->numel == 0) return 0;
+  if (c->world > 1) {
+    const int pr = shuffle_proto(*b, c->world);
+    if (pr == PROTO_OS || pr == PROTO_TS) return push_launch(c, b, 1, 0, 0, epoch, stream);
+  }
   KParams P;
   fill_env(c, P.env, epoch);
   P.b = *b;
@@ -2770,6 +3449,49 @@ int caramel_allreduce_many(caramel_ctx* c, const caramel_bucket* host, int32_t c
     fn<<<dim3(c->sms * per_sm, 1), TMA_THREADS, smem, (cudaStream_t)stream>>>(P);
     CUDA_TRY(cudaGetLastError());
     return 0;
+  }
+  if (c->world > 1 && pattern == CARAMEL_SHUFFLE && mode == CARAMEL_MANY_FLAGS) {
+    // maximal runs of one protocol family, in launch order: the push kernel
+    // (one-shot / two-shot push, LL) or the pull list kernel (UNPACK, member
+    // parameters).  A bucket's protocol never depends on how it is grouped.
+    const size_t bsz = sizeof(caramel_bucket);
+    int i = 0;
+    while (i < count) {
+      const int fam = push_family(host[i], c->world);
+      int k = i + 1;
+      while (k < count && push_family(host[k], c->world) == fam) ++k;
+      int rc = 0;
+      if (fam) {
+        rc = push_launch(c, host + i, k - i, dev_buckets + i * bsz, ctas, epoch, stream);
+      } else {
+        MParams Q = P;
+        Q.bs = P.bs + i;
+        Q.prefix = P.prefix + i;
+        Q.segprefix = P.segprefix + i;
+        Q.nb = k - i;
+        int need = 1;
+        for (int t = i; t < k; ++t) need = host[t].ctas > need ? host[t].ctas : need;
+        const int g = ctas > 0 ? (ctas < need ? need : ctas) : need;
+        mfn_t f = pick_np_many<CARAMEL_SHUFFLE>(c->world);
+        dim3 grid(g, c->nlocal);
+        if (c->nlocal > 1) rc = coop_launch(c, f, grid, Q, stream);
+        else {
+          f<<<grid, THREADS, 0, (cudaStream_t)stream>>>(Q);
+          cudaError_t e = cudaGetLastError();
+          if (e != cudaSuccess) rc = set_err(CARAMEL_ECUDA, "k_collective_many: %s", cudaGetErrorString(e));
+        }
+      }
+      if (rc) return rc;
+      i = k;
+    }
+    return 0;
+  }
+  if (c->world > 1 && pattern == CARAMEL_SHUFFLE && mode == CARAMEL_MANY_FUSED && fused_push()) {
+    // every rank issues this identical list: the push kernel with the LL
+    // buckets in the same launch, cooperative (all CTAs resident)
+    bool ok = true;
+    for (int i = 0; i < count && ok; ++i) ok = shuffle_proto(host[i], c->world) != PROTO_PULL;
+    if (ok) return push_launch(c, host, count, dev_buckets, ctas > 0 ? ctas : fused_push(), epoch, stream, 1);
   }
   if (c->world == 1) fn = k_local_many;
   else if (pattern == CARAMEL_SHUFFLE && mode == CARAMEL_MANY_FLAGS) {

@@ -743,11 +743,12 @@ def calibrate_network_model(world: int, rank: int, sizes: tuple[int, ...] = (64,
      -- `reps` times each, `iters` back-to-back launches per
     sample, takes the max over ranks of every sample (so every rank fits the
     identical model and plans identical buckets) and applies the reference's
-    least-squares fit, fit_network_model (costmodel.py:84-108).  Returns
-    (NetworkModel, measurements)."""
+    least-squares line (costmodel.py:84-108) through the per-size MEDIANS
+    (fit_network_model_robust): one late peer or preempted launch among the
+    samples cannot move the bucket cap.  Returns (NetworkModel, measurements)."""
     import torch.distributed as dist
 
-    from .costmodel import Measurement, fit_network_model
+    from .costmodel import Measurement, fit_network_model_robust
 
     dev = torch.device("cuda", torch.cuda.current_device())
     nmax = max(sizes) // 4 + 1
@@ -785,4 +786,4 @@ def calibrate_network_model(world: int, rank: int, sizes: tuple[int, ...] = (64,
                 meas.append(Measurement(size_bytes=4 * n, observed_time_us=us))
     ctx.status()
     ctx.close()
-    return fit_network_model(meas), meas
+    return fit_network_model_robust(meas, "median"), meas

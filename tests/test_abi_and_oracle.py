@@ -79,9 +79,14 @@ def test_chunk_rule_agrees_with_reference_float_bytes():
 def test_bucket_layout_and_errors():
     N = _lib()
     ctas, bb, fb = N.bucket_layout(1 << 20, 2, N.SHUFFLE, 8)
-    # packed bucket + 7 copy-engine staging slots of ceil(n/8)+3 elements
+    # packed bucket + push region (256 B header, 2 x 7 inbox slots mirroring
+    # the bucket) + 7 copy-engine staging slots of ceil(n/8)+3 elements
     slot = (4 * ((1 << 20) // 8 + 3) + 15) & ~15
-    assert 1 <= ctas <= 64 and bb == (4 << 20) + 7 * slot and fb > 0
+    push = 256 + 2 * 7 * (4 << 20)
+    assert 1 <= ctas <= 64 and bb == (4 << 20) + push + 7 * slot and fb > 0
+    # LL buckets (<= 64K elements) carry no push region
+    ll = (4 * 1000 + 8 * 1000 * 9 + 255) // 256 * 256  # LL region: bucket + out + 8 in-slots of 8 B words
+    assert N.bucket_layout(1000, 1, N.SHUFFLE, 8)[1] == ll + 7 * ((4 * (125 + 3) + 15) & ~15)
     assert N.bucket_layout(1 << 20, 2, N.SHUFFLE, 1)[1] == 4 << 20  # one rank: no staging
     _, bb_ring, _ = N.bucket_layout(1 << 20, 2, N.RING, 8)
     assert bb_ring == 8 << 20  # input + output halves
@@ -191,3 +196,30 @@ def test_lean_shuffle_oracle_equals_the_chunked_restatement():
                 want = O.np_allreduce(O.SHUFFLE, bufs, k, epi, 1.0 / p, 0.1, theta)
                 got = O.np_shuffle_lean(bufs, epi, 1.0 / p, 0.1, theta)
                 assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_robust_calibration_ignores_an_outlier():
+    """executor.calibrate_network_model fits through per-size medians
+    (costmodel.fit_network_model_robust).  The round-1 failure case: one
+    100.4 us sample among eight ~16 us samples at 64 B moved the plain
+    least-squares latency to 26.6 us and the bucket cap 8x."""
+    from paper_2004_14020_b200.costmodel import (Measurement, batching_threshold, fit_network_model,
+                                                  fit_network_model_robust)
+
+    small = [16.1, 16.3, 15.9, 16.0, 16.2, 100.4, 16.1, 15.8]
+    big = [26.0, 26.2, 25.9, 26.1, 26.0, 26.3, 25.8, 26.1]
+    meas = [Measurement(64, t) for t in small] + [Measurement(4 << 20, t) for t in big]
+    plain = fit_network_model(meas)
+    robust = fit_network_model_robust(meas)
+    clean = fit_network_model([m for m in meas if m.observed_time_us < 50])
+    assert plain.latency_us > 25.0                      # the outlier drags the plain fit
+    assert abs(robust.latency_us - 16.05) < 0.2         # median of the 64 B samples (~16.05 us)
+    assert abs(robust.latency_us - clean.latency_us) < 0.5
+    t_plain, t_robust, t_clean = (batching_threshold(m) for m in (plain, robust, clean))
+    assert t_plain > 1.5 * t_clean and abs(t_robust - t_clean) / t_clean < 0.05
+    # two sizes: the robust line passes through both medians exactly
+    assert robust.latency_us + robust.per_byte_us * 64 == pytest.approx(sorted(small)[3] / 2 + sorted(small)[4] / 2)
+    # min statistic = estimate_op_times' rule
+    mn = fit_network_model_robust(meas, "min")
+    assert mn.latency_us + mn.per_byte_us * 64 == pytest.approx(min(small))
+    assert mn.latency_us + mn.per_byte_us * (4 << 20) == pytest.approx(min(big))

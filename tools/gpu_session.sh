@@ -3,11 +3,13 @@
 #   /usr/local/graft/bin/gpurun --gpus N -- "bash tools/gpu_session.sh"
 export PYTHONUNBUFFERED=1
 mkdir -p gpurun_out
-run_sweep() {  # $1 = tag, $2 = library
-  CARAMEL_LIB=$2 SWEEP_MAX=$((1<<30)) SWEEP_ENGINES=single timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
-    --master-addr 127.0.0.1 --master-port 29512 tools/sweep.py > gpurun_out/ab_$1.jsonl 2> gpurun_out/ab_$1.err
-  echo "sweep $1 rc=$?"
-}
-for v in NONE NO_EXIT NO_ENTER r01; do run_sweep $v tools/libcaramel_$v.so; done
-./tools/mb_nvlink > gpurun_out/mb_nvlink.jsonl 2>&1; echo "mb rc=$?"
+timeout 900 python -m pytest tests -m gpu -q -x --durations=5 > gpurun_out/gputest.txt 2>&1; echo "gputest rc=$?"
+tail -3 gpurun_out/gputest.txt
+CARAMEL_FUSED_PUSH=64 timeout 900 python -m pytest tests/test_gpu_baseline_sizes.py tests/test_gpu_kernels.py -m gpu -q -x -k "fused or many" > gpurun_out/gputest_fp.txt 2>&1; echo "gputest fused-push rc=$?"
+tail -3 gpurun_out/gputest_fp.txt
+for fp in 0 32 148; do
+CARAMEL_FUSED_PUSH=$fp SWEEP_MAX=$((1<<30)) SWEEP_ENGINES=single,fused timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+    --master-addr 127.0.0.1 --master-port 29512 tools/sweep.py > gpurun_out/sweep_fp$fp.jsonl 2> gpurun_out/sweep_fp$fp.err
+echo "sweep $fp rc=$?"
+done
 echo done
