@@ -707,8 +707,21 @@ __host__ __device__ __forceinline__ uint64_t push_off(uint64_t numel, int patter
   return (kernel_region_bytes(numel, pattern, world) + 255) & ~255ull;
 }
 __host__ __device__ __forceinline__ uint64_t push_slot_bytes(uint64_t numel) { return (4 * numel + 255) & ~255ull; }
-__host__ __device__ __forceinline__ uint64_t push_region_bytes(uint64_t numel, int pattern, int world) {
-  return has_push_region(numel, pattern, world) ? 256 + 2ull * (world - 1) * push_slot_bytes(numel) : 0;
+// Push items: chunk c of `depth`, tile range r of push_ranges() ~PUSH_RANGE_BYTES each.
+#define PUSH_RANGE_BYTES (128u << 10)
+__host__ __device__ __forceinline__ int push_ranges(uint64_t numel, int depth) {
+  const uint64_t per_chunk = 4 * numel / (uint64_t)(depth > 0 ? depth : 1);
+  const uint64_t r = (per_chunk + PUSH_RANGE_BYTES - 1) / PUSH_RANGE_BYTES;
+  return r < 1 ? 1 : (int)r;
+}
+// flag words of the push items: [chunk][range][READY, DONE][source rank]
+__host__ __device__ __forceinline__ uint64_t push_flag_bytes(uint64_t numel, int depth, int world) {
+  return ((uint64_t)depth * push_ranges(numel, depth) * 2 * world * 4 + 255) & ~255ull;
+}
+__host__ __device__ __forceinline__ uint64_t push_region_bytes(uint64_t numel, int depth, int pattern, int world) {
+  return has_push_region(numel, pattern, world)
+             ? 256 + push_flag_bytes(numel, depth, world) + 2ull * (world - 1) * push_slot_bytes(numel)
+             : 0;
 }
 
 // Protocols of a two-shot (SHUFFLE) bucket at world > 1.  A function of the
@@ -741,7 +754,7 @@ __host__ __device__ __forceinline__ int shuffle_proto(const caramel_bucket& b, i
   if (use_ll(b.pattern, world, b.numel)) return PROTO_LL;
   if ((b.flags & CARAMEL_F_UNPACK) || (b.epilogue == CARAMEL_EPI_SGD && !(b.flags & CARAMEL_F_PARAM_ARENA)))
     return PROTO_PULL;
-  return (world == 2 || 4 * b.numel <= os_max) ? PROTO_OS : PROTO_TS;
+  return 4 * b.numel <= os_max ? PROTO_OS : PROTO_TS;
 }
 
 // x / d for the chunk/shard rule: 32-bit division when x fits (exact either way)
@@ -2216,12 +2229,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_collective_many(const __grid_con
 #define PUSH_THREADS THREADS     // warp 0 pusher, warp 1 loader, warps 2.. math
 #define PUSH_RSTAGES 3           // reduce ring stages
 #define PUSH_PSTAGES 3           // push ring stages
-#define PUSH_PTILE (32u << 10)   // push ring tile bytes
-#define PUSH_RANGE_BYTES (128u << 10)  // item size target (per chunk); CARAMEL_PUSH_RANGE_KB overrides
+#define PUSH_PTILE (24u << 10)   // push ring tile bytes
 
 template <int NP>
 struct PushGeo {
-  static constexpr int TT = NP <= 2 ? 2048 : NP <= 4 ? 1024 : 512;  // floats per reduce input tile
+  static constexpr int TT = NP <= 2 ? 3072 : NP <= 4 ? 2048 : 1024;  // floats per reduce input tile
   static constexpr int RSF = (NP + 2) * TT;                          // floats per reduce stage: in[NP], theta, out
   static constexpr size_t PUSH_OFF = (size_t)PUSH_RSTAGES * RSF * 4;
   static constexpr size_t BAR_OFF = PUSH_OFF + (size_t)PUSH_PSTAGES * PUSH_PTILE;
@@ -2232,19 +2244,9 @@ struct PushParams {
   Env env;
   const caramel_bucket* bs;  // device list, or nullptr: the single bucket `one`
   int nb;
-  uint32_t range_bytes;      // PUSH_RANGE_BYTES unless overridden
   int with_ll;               // FUSED lists: LL buckets handled in this launch
   caramel_bucket one;
 };
-
-// tile ranges per chunk of one bucket (LL: its own CTA slots)
-__host__ __device__ __forceinline__ int push_ranges(const caramel_bucket& b, int world, uint32_t range_bytes) {
-  if (shuffle_proto(b, world) == PROTO_LL) return b.ctas;
-  const uint64_t per_chunk = 4 * b.numel / (uint64_t)(b.depth > 0 ? b.depth : 1);
-  uint64_t g = (per_chunk + range_bytes - 1) / range_bytes;
-  if (g > (uint64_t)b.ctas) g = b.ctas;  // the flag block holds b.ctas slots per chunk
-  return g < 1 ? 1 : (int)g;
-}
 
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
@@ -2269,7 +2271,7 @@ __device__ __forceinline__ uint64_t push_region(const Env& E, const caramel_buck
 }
 __device__ __forceinline__ float* push_inbox(const Env& E, const caramel_bucket& B, int rank, int buf, int src) {
   const int p = E.world, slot = src < rank ? src : src - 1;
-  return reinterpret_cast<float*>(push_region(E, B, rank) + 256 +
+  return reinterpret_cast<float*>(push_region(E, B, rank) + 256 + push_flag_bytes(B.numel, B.depth, p) +
                                   ((uint64_t)buf * (p - 1) + slot) * push_slot_bytes(B.numel));
 }
 __device__ __forceinline__ float* push_out(const Env& E, const caramel_bucket& B, int rank) {
@@ -2278,8 +2280,8 @@ __device__ __forceinline__ float* push_out(const Env& E, const caramel_bucket& B
 }
 __device__ __forceinline__ uint32_t* push_flag(const Env& E, const caramel_bucket& B, int rank, int c, int r,
                                                int slot, int src) {
-  return reinterpret_cast<uint32_t*>(E.arena[rank] + B.flag_off) +
-         ((((uint64_t)c * B.ctas + r) * 2 + slot) * E.world + src);
+  return reinterpret_cast<uint32_t*>(push_region(E, B, rank) + 256) +
+         ((((uint64_t)c * push_ranges(B.numel, B.depth) + r) * 2 + slot) * E.world + src);
 }
 
 // element range of item (c, r): OS -> range r of chunk c; TS -> range r of shard (c, s)
@@ -2305,7 +2307,7 @@ __device__ __forceinline__ void for_my_items(const PushParams& P, int me, F f) {
     const caramel_bucket B = P.bs ? P.bs[i] : P.one;
     const int proto = shuffle_proto(B, p);
     if ((proto != PROTO_OS && proto != PROTO_TS) || B.numel == 0) continue;
-    const int R = push_ranges(B, p, P.range_bytes);
+    const int R = push_ranges(B.numel, B.depth);
     const uint64_t n = (uint64_t)B.depth * R;
     // first item of this bucket that is mine
     uint64_t first = (g >= (int)(k % G)) ? k + (g - (k % G)) : k + (G - (k % G)) + g;
@@ -2365,15 +2367,17 @@ __device__ uint32_t push_copy(PushRing& S, const float* src, float* const* dst, 
 }
 
 struct Pending {  // an item whose stores are in flight, to flag once they landed
-  const caramel_bucket* B;
+  uint64_t flag_off;  // its bucket's push flags (byte offset in every rank's arena)
+  int ranges;         // ranges per chunk
   int c, r, slot, valid;
-  uint32_t groups;  // bulk groups committed after it
 };
 
-__device__ __forceinline__ void flag_peers(const Env& E, const caramel_bucket& B, int me, int c, int r, int slot,
-                                           uint32_t epoch) {
+__device__ __forceinline__ void flag_peers(const Env& E, const Pending& it, int me, uint32_t epoch) {
   for (int q = 0; q < E.world; ++q)
-    if (q != me) st_relaxed_sys(push_flag(E, B, q, c, r, slot, me), epoch);
+    if (q != me)
+      st_relaxed_sys(reinterpret_cast<uint32_t*>(E.arena[q] + it.flag_off) +
+                         ((((uint64_t)it.c * it.ranges + it.r) * 2 + it.slot) * E.world + me),
+                     epoch);
 }
 
 // publish `pend` once at most `keep` bulk groups (committed after it) are pending
@@ -2382,19 +2386,15 @@ __device__ __forceinline__ void publish_pending(const Env& E, Pending& pend, int
   bulk_wait_upto(keep);
   fence_proxy_async_global();
   fence_acq_rel_sys();
-  flag_peers(E, *pend.B, me, pend.c, pend.r, pend.slot, epoch);
+  flag_peers(E, pend, me, epoch);
   pend.valid = 0;
 }
 
-__device__ void pusher(const PushParams& P, PushRing& S, int me, uint32_t epoch, caramel_bucket* hold) {
+__device__ void pusher(const PushParams& P, PushRing& S, int me, uint32_t epoch) {
   const Env& E = P.env;
   const int p = E.world;
-  Pending pend{nullptr, 0, 0, SLOT_READY, 0, 0};
-  int hi_ = 0;  // alternate between two bucket copies so `pend` can point at the previous one
+  Pending pend{0, 0, 0, 0, SLOT_READY, 0};
   for_my_items(P, me, [&](int, const caramel_bucket& B, int proto, int c, int r, int R, int buf) {
-    caramel_bucket& Bh = hold[hi_];
-    Bh = B;
-    hi_ ^= 1;
     const float* mine = reinterpret_cast<const float*>(E.arena[me] + B.bucket_off);
     uint32_t groups = 0;
     if (proto == PROTO_OS) {
@@ -2414,7 +2414,7 @@ __device__ void pusher(const PushParams& P, PushRing& S, int me, uint32_t epoch,
       }
     }
     publish_pending(E, pend, me, epoch, groups);  // the previous item has landed once <= `groups` remain
-    pend = Pending{&Bh, c, r, SLOT_READY, 1, groups};
+    pend = Pending{B.bucket_off + push_off(B.numel, CARAMEL_SHUFFLE, p) + 256, R, c, r, SLOT_READY, 1};
   });
   publish_pending(E, pend, me, epoch, 0);
 }
@@ -2432,21 +2432,16 @@ __device__ __forceinline__ uint32_t tiles_of(uint64_t a, uint64_t b) {
 }
 
 template <int NP>
-__device__ void loader(const PushParams& P, ReduceRing& S, int me, uint32_t epoch, int* abort_flag,
-                       caramel_bucket* hold) {
+__device__ void loader(const PushParams& P, ReduceRing& S, int me, uint32_t epoch, int* abort_flag) {
   constexpr int TT = PushGeo<NP>::TT, SF = PushGeo<NP>::RSF;
   const Env& E = P.env;
   const int p = E.world;
   uint32_t u = 0;  // ring position (tiles loaded so far)
   uint32_t issued_items = 0;
-  Pending pend{nullptr, 0, 0, SLOT_DONE, 0, 0};
-  int hi_ = 0;
+  Pending pend{0, 0, 0, 0, SLOT_DONE, 0};
   bool ok = true;
   for_my_items(P, me, [&](int, const caramel_bucket& B, int proto, int c, int r, int R, int buf) {
     if (!ok) return;
-    caramel_bucket& Bh = hold[hi_];
-    Bh = B;
-    hi_ ^= 1;
     // the item's inputs: READY from every peer
     for (int q = 0; q < p && ok; ++q) {
       if (q == me) continue;
@@ -2519,10 +2514,8 @@ __device__ void loader(const PushParams& P, ReduceRing& S, int me, uint32_t epoc
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     u += nt;
     ++issued_items;
-    if (proto == PROTO_TS) {
-      publish_pending(E, pend, me, epoch, nt);
-      pend = Pending{&Bh, c, r, SLOT_DONE, 1, nt};
-    }
+    publish_pending(E, pend, me, epoch, nt);  // the previous TS item's all-gather has landed
+    if (proto == PROTO_TS) pend = Pending{B.bucket_off + push_off(B.numel, CARAMEL_SHUFFLE, p) + 256, R, c, r, SLOT_DONE, 1};
   });
   if (!ok) {  // wake the math warps and stop them
     *reinterpret_cast<volatile int*>(abort_flag) = 1;
@@ -2576,7 +2569,6 @@ template <int NP>
 __global__ void __launch_bounds__(PUSH_THREADS, 1) k_push(const __grid_constant__ PushParams P) {
   extern __shared__ __align__(128) unsigned char dyn_smem[];
   __shared__ int s_abort;
-  __shared__ caramel_bucket s_hold[2][2];  // pusher / loader: the buckets of in-flight items
   const Env E = P.env;
   if (cta_poisoned(E)) return;
   const int lr_idx = blockIdx.y;
@@ -2603,23 +2595,7 @@ __global__ void __launch_bounds__(PUSH_THREADS, 1) k_push(const __grid_constant_
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  // ---- pre: PACK (gather my items' ranges into my bucket) and LL scatter ----
-  bool any_pack = false;
-  for (int i = 0; i < nb && !any_pack; ++i) any_pack = (P.bs ? P.bs[i] : P.one).flags & CARAMEL_F_PACK;
-  if (any_pack) {
-    for_my_items(P, me, [&](int, const caramel_bucket& B, int proto, int c, int r, int R, int) {
-      if (!(B.flags & CARAMEL_F_PACK)) return;
-      const caramel_segment* segs = reinterpret_cast<const caramel_segment*>(B.segs) + (uint64_t)lr_idx * B.nseg;
-      float* bkt = reinterpret_cast<float*>(E.arena[me] + B.bucket_off);
-      for (int s = 0; s < (proto == PROTO_TS ? p : 1); ++s) {
-        uint64_t lo, hi;
-        item_range(B, proto, p, c, s, r, R, lo, hi);
-        pack_range(segs, B.nseg, bkt, lo, hi, g_tab);
-      }
-    });
-    fence_proxy_async_global();  // generic-proxy pack stores -> the TMA loads of the push
-    __syncthreads();
-  }
+  // (PACK buckets were gathered into the bucket by k_pack launches before this kernel)
   auto ll_pass = [&](int phase) {
     if (!P.with_ll) return;
     const int G = gridDim.x;
@@ -2642,9 +2618,9 @@ __global__ void __launch_bounds__(PUSH_THREADS, 1) k_push(const __grid_constant_
   // ---- the push / reduce pipeline ------------------------------------------------
   const int warp = threadIdx.x >> 5;
   if (warp == 0) {
-    if (threadIdx.x == 0) pusher(P, PR, me, epoch, s_hold[0]);
+    if (threadIdx.x == 0) pusher(P, PR, me, epoch);
   } else if (warp == 1) {
-    if (threadIdx.x == 32) loader<NP>(P, RR, me, epoch, &s_abort, s_hold[1]);
+    if (threadIdx.x == 32) loader<NP>(P, RR, me, epoch, &s_abort);
   } else {
     math_warps<NP>(P, RR, me, &s_abort);
   }
@@ -2678,10 +2654,11 @@ __global__ void __launch_bounds__(PUSH_THREADS, 1) k_push(const __grid_constant_
     uint64_t k = 0;
     for (int i = 0; i < nb; ++i) {
       const caramel_bucket B = P.bs ? P.bs[i] : P.one;
-      if (shuffle_proto(B, p) != PROTO_OS || B.numel == 0) continue;
-      const uint64_t n = (uint64_t)B.depth * push_ranges(B, p, P.range_bytes);
+      const int proto = shuffle_proto(B, p);
+      if ((proto != PROTO_OS && proto != PROTO_TS) || B.numel == 0) continue;
+      const uint64_t n = (uint64_t)B.depth * push_ranges(B.numel, B.depth);
       const uint64_t off = (blockIdx.x + G - k % G) % G;  // my first item index within the bucket
-      if (off < n) {
+      if (proto == PROTO_OS && off < n) {
         const uint32_t parts = (uint32_t)(n < (uint64_t)G ? n : (uint64_t)G);
         uint32_t* h = reinterpret_cast<uint32_t*>(push_region(E, B, me));
         const uint32_t old = atomicAdd(h + 1, 1u);
@@ -2865,8 +2842,8 @@ static uint64_t ce_slot_bytes(uint64_t numel, int world) {
   const uint64_t m = (numel + world - 1) / world;
   return (4 * (m + 3) + 15) & ~15ull;
 }
-static uint64_t ce_stage_off(uint64_t numel, int pattern, int world) {
-  return push_off(numel, pattern, world) + push_region_bytes(numel, pattern, world);
+static uint64_t ce_stage_off(uint64_t numel, int depth, int pattern, int world) {
+  return push_off(numel, pattern, world) + push_region_bytes(numel, depth, pattern, world);
 }
 
 int caramel_bucket_layout(uint64_t numel, int depth, int pattern, int world, int32_t* ctas,
@@ -2897,7 +2874,7 @@ int caramel_bucket_layout(uint64_t numel, int depth, int pattern, int world, int
   if (bucket_bytes) {
     *bucket_bytes = kernel_region_bytes(numel, pattern, world);
     if (world > 1 && pattern == CARAMEL_SHUFFLE)  // + the copy-engine engine's staging slots
-      *bucket_bytes = ce_stage_off(numel, pattern, world) + (uint64_t)(world - 1) * ce_slot_bytes(numel, world);
+      *bucket_bytes = ce_stage_off(numel, depth, pattern, world) + (uint64_t)(world - 1) * ce_slot_bytes(numel, world);
   }
   if (flag_bytes) {
     uint64_t fb = world == 1 ? 0 : (uint64_t)depth * g * nslots(pattern, world) * world * 4;
@@ -3176,12 +3153,6 @@ static size_t push_smem(int p) {
   }
 }
 
-// item size of the push kernels (identical on every rank, like the LL cutoff)
-static uint32_t push_range_bytes() {
-  static uint32_t v = 0;
-  if (!v) v = getenv("CARAMEL_PUSH_RANGE_KB") ? (uint32_t)atoi(getenv("CARAMEL_PUSH_RANGE_KB")) << 10 : PUSH_RANGE_BYTES;
-  return v < 4096 ? 4096 : v;
-}
 // CTAs of a push launch when the caller leaves it to the library
 static int push_default_ctas() {
   static int v = 0;
@@ -3207,7 +3178,7 @@ static int validate_bucket(const caramel_ctx* c, const caramel_bucket* b) {
   const int proto = shuffle_proto(*b, c->world);
   const uint64_t span2 = (proto == PROTO_OS || proto == PROTO_TS)
                              ? push_off(b->numel, CARAMEL_SHUFFLE, c->world) +
-                                   push_region_bytes(b->numel, CARAMEL_SHUFFLE, c->world)
+                                   push_region_bytes(b->numel, b->depth, CARAMEL_SHUFFLE, c->world)
                              : span;
   if (b->bucket_off + (span2 > span ? span2 : span) > c->arena_bytes)
     return set_err(CARAMEL_EINVAL, "bucket [%llu, +%llu B) exceeds the arena (size it with caramel_bucket_layout)",
@@ -3278,48 +3249,6 @@ static int coop_launch(const caramel_ctx* c, void (*fn)(Params), dim3 grid, cons
 
 extern "C" {
 
-// The push kernel over `count` buckets (host copy `host`; device copy at
-// `dev_list`, or 0 for a single bucket passed by value).  ctas <= 0: the
-// largest tile-range count of the list.
-static int push_launch(caramel_ctx* c, const caramel_bucket* host, int count, uint64_t dev_list, int ctas,
-                       uint32_t epoch, void* stream, int with_ll = 0) {
-  PushParams P;
-  memset(&P, 0, sizeof(P));
-  fill_env(c, P.env, epoch);
-  P.bs = reinterpret_cast<const caramel_bucket*>(dev_list);
-  P.nb = count;
-  P.range_bytes = push_range_bytes();
-  P.with_ll = with_ll;
-  P.one = host[0];
-  // default grid: enough CTAs for the items, at most CARAMEL_PUSH_CTAS (a
-  // small footprint leaves the SMs to the backward pass); LL buckets need
-  // their own CTA slots
-  uint64_t items = 0;
-  int G = 1;
-  for (int i = 0; i < count; ++i) {
-    const int pr = shuffle_proto(host[i], c->world);
-    if (pr == PROTO_LL) G = host[i].ctas > G ? host[i].ctas : G;
-    else items += (uint64_t)host[i].depth * push_ranges(host[i], c->world, P.range_bytes);
-  }
-  const uint64_t want = items < (uint64_t)push_default_ctas() ? items : (uint64_t)push_default_ctas();
-  if ((int)want > G) G = (int)want;
-  if (ctas > 0) G = ctas;
-  if (c->nlocal > 1 && G * c->nlocal > c->sms) G = c->sms / c->nlocal;  // emulated ranks: all co-resident
-  const int p = c->world;
-  pfn_push fn = pick_push(p);
-  const size_t smem = push_smem(p);
-  static bool attr[MAXR + 1] = {false};
-  if (!attr[p]) {
-    CUDA_TRY(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr[p] = true;
-  }
-  dim3 grid(G, c->nlocal);
-  if (c->nlocal > 1 || with_ll) return coop_launch(c, fn, grid, P, stream, smem);
-  fn<<<grid, THREADS, smem, (cudaStream_t)stream>>>(P);
-  CUDA_TRY(cudaGetLastError());
-  return 0;
-}
-
 // CARAMEL_MANY_FUSED lists through the push kernel with this many CTAs (0: the
 // grid-barrier pull kernel k_shuffle_fused)
 static int fused_push() {
@@ -3333,6 +3262,59 @@ static int fused_push() {
 static int push_family(const caramel_bucket& b, int world) {
   const int pr = shuffle_proto(b, world);
   return pr == PROTO_OS || pr == PROTO_TS;
+}
+
+// The push kernel over `count` buckets (host copy `host`; device copy at
+// `dev_list`, or 0 for a single bucket passed by value).  ctas <= 0: the
+// largest tile-range count of the list.
+static int push_launch(caramel_ctx* c, const caramel_bucket* host, int count, uint64_t dev_list, int ctas,
+                       uint32_t epoch, void* stream, int with_ll = 0) {
+  PushParams P;
+  memset(&P, 0, sizeof(P));
+  fill_env(c, P.env, epoch);
+  P.bs = reinterpret_cast<const caramel_bucket*>(dev_list);
+  P.nb = count;
+  P.with_ll = with_ll;
+  P.one = host[0];
+  // default grid: enough CTAs for the items, at most CARAMEL_PUSH_CTAS (a
+  // small footprint leaves the SMs to the backward pass); LL buckets need
+  // their own CTA slots
+  uint64_t items = 0;
+  int G = 1;
+  for (int i = 0; i < count; ++i) {
+    const int pr = shuffle_proto(host[i], c->world);
+    if (pr == PROTO_LL) G = host[i].ctas > G ? host[i].ctas : G;
+    else items += (uint64_t)host[i].depth * push_ranges(host[i].numel, host[i].depth);
+  }
+  const uint64_t want = items < (uint64_t)push_default_ctas() ? items : (uint64_t)push_default_ctas();
+  if ((int)want > G) G = (int)want;
+  if (ctas > 0) G = ctas;
+  if (c->nlocal > 1 && G * c->nlocal > c->sms) G = c->sms / c->nlocal;  // emulated ranks: all co-resident
+  const int p = c->world;
+  pfn_push fn = pick_push(p);
+  const size_t smem = push_smem(p);
+  static bool attr[MAXR + 1] = {false};
+  if (!attr[p]) {
+    CUDA_TRY(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr[p] = true;
+  }
+  // PACK buckets: gather the members into each local rank's bucket first (K1)
+  for (int i = 0; i < count; ++i) {
+    const caramel_bucket& b = host[i];
+    if (!(b.flags & CARAMEL_F_PACK) || !b.numel || !push_family(b, c->world)) continue;
+    for (int lr = 0; lr < c->nlocal; ++lr) {
+      const caramel_segment* segs = reinterpret_cast<const caramel_segment*>(b.segs) + (uint64_t)lr * b.nseg;
+      float* bkt = reinterpret_cast<float*>(c->arena[c->rank + lr] + b.bucket_off);
+      k_pack<<<grid_for(b.numel, (const void*)k_pack), THREADS, 0, (cudaStream_t)stream>>>(segs, b.nseg, b.numel,
+                                                                                           bkt);
+    }
+    CUDA_TRY(cudaGetLastError());
+  }
+  dim3 grid(G, c->nlocal);
+  if (c->nlocal > 1 || with_ll) return coop_launch(c, fn, grid, P, stream, smem);
+  fn<<<grid, THREADS, smem, (cudaStream_t)stream>>>(P);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
 }
 
 static int launch(caramel_ctx* c, const caramel_bucket* b, uint32_t epoch, void* stream) {
@@ -3629,7 +3611,7 @@ static int ce_validate(caramel_ctx* c, const caramel_bucket* host, int32_t count
       return set_err(CARAMEL_EINVAL, "allreduce_ce: the SGD epilogue needs PARAM_ARENA");
     int rc = validate_bucket(c, &b);
     if (rc) return rc;
-    const uint64_t end = b.bucket_off + ce_stage_off(b.numel, CARAMEL_SHUFFLE, p) + (uint64_t)(p - 1) * ce_slot_bytes(b.numel, p);
+    const uint64_t end = b.bucket_off + ce_stage_off(b.numel, b.depth, CARAMEL_SHUFFLE, p) + (uint64_t)(p - 1) * ce_slot_bytes(b.numel, p);
     if (b.numel && end > c->arena_bytes)
       return set_err(CARAMEL_EINVAL, "allreduce_ce: bucket + staging slots exceed the arena (size it with caramel_bucket_layout)");
   }
@@ -3666,7 +3648,7 @@ static int ce_enqueue(caramel_ctx* c, const caramel_bucket* host, int32_t count,
     for (int i = 0; i < count; ++i) {
       const uint64_t n = host[i].numel, lo = shard_lo(n, p, q), hi = shard_lo(n, p, q + 1);
       if (hi <= lo) continue;
-      const uint64_t stg = host[i].bucket_off + ce_stage_off(n, CARAMEL_SHUFFLE, p) + k * ce_slot_bytes(n, p) + 4 * (lo & 3);
+      const uint64_t stg = host[i].bucket_off + ce_stage_off(n, host[i].depth, CARAMEL_SHUFFLE, p) + k * ce_slot_bytes(n, p) + 4 * (lo & 3);
       CUDA_TRY(cudaMemcpyAsync((void*)(c->arena[q] + stg), (const void*)(c->arena[me] + host[i].bucket_off + 4 * lo),
                                4 * (hi - lo), cudaMemcpyDeviceToDevice, c->ce_send));
     }
@@ -3688,7 +3670,7 @@ static int ce_enqueue(caramel_ctx* c, const caramel_bucket* host, int32_t count,
       if (hi <= lo) continue;
       CeItem& it = P.it[P.count++];
       it.src = host[i].bucket_off + 4 * lo;
-      it.stg = host[i].bucket_off + ce_stage_off(n, CARAMEL_SHUFFLE, p) + 4 * (lo & 3);
+      it.stg = host[i].bucket_off + ce_stage_off(n, host[i].depth, CARAMEL_SHUFFLE, p) + 4 * (lo & 3);
       it.slot = ce_slot_bytes(n, p);
       it.dst = (sgd ? host[i].param_off : host[i].bucket_off) + 4 * lo;
       it.n = hi - lo;

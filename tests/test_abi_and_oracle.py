@@ -79,10 +79,11 @@ def test_chunk_rule_agrees_with_reference_float_bytes():
 def test_bucket_layout_and_errors():
     N = _lib()
     ctas, bb, fb = N.bucket_layout(1 << 20, 2, N.SHUFFLE, 8)
-    # packed bucket + push region (256 B header, 2 x 7 inbox slots mirroring
+    # packed bucket + push region (256 B header, per-item flags: 2 chunks x 16
+    # ranges of 128 KB x {READY, DONE} x 8 sources, 2 x 7 inbox slots mirroring
     # the bucket) + 7 copy-engine staging slots of ceil(n/8)+3 elements
     slot = (4 * ((1 << 20) // 8 + 3) + 15) & ~15
-    push = 256 + 2 * 7 * (4 << 20)
+    push = 256 + 2 * 16 * 2 * 8 * 4 + 2 * 7 * (4 << 20)
     assert 1 <= ctas <= 64 and bb == (4 << 20) + push + 7 * slot and fb > 0
     # LL buckets (<= 64K elements) carry no push region
     ll = (4 * 1000 + 8 * 1000 * 9 + 255) // 256 * 256  # LL region: bucket + out + 8 in-slots of 8 B words
