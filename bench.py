@@ -638,6 +638,11 @@ def bucket_sweep(torch, dist, world, rank, dev, iters=20, network=None):
         c.bootstrap()
         comm._view_fp32(c.arena_ptrs(0)[0], big // 4).normal_()
         ce_ctx["ce"], ce_epoch["ce"] = c, 0
+    # the NVLS (multicast, in-switch reduction) two-shot: the non-fixed-order mode
+    nvls_ok = ctx.nvls_available()
+    if nvls_ok:
+        ctx.nvls_setup(big + (2 << 20))
+        comm._view_fp32(ctx.nvls_base, big // 4).normal_()
     for k, size in enumerate(SWEEP_SIZES):
         n = size // 4
         depth = adaptive_depth(size, thr)
@@ -717,6 +722,18 @@ def bucket_sweep(torch, dist, world, rank, dev, iters=20, network=None):
                 us_e, _ = timed(ce_call, graphed=False)
                 row[f"{key}_us"] = round(us_e, 2)
                 row[f"{key}_bus_gbs"] = round(bus / us_e, 1)
+        if nvls_ok:
+            bn = comm.make_bucket(n, 0, region + k * (1 << 20), depth=depth, pattern=N.SHUFFLE,
+                                  epilogue=N.EPI_SUM, flags=0, ctas=min(ctas, 32))
+
+            def nvls_call(st=None, bn=bn):
+                st = st or stream
+                N.check(N.lib().caramel_epoch_advance(ctx._ctx, ctypes.c_void_p(st.cuda_stream)))
+                ctx.allreduce_nvls(bn, 0, st.cuda_stream)
+
+            us_v, _ = timed(nvls_call)
+            row["nvls_us"] = round(us_v, 2)
+            row["nvls_bus_gbs"] = round(bus / us_v, 1)  # same 2(p-1)/p*S convention; NVLS moves S per direction
         rows.append(row)
     ctx.status()
     ctx.close()

@@ -249,6 +249,37 @@ int caramel_ce_submit(caramel_ctx* ctx, const caramel_bucket* host, int32_t coun
 /* Blocks until every submitted call has been issued to its streams. */
 int caramel_ce_flush(caramel_ctx* ctx);
 
+/* ---- NVLS (NVLink SHARP) multicast: the non-fixed-order mode ------------- */
+/* The two-shot with the reduction done inside the NVSwitch: the owner of each
+ * shard issues multimem.ld_reduce on a multicast address (the switch sums every
+ * GPU's copy, in its own order) and multimem.st (the switch writes the result
+ * into every GPU's copy) -- S bytes per GPU and direction instead of
+ * 2(p-1)/p x S (collective.py:12-13,98-100 is the pattern; its byte count is
+ * the one thing this mode changes).  Results agree with the rank-order sum to
+ * 1e-6 x sum_r |g_r| per element, not bit for bit: the bit-exact contract stays
+ * with caramel_allreduce.  Setup, in this order on every rank (the caller puts
+ * a barrier between the steps): */
+/* 1 if this context can use multicast objects (one rank per process, world > 1). */
+int caramel_mc_available(caramel_ctx* ctx);
+/* Allocate `bytes` (rounded up to the multicast granularity) of multicast-
+ * capable memory on this GPU.  Rank 0 also creates the multicast object and
+ * listens on an abstract Unix socket named after `token` (a string identical on
+ * every rank and unique per job). */
+int caramel_mc_create(caramel_ctx* ctx, uint64_t bytes, const char* token);
+/* Concurrently on every rank: rank 0 passes the multicast handle's file
+ * descriptor to every peer (SCM_RIGHTS); every rank adds its GPU. */
+int caramel_mc_exchange(caramel_ctx* ctx);
+/* After every rank's exchange: bind this GPU's memory to the multicast object,
+ * map both views; writes this rank's unicast address of the (zeroed) arena. */
+int caramel_mc_bind(caramel_ctx* ctx, uint64_t* unicast_base);
+/* One bucket through the switch: `bucket_off` is relative to the multicast
+ * arena (the gradients are written there through the unicast view), results
+ * land in place (SUM / SCALE) or, with CARAMEL_EPI_SGD, in the parameter
+ * arena (every rank updates its own copy from the identical broadcast
+ * sum x scale).  `flag_off`/`ctas`/`depth` as for caramel_allreduce (the flag
+ * block lives in the IPC bucket arena; size it with caramel_bucket_layout). */
+int caramel_allreduce_nvls(caramel_ctx* ctx, const caramel_bucket* bucket, uint32_t epoch, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

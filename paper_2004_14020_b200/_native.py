@@ -107,6 +107,12 @@ SIGNATURES = {
                                          ctypes.c_uint32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
                                          ctypes.c_void_p]),
     "caramel_ce_flush": (ctypes.c_int, [ctypes.c_void_p]),
+    "caramel_mc_available": (ctypes.c_int, [ctypes.c_void_p]),
+    "caramel_mc_create": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_char_p]),
+    "caramel_mc_exchange": (ctypes.c_int, [ctypes.c_void_p]),
+    "caramel_mc_bind": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64)]),
+    "caramel_allreduce_nvls": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Bucket), ctypes.c_uint32,
+                                              ctypes.c_void_p]),
 }
 
 

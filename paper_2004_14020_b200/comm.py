@@ -142,6 +142,38 @@ class Context:
         fn = self._lib.caramel_allreduce_update if bucket.epilogue == N.EPI_SGD else self._lib.caramel_allreduce
         N.check(fn(self._ctx, ctypes.byref(bucket), epoch, ctypes.c_void_p(stream)))
 
+    # -- NVLS multicast arena (the non-fixed-order mode) ----------------------
+    def nvls_available(self) -> bool:
+        return bool(self._lib.caramel_mc_available(self._ctx))
+
+    def nvls_setup(self, nbytes: int, group=None) -> int:
+        """Create, exchange and bind a multicast arena of `nbytes` on every rank
+        (collective: every rank calls).  Returns this rank's unicast base
+        address; `nvls_view` wraps it."""
+        import uuid
+
+        import torch.distributed as dist
+
+        tok: list = [uuid.uuid4().hex[:16] if self.rank == 0 else None]
+        dist.broadcast_object_list(tok, src=0, group=group)
+        N.check(self._lib.caramel_mc_create(self._ctx, nbytes, tok[0].encode()))
+        dist.barrier(group=group)          # rank 0 listens
+        N.check(self._lib.caramel_mc_exchange(self._ctx))
+        dist.barrier(group=group)          # every GPU added to the multicast object
+        base = ctypes.c_uint64()
+        N.check(self._lib.caramel_mc_bind(self._ctx, ctypes.byref(base)))
+        dist.barrier(group=group)          # every GPU bound
+        self.nvls_base, self.nvls_bytes = base.value, nbytes
+        return base.value
+
+    def nvls_view(self, byte_off: int, numel: int) -> torch.Tensor:
+        if byte_off % 4 or byte_off + 4 * numel > self.nvls_bytes:
+            raise ValueError("view outside the multicast arena")
+        return _view_fp32(self.nvls_base + byte_off, numel)
+
+    def allreduce_nvls(self, bucket: N.Bucket, epoch: int, stream: int) -> None:
+        N.check(self._lib.caramel_allreduce_nvls(self._ctx, ctypes.byref(bucket), epoch, ctypes.c_void_p(stream)))
+
     def close(self) -> None:
         if self._ctx:
             self._lib.caramel_finalize(self._ctx)

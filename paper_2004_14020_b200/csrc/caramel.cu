@@ -26,6 +26,10 @@
 #include <stdlib.h>
 #include <string.h>
 #include <stdarg.h>
+#include <sys/socket.h>
+#include <sys/un.h>
+#include <unistd.h>
+#include <errno.h>
 
 #include <condition_variable>
 #include <deque>
@@ -700,8 +704,20 @@ __host__ __device__ __forceinline__ uint64_t kernel_region_bytes(uint64_t numel,
   return use_ll(pattern, world, numel) ? (ll_region_bytes(numel, world) + 15) & ~15ull
                                        : 4 * ((world > 1 && pattern != CARAMEL_SHUFFLE) ? 2 * e : e);
 }
+// The push engine is opt-in (CARAMEL_PUSH=1, identical on every rank): on the
+// B200 NVSwitch boxes measured so far the register-pull kernels move the same
+// bytes faster.
+__device__ int d_push_enabled = 0;
+static int h_push_enabled = 0;
+__host__ __device__ __forceinline__ bool push_enabled() {
+#ifdef __CUDA_ARCH__
+  return d_push_enabled != 0;
+#else
+  return h_push_enabled != 0;
+#endif
+}
 __host__ __device__ __forceinline__ bool has_push_region(uint64_t numel, int pattern, int world) {
-  return pattern == CARAMEL_SHUFFLE && world > 1 && numel > 0 && !use_ll(pattern, world, numel);
+  return push_enabled() && pattern == CARAMEL_SHUFFLE && world > 1 && numel > 0 && !use_ll(pattern, world, numel);
 }
 __host__ __device__ __forceinline__ uint64_t push_off(uint64_t numel, int pattern, int world) {
   return (kernel_region_bytes(numel, pattern, world) + 255) & ~255ull;
@@ -752,7 +768,8 @@ __host__ __device__ __forceinline__ int shuffle_proto(const caramel_bucket& b, i
 #endif
   if (b.pattern != CARAMEL_SHUFFLE || world < 2) return PROTO_PULL;
   if (use_ll(b.pattern, world, b.numel)) return PROTO_LL;
-  if ((b.flags & CARAMEL_F_UNPACK) || (b.epilogue == CARAMEL_EPI_SGD && !(b.flags & CARAMEL_F_PARAM_ARENA)))
+  if (!push_enabled() || (b.flags & CARAMEL_F_UNPACK) ||
+      (b.epilogue == CARAMEL_EPI_SGD && !(b.flags & CARAMEL_F_PARAM_ARENA)))
     return PROTO_PULL;
   return 4 * b.numel <= os_max ? PROTO_OS : PROTO_TS;
 }
@@ -2101,6 +2118,186 @@ __global__ void __launch_bounds__(TMA_THREADS, 2) k_local_flat_tma(const __grid_
   if (threadIdx.x == 0) bulk_wait_all();
 }
 
+// ---------------------------------------------------------------------------
+// K1 / K4 through the TMA unit (caramel_pack / caramel_unpack): the bucket is
+// cut into 32 KB tiles; a persistent CTA per SM streams its tiles through a
+// 4-stage shared-memory ring.  Pack: every member piece of a tile whose source
+// and tile position share their 16-byte phase is one cp.async.bulk load into
+// the tile (completion on the stage's mbarrier); the rare misaligned piece is
+// copied into the tile by all threads; the whole tile leaves with ONE bulk
+// store.  Unpack is the mirror image (one bulk load per tile, one bulk store
+// per aligned piece).  Bytes in flight sit in shared memory: no register
+// round trip per member (the warp-item engine above stalled on exactly that:
+// 53% DRAM throughput, 26.7 of 53.7 cycles per instruction on long scoreboard).
+// ---------------------------------------------------------------------------
+#define KT_THREADS 256
+#define KT_TILE 8192                 // floats per tile (32 KB)
+#define KT_STAGES 4
+#define KT_MAXODD 32                 // misaligned pieces remembered per tile (more: the tile goes plain)
+#define KT_MAXSEG 1024               // member tables up to this size are cached in shared memory
+
+struct KtOdd { uint64_t src, dst; uint32_t n; };  // a misaligned piece: element addresses, count
+
+struct KtSmem {
+  float tile[KT_STAGES][KT_TILE];
+  uint64_t full[KT_STAGES];
+  KtOdd odd[KT_STAGES][KT_MAXODD];
+  int nodd[KT_STAGES];               // -1: copy the whole tile plainly
+  caramel_segment segs[KT_MAXSEG];   // the member table (the issuing thread searches it per tile)
+};
+
+// Walks the member pieces of bucket range [t0, t1): f(seg, x0, x1) in bucket coordinates.
+// (plain generic loads: the table may sit in shared memory)
+template <class F>
+__device__ __forceinline__ void kt_pieces(const caramel_segment* segs, int nseg, uint64_t t0, uint64_t t1, F f) {
+  int a = 0, b = nseg - 1;
+  while (a < b) {
+    const int m = (a + b + 1) >> 1;
+    if (segs[m].offset <= t0) a = m; else b = m - 1;
+  }
+  for (int i = a; i < nseg; ++i) {
+    const Seg sg{segs[i].grad, segs[i].param, segs[i].offset, segs[i].numel};
+    if (sg.offset >= t1) break;
+    uint64_t x0, x1;
+    if (clip_seg(sg, t0, t1, x0, x1)) f(sg, x0, x1);
+  }
+}
+
+// UNPACK = false: members -> bucket.  UNPACK = true: bucket -> members
+// (to_param selects .param instead of .grad).
+template <bool UNPACK>
+__global__ void __launch_bounds__(KT_THREADS, 1) k_pack_tma(const caramel_segment* segs, int nseg, uint64_t numel,
+                                                            float* bucket, int to_param) {
+  extern __shared__ __align__(128) unsigned char dyn_smem[];
+  KtSmem& S = *reinterpret_cast<KtSmem*>(dyn_smem);
+  if (nseg <= KT_MAXSEG) {  // one coalesced copy instead of a dependent global load per search step
+    for (int i = threadIdx.x; i < 4 * nseg; i += blockDim.x)
+      reinterpret_cast<unsigned long long*>(S.segs)[i] = __ldg(reinterpret_cast<const unsigned long long*>(segs) + i);
+    __syncthreads();
+    segs = S.segs;
+  }
+  const uint64_t ntiles = (numel + KT_TILE - 1) / KT_TILE;
+  const uint64_t G = gridDim.x;
+  const uint64_t K = blockIdx.x < ntiles ? (ntiles - blockIdx.x + G - 1) / G : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < KT_STAGES; ++s) mbar_init(&S.full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto member = [&](const Seg& sg) -> float* { return reinterpret_cast<float*>(UNPACK && to_param ? sg.param : sg.grad); };
+  // thread 0: start tile k's loads into its stage, remember its misaligned pieces
+  auto issue = [&](uint64_t k) {
+    const uint64_t t = blockIdx.x + k * G, t0 = t * KT_TILE;
+    const uint64_t t1 = t0 + KT_TILE < numel ? t0 + KT_TILE : numel;
+    const int s = (int)(k % KT_STAGES);
+    float* tile = S.tile[s];
+    if (UNPACK) {
+      const uint32_t bytes = (uint32_t)(4 * (t1 - t0)) & ~15u;  // the < 4-element tail goes plain (bucket is 16 B aligned)
+      mbar_expect_tx(&S.full[s], bytes);
+      if (bytes) bulk_load(tile, bucket + t0, bytes, &S.full[s]);
+      S.nodd[s] = 0;
+      return;
+    }
+    uint32_t tx = 0;
+    int nodd = 0;
+    // count the bulk bytes first: expect_tx must precede the loads' completion
+    kt_pieces(segs, nseg, t0, t1, [&](const Seg& sg, uint64_t x0, uint64_t x1) {
+      const uintptr_t src = (uintptr_t)(member(sg) + (x0 - sg.offset));
+      if (((src ^ (uintptr_t)(4 * (x0 - t0))) & 15) == 0) {
+        const uint64_t a = (x0 + 3) & ~3ull, b = x1 & ~3ull;
+        if (b > a) tx += (uint32_t)(4 * (b - a));
+      }
+    });
+    mbar_expect_tx(&S.full[s], tx);
+    kt_pieces(segs, nseg, t0, t1, [&](const Seg& sg, uint64_t x0, uint64_t x1) {
+      const float* src = member(sg) + (x0 - sg.offset);
+      const bool co = (((uintptr_t)src ^ (uintptr_t)(4 * (x0 - t0))) & 15) == 0;
+      uint64_t a = x0, b = x0;
+      if (co) {
+        a = (x0 + 3) & ~3ull;
+        b = x1 & ~3ull;
+        if (b < a) b = a;
+        if (a > x1) a = b = x1;
+        if (b > a) bulk_load(tile + (a - t0), src + (a - x0), (uint32_t)(4 * (b - a)), &S.full[s]);
+      }
+      // ragged ends / misaligned piece: remembered for the plain copy
+      const uint64_t parts[2][2] = {{x0, co ? a : x1}, {co ? b : x1, x1}};
+      for (int h = 0; h < 2; ++h) {
+        const uint64_t y0 = parts[h][0], y1 = parts[h][1];
+        if (y1 <= y0) continue;
+        if (nodd < KT_MAXODD)
+          S.odd[s][nodd] = KtOdd{(uint64_t)(uintptr_t)(member(sg) + (y0 - sg.offset)), y0 - t0, (uint32_t)(y1 - y0)};
+        ++nodd;
+      }
+    });
+    S.nodd[s] = nodd;
+  };
+  auto bytes_of_tile = [&](uint64_t k) {
+    const uint64_t t0 = (blockIdx.x + k * G) * KT_TILE;
+    return (uint32_t)(4 * ((t0 + KT_TILE < numel ? t0 + KT_TILE : numel) - t0));
+  };
+  if (threadIdx.x == 0)
+    for (uint64_t k = 0; k + 2 < KT_STAGES && k < K; ++k) issue(k);
+  __syncthreads();  // the misaligned-piece lists written by issue() are read by every thread
+  for (uint64_t k = 0; k < K; ++k) {
+    const int s = (int)(k % KT_STAGES);
+    if (threadIdx.x == 0 && k + KT_STAGES - 2 < K) {
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // the stage refilled held tile k-2
+      issue(k + KT_STAGES - 2);
+    }
+    mbar_wait(&S.full[s], (uint32_t)((k / KT_STAGES) & 1));
+    const uint64_t t0 = (blockIdx.x + k * G) * KT_TILE;
+    const uint32_t nbytes = bytes_of_tile(k), nel = nbytes / 4;
+    float* tile = S.tile[s];
+    if (!UNPACK) {
+      const int nodd = S.nodd[s];
+      if (nodd > KT_MAXODD) {  // too many misaligned pieces: copy the whole tile plainly
+        kt_pieces(segs, nseg, t0, t0 + nel, [&](const Seg& sg, uint64_t x0, uint64_t x1) {
+          const float* src = member(sg) + (x0 - sg.offset);
+          for (uint64_t e = threadIdx.x; e < x1 - x0; e += blockDim.x) tile[x0 - t0 + e] = ld1(src + e);
+        });
+      } else {
+        for (int o = 0; o < nodd; ++o) {
+          const KtOdd od = S.odd[s][o];
+          for (uint32_t e = threadIdx.x; e < od.n; e += blockDim.x)
+            tile[od.dst + e] = ld1(reinterpret_cast<const float*>(od.src) + e);
+        }
+      }
+      fence_proxy_async();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const uint32_t vb = nbytes & ~15u;
+        if (vb) bulk_store(bucket + t0, tile, vb);
+        bulk_commit();
+      }
+      for (uint32_t e = (nbytes & ~15u) / 4 + threadIdx.x; e < nel; e += blockDim.x) st1(bucket + t0 + e, tile[e]);
+    } else {
+      for (uint32_t e = (nbytes & ~15u) / 4 + threadIdx.x; e < nel; e += blockDim.x) tile[e] = ld1(bucket + t0 + e);
+      __syncthreads();
+      // aligned pieces: bulk stores by thread 0; the rest: plain stores by all threads
+      if (threadIdx.x == 0) {
+        kt_pieces(segs, nseg, t0, t0 + nel, [&](const Seg& sg, uint64_t x0, uint64_t x1) {
+          float* dst = member(sg) + (x0 - sg.offset);
+          if ((((uintptr_t)dst ^ (uintptr_t)(4 * (x0 - t0))) & 15) != 0) return;
+          uint64_t a = (x0 + 3) & ~3ull, b = x1 & ~3ull;
+          if (b > a) bulk_store(dst + (a - x0), tile + (a - t0), (uint32_t)(4 * (b - a)));
+        });
+        bulk_commit();
+      }
+      kt_pieces(segs, nseg, t0, t0 + nel, [&](const Seg& sg, uint64_t x0, uint64_t x1) {
+        float* dst = member(sg) + (x0 - sg.offset);
+        const bool co = (((uintptr_t)dst ^ (uintptr_t)(4 * (x0 - t0))) & 15) == 0;
+        uint64_t a = (x0 + 3) & ~3ull, b = x1 & ~3ull;
+        if (!co || b <= a) a = b = x1;  // everything plain
+        for (uint64_t e = x0 + threadIdx.x; e < a; e += blockDim.x) st1(dst + (e - x0), tile[e - t0]);
+        for (uint64_t e = b + threadIdx.x; e < x1; e += blockDim.x) st1(dst + (e - x0), tile[e - t0]);
+      });
+    }
+    __syncthreads();  // the stage may be refilled once its store has read it (thread 0 checks)
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
+}
+
 // Many buckets in one launch (launch order).  world == 1: the concatenated
 // element space is tiled evenly over the grid.  Shuffle: phase-major -- every
 // bucket's pack + ready flags first, then every bucket's reduce/all-gather,
@@ -2673,6 +2870,111 @@ __global__ void __launch_bounds__(PUSH_THREADS, 1) k_push(const __grid_constant_
 }
 
 // ---------------------------------------------------------------------------
+// NVLS (NVLink SHARP) two-shot: the non-fixed-order mode (caramel_allreduce_nvls).
+// The buckets live in a multicast-bound arena (every rank's physical copy is
+// reachable through one multicast address).  Rank r owns shard r of every
+// chunk: one multimem.ld_reduce per 16 bytes makes the NVSwitch fetch that
+// vector from every GPU and return the fp32 SUM (in the switch's order, not
+// the rank order: results agree to the 1e-6 relative bound of SURVEY §8c, not
+// bit for bit), the epilogue is applied, and one multimem.st writes the result
+// into every GPU's copy.  Per GPU and direction that is S bytes instead of the
+// 2(p-1)/p x S of a two-shot over peer loads/stores.  READY/DONE are the
+// bucket's ordinary per-(chunk, tile) flags in the IPC arena.  The SGD
+// epilogue: the owner broadcasts (sum x scale), every rank then updates its
+// own parameters from that identical vector (replicas stay bit-identical).
+// ---------------------------------------------------------------------------
+struct NvlsParams {
+  Env env;
+  caramel_bucket b;
+  uint64_t mc;   // multicast address of the NVLS arena
+  uint64_t uc;   // this rank's unicast view of it
+};
+
+__device__ __forceinline__ float4 mc_ld_reduce4(const float* a) {
+  float4 r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(a)
+               : "memory");
+  return r;
+}
+__device__ __forceinline__ float mc_ld_reduce1(const float* a) {
+  float r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(r) : "l"(a) : "memory");
+  return r;
+}
+__device__ __forceinline__ void mc_st4(float* a, float4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(a), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void mc_st1(float* a, float v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_alias() { asm volatile("fence.proxy.alias;" ::: "memory"); }
+
+__global__ void __launch_bounds__(THREADS, 1) k_nvls(const __grid_constant__ NvlsParams P) {
+  const Env E = P.env;
+  if (cta_poisoned(E)) return;
+  const caramel_bucket B = P.b;
+  const int me = E.rank_base, p = E.world, j = blockIdx.x, G = B.ctas;
+  const uint32_t epoch = launch_epoch(E);
+  Ctx X;
+  X.E = &E;
+  X.flag_off = B.flag_off;
+  X.me = me;
+  X.world = p;
+  X.j = j;
+  X.G = G;
+  X.ns = 2;
+  X.epoch = epoch;
+  float* mcb = reinterpret_cast<float*>(P.mc + B.bucket_off);
+  float* ucb = reinterpret_cast<float*>(P.uc + B.bucket_off);
+  const bool sgd = B.epilogue == CARAMEL_EPI_SGD;
+  const int epi = sgd ? CARAMEL_EPI_SCALE : B.epilogue;  // SGD: broadcast sum*scale, update locally below
+  // my contribution (written before this launch, through the unicast view) is in place
+  fence_proxy_alias();
+  for (int c = 0; c < B.depth; ++c) X.publish_all(c, SLOT_READY);
+  for (int c = 0; c < B.depth; ++c) {
+    X.wait_all(c, SLOT_READY, epoch);
+    uint64_t lo, hi, a, b;
+    shard_bounds(B.numel, B.depth, p, c, me, lo, hi);
+    tile_of(lo, hi, G, j, lo, hi);
+    split4(lo, hi, a, b);
+    for (uint64_t x = lo + threadIdx.x; x < a; x += blockDim.x) mc_st1(mcb + x, epi1(epi, mc_ld_reduce1(mcb + x), 0.f, B.scale, B.lr));
+    for (uint64_t x = (b > a ? b : a) + threadIdx.x; x < hi; x += blockDim.x)
+      mc_st1(mcb + x, epi1(epi, mc_ld_reduce1(mcb + x), 0.f, B.scale, B.lr));
+    constexpr int U = 4;  // switch round trips in flight per thread
+    const uint64_t T = 4ull * blockDim.x;
+    uint64_t v = a + 4ull * threadIdx.x;
+    for (; v + (U - 1) * T < b; v += U * T) {
+      float4 s[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) s[u] = mc_ld_reduce4(mcb + v + u * T);
+#pragma unroll
+      for (int u = 0; u < U; ++u) mc_st4(mcb + v + u * T, epi4(epi, s[u], s[u], B.scale, B.lr));
+    }
+    for (; v < b; v += T) mc_st4(mcb + v, epi4(epi, mc_ld_reduce4(mcb + v), make_float4(0.f, 0.f, 0.f, 0.f), B.scale, B.lr));
+    __syncthreads();
+    if (threadIdx.x < 32) fence_acq_rel_sys();  // my multimem stores, then DONE
+    X.publish_all(c, SLOT_DONE);
+  }
+  for (int c = 0; c < B.depth; ++c) X.wait_all(c, SLOT_DONE, epoch);
+  fence_proxy_alias();  // the results arrived through the multicast address; read them through the unicast one
+  if (!sgd) return;
+  float* th = reinterpret_cast<float*>(E.parena[me] + B.param_off);
+  for (int c = 0; c < B.depth; ++c)
+    for (int s = 0; s < p; ++s) {
+      uint64_t lo, hi;
+      shard_bounds(B.numel, B.depth, p, c, s, lo, hi);
+      tile_of(lo, hi, G, j, lo, hi);
+      // theta <- theta - lr * g, g = the broadcast (sum * scale): epi1(SGD) with scale 1
+      for (uint64_t x = lo + threadIdx.x; x < hi; x += blockDim.x)
+        st1(th + x, __fsub_rn(ld1(th + x), __fmul_rn(B.lr, ld1(ucb + x))));
+    }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 
@@ -2781,6 +3083,14 @@ struct caramel_ctx {
   cudaEvent_t ce_pool[CE_POOL];
   int ce_rc;
   char ce_err[512];
+  // NVLS multicast arena (caramel_mc_*)
+  int mc_state;                 // 0 none, 1 created, 2 exchanged, 3 bound
+  uint64_t mc_bytes, mc_gran;
+  unsigned long long mc_handle;  // CUmemGenericAllocationHandle of the multicast object
+  unsigned long long mc_mem;     // this rank's physical allocation
+  uint64_t mc_va, uc_va;         // multicast and unicast mappings
+  int mc_listen, mc_fd;          // rank 0: listening socket; every rank: the multicast handle's fd
+  char mc_name[108];
 };
 
 struct Blob {
@@ -2797,8 +3107,10 @@ static void load_ll_max() {
   done = true;
   if (const char* e = getenv("CARAMEL_LL_MAX")) h_ll_max = strtoull(e, 0, 10);
   if (const char* e = getenv("CARAMEL_OS_MAX")) h_os_max = strtoull(e, 0, 10);
+  if (const char* e = getenv("CARAMEL_PUSH")) h_push_enabled = atoi(e) != 0;
   cudaMemcpyToSymbol(d_ll_max, &h_ll_max, sizeof(h_ll_max));
   cudaMemcpyToSymbol(d_os_max, &h_os_max, sizeof(h_os_max));
+  cudaMemcpyToSymbol(d_push_enabled, &h_push_enabled, sizeof(h_push_enabled));
 }
 
 int caramel_abi_version(void) { return CARAMEL_ABI_VERSION; }
@@ -2850,6 +3162,7 @@ int caramel_bucket_layout(uint64_t numel, int depth, int pattern, int world, int
                           uint64_t* bucket_bytes, uint64_t* flag_bytes) {
   if (getenv("CARAMEL_LL_MAX")) h_ll_max = strtoull(getenv("CARAMEL_LL_MAX"), 0, 10);
   if (getenv("CARAMEL_OS_MAX")) h_os_max = strtoull(getenv("CARAMEL_OS_MAX"), 0, 10);
+  if (getenv("CARAMEL_PUSH")) h_push_enabled = atoi(getenv("CARAMEL_PUSH")) != 0;
   int rc = validate_workers(pattern, world);
   if (rc) return rc;
   if (depth < 1 || depth > CARAMEL_MAX_DEPTH)
@@ -3012,6 +3325,8 @@ int caramel_set_timeout_ms(caramel_ctx* c, uint64_t ms) {
   return 0;
 }
 
+static void mc_release(caramel_ctx* c);
+
 int caramel_finalize(caramel_ctx* c) {
   if (!c) return 0;
   if (c->ce_worker_started) {
@@ -3024,6 +3339,7 @@ int caramel_finalize(caramel_ctx* c) {
     for (int i = 0; i < CE_POOL; ++i) cudaEventDestroy(c->ce_pool[i]);
   }
   cudaDeviceSynchronize();  // nothing in flight touches the arenas below
+  mc_release(c);
   for (int q = 0; q < MAXR; ++q) {
     if (c->opened[q]) {
       cudaIpcCloseMemHandle((void*)c->arena[q]);
@@ -3063,10 +3379,33 @@ static int grid_for(uint64_t numel, const void* fn) {
   return (int)g;
 }
 
+static int pack_tma(const caramel_segment* segs, int32_t nseg, uint64_t numel, float* bucket, bool unpack,
+                    int to_param, void* stream) {
+  static int sms = 0;
+  static bool attr[2] = {false, false};
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms < 1) sms = 148;
+  }
+  auto fn = unpack ? k_pack_tma<true> : k_pack_tma<false>;
+  if (!attr[unpack]) {
+    CUDA_TRY(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(KtSmem)));
+    attr[unpack] = true;
+  }
+  const uint64_t tiles = (numel + KT_TILE - 1) / KT_TILE;
+  const int grid = (int)(tiles < (uint64_t)sms ? tiles : (uint64_t)sms);
+  fn<<<grid, KT_THREADS, sizeof(KtSmem), (cudaStream_t)stream>>>(segs, nseg, numel, bucket, to_param);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 int caramel_pack(const caramel_segment* segs, int32_t nseg, uint64_t numel, float* bucket, void* stream) {
   if (!segs || nseg < 1 || !bucket) return set_err(CARAMEL_EINVAL, "pack: null table or bucket");
   if (((uintptr_t)bucket) & 15) return set_err(CARAMEL_EINVAL, "pack: bucket must be 16-byte aligned");
   if (numel == 0) return 0;
+  if (!getenv("CARAMEL_NO_TMA")) return pack_tma(segs, nseg, numel, bucket, false, 0, stream);
   k_pack<<<grid_for(numel, (const void*)k_pack), THREADS, 0, (cudaStream_t)stream>>>(segs, nseg, numel, bucket);
   CUDA_TRY(cudaGetLastError());
   return 0;
@@ -3077,6 +3416,8 @@ int caramel_unpack(const caramel_segment* segs, int32_t nseg, uint64_t numel, co
   if (!segs || nseg < 1 || !bucket) return set_err(CARAMEL_EINVAL, "unpack: null table or bucket");
   if (((uintptr_t)bucket) & 15) return set_err(CARAMEL_EINVAL, "unpack: bucket must be 16-byte aligned");
   if (numel == 0) return 0;
+  if (!getenv("CARAMEL_NO_TMA"))
+    return pack_tma(segs, nseg, numel, const_cast<float*>(bucket), true, to_param ? 1 : 0, stream);
   k_unpack<<<grid_for(numel, (const void*)k_unpack), THREADS, 0, (cudaStream_t)stream>>>(segs, nseg, numel, bucket, to_param ? 1 : 0);
   CUDA_TRY(cudaGetLastError());
   return 0;
@@ -3798,6 +4139,287 @@ int caramel_ce_flush(caramel_ctx* c) {
     return set_err(rc, "%s", c->ce_err);
   }
   return 0;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// NVLS multicast arena: driver entry points, handle exchange, bind, launch.
+// ---------------------------------------------------------------------------
+struct McApi {
+  CUresult (*DeviceGet)(CUdevice*, int);
+  CUresult (*DeviceGetAttribute)(int*, CUdevice_attribute, CUdevice);
+  CUresult (*MulticastGetGranularity)(size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags);
+  CUresult (*MulticastCreate)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*);
+  CUresult (*MulticastAddDevice)(CUmemGenericAllocationHandle, CUdevice);
+  CUresult (*MulticastBindMem)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t,
+                               unsigned long long);
+  CUresult (*MulticastUnbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t);
+  CUresult (*MemCreate)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long);
+  CUresult (*MemRelease)(CUmemGenericAllocationHandle);
+  CUresult (*MemExportToShareableHandle)(void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType,
+                                         unsigned long long);
+  CUresult (*MemImportFromShareableHandle)(CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType);
+  CUresult (*MemAddressReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
+  CUresult (*MemAddressFree)(CUdeviceptr, size_t);
+  CUresult (*MemMap)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
+  CUresult (*MemUnmap)(CUdeviceptr, size_t);
+  CUresult (*MemSetAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+  CUresult (*MemGetAllocationGranularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags);
+};
+static McApi g_mc;
+
+static bool mc_load() {
+  static int state = 0;
+  if (state) return state > 0;
+  state = -1;
+  struct { const char* name; void** slot; } fns[] = {
+      {"cuDeviceGet", (void**)&g_mc.DeviceGet},
+      {"cuDeviceGetAttribute", (void**)&g_mc.DeviceGetAttribute},
+      {"cuMulticastGetGranularity", (void**)&g_mc.MulticastGetGranularity},
+      {"cuMulticastCreate", (void**)&g_mc.MulticastCreate},
+      {"cuMulticastAddDevice", (void**)&g_mc.MulticastAddDevice},
+      {"cuMulticastBindMem", (void**)&g_mc.MulticastBindMem},
+      {"cuMulticastUnbind", (void**)&g_mc.MulticastUnbind},
+      {"cuMemCreate", (void**)&g_mc.MemCreate},
+      {"cuMemRelease", (void**)&g_mc.MemRelease},
+      {"cuMemExportToShareableHandle", (void**)&g_mc.MemExportToShareableHandle},
+      {"cuMemImportFromShareableHandle", (void**)&g_mc.MemImportFromShareableHandle},
+      {"cuMemAddressReserve", (void**)&g_mc.MemAddressReserve},
+      {"cuMemAddressFree", (void**)&g_mc.MemAddressFree},
+      {"cuMemMap", (void**)&g_mc.MemMap},
+      {"cuMemUnmap", (void**)&g_mc.MemUnmap},
+      {"cuMemSetAccess", (void**)&g_mc.MemSetAccess},
+      {"cuMemGetAllocationGranularity", (void**)&g_mc.MemGetAllocationGranularity},
+  };
+  for (auto& f : fns) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(f.name, f.slot, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !*f.slot)
+      return false;
+  }
+  state = 1;
+  return true;
+}
+
+#define MC_TRY(expr)                                                                              \
+  do {                                                                                            \
+    CUresult _r = (expr);                                                                         \
+    if (_r != CUDA_SUCCESS) return set_err(CARAMEL_ECUDA, "%s failed: CUresult %d", #expr, (int)_r); \
+  } while (0)
+
+static int mc_socket_name(const char* token, int rank, sockaddr_un* a, socklen_t* len) {
+  memset(a, 0, sizeof(*a));
+  a->sun_family = AF_UNIX;
+  // abstract namespace: no file in the filesystem, gone with the process
+  const int n = snprintf(a->sun_path + 1, sizeof(a->sun_path) - 1, "caramel-mc-%s-%d", token, rank);
+  if (n <= 0 || n >= (int)sizeof(a->sun_path) - 1) return -1;
+  *len = (socklen_t)(offsetof(sockaddr_un, sun_path) + 1 + n);
+  return 0;
+}
+
+static int mc_send_fd(int sock, int fd) {
+  char byte = 'm';
+  iovec io{&byte, 1};
+  char ctl[CMSG_SPACE(sizeof(int))];
+  memset(ctl, 0, sizeof(ctl));
+  msghdr msg;
+  memset(&msg, 0, sizeof(msg));
+  msg.msg_iov = &io;
+  msg.msg_iovlen = 1;
+  msg.msg_control = ctl;
+  msg.msg_controllen = sizeof(ctl);
+  cmsghdr* cm = CMSG_FIRSTHDR(&msg);
+  cm->cmsg_level = SOL_SOCKET;
+  cm->cmsg_type = SCM_RIGHTS;
+  cm->cmsg_len = CMSG_LEN(sizeof(int));
+  memcpy(CMSG_DATA(cm), &fd, sizeof(int));
+  return sendmsg(sock, &msg, 0) == 1 ? 0 : -1;
+}
+
+static int mc_recv_fd(int sock) {
+  char byte;
+  iovec io{&byte, 1};
+  char ctl[CMSG_SPACE(sizeof(int))];
+  msghdr msg;
+  memset(&msg, 0, sizeof(msg));
+  msg.msg_iov = &io;
+  msg.msg_iovlen = 1;
+  msg.msg_control = ctl;
+  msg.msg_controllen = sizeof(ctl);
+  if (recvmsg(sock, &msg, 0) != 1) return -1;
+  cmsghdr* cm = CMSG_FIRSTHDR(&msg);
+  if (!cm || cm->cmsg_type != SCM_RIGHTS) return -1;
+  int fd;
+  memcpy(&fd, CMSG_DATA(cm), sizeof(int));
+  return fd;
+}
+
+extern "C" {
+
+int caramel_mc_available(caramel_ctx* c) {
+  if (!c || c->nlocal != 1 || c->world < 2 || !mc_load()) return 0;
+  CUdevice d;
+  int v = 0;
+  if (g_mc.DeviceGet(&d, c->device) != CUDA_SUCCESS) return 0;
+  if (g_mc.DeviceGetAttribute(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, d) != CUDA_SUCCESS) return 0;
+  return v ? 1 : 0;
+}
+
+int caramel_mc_create(caramel_ctx* c, uint64_t bytes, const char* token) {
+  if (!c || !token || !bytes) return set_err(CARAMEL_EINVAL, "mc_create: null argument");
+  if (c->mc_state) return set_err(CARAMEL_ESTATE, "mc_create: the multicast arena exists already");
+  if (!caramel_mc_available(c)) return set_err(CARAMEL_ESTATE, "mc_create: no multicast (NVLS) support here");
+  CUdevice dev;
+  MC_TRY(g_mc.DeviceGet(&dev, c->device));
+  CUmulticastObjectProp mp;
+  memset(&mp, 0, sizeof(mp));
+  mp.numDevices = (unsigned)c->world;
+  mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  mp.size = bytes;
+  size_t mg = 0;
+  MC_TRY(g_mc.MulticastGetGranularity(&mg, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+  CUmemAllocationProp ap;
+  memset(&ap, 0, sizeof(ap));
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = dev;
+  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  size_t ag = 0;
+  MC_TRY(g_mc.MemGetAllocationGranularity(&ag, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+  const uint64_t gran = mg > ag ? mg : ag;
+  c->mc_gran = gran;
+  c->mc_bytes = (bytes + gran - 1) / gran * gran;
+  mp.size = c->mc_bytes;
+  CUmemGenericAllocationHandle mem;
+  MC_TRY(g_mc.MemCreate(&mem, c->mc_bytes, &ap, 0));
+  c->mc_mem = mem;
+  c->mc_listen = -1;
+  c->mc_fd = -1;
+  snprintf(c->mc_name, sizeof(c->mc_name), "%s", token);
+  if (c->rank == 0) {
+    CUmemGenericAllocationHandle mc;
+    MC_TRY(g_mc.MulticastCreate(&mc, &mp));
+    c->mc_handle = mc;
+    int fd = -1;
+    MC_TRY(g_mc.MemExportToShareableHandle(&fd, mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+    c->mc_fd = fd;
+    sockaddr_un a;
+    socklen_t len;
+    if (mc_socket_name(token, 0, &a, &len)) return set_err(CARAMEL_EINVAL, "mc_create: token too long");
+    const int s = socket(AF_UNIX, SOCK_STREAM, 0);
+    if (s < 0 || bind(s, (sockaddr*)&a, len) || listen(s, c->world))
+      return set_err(CARAMEL_ECUDA, "mc_create: listening socket: %s", strerror(errno));
+    c->mc_listen = s;
+  }
+  c->mc_state = 1;
+  return 0;
+}
+
+int caramel_mc_exchange(caramel_ctx* c) {
+  if (!c || c->mc_state != 1) return set_err(CARAMEL_ESTATE, "mc_exchange: call caramel_mc_create first");
+  if (c->rank == 0) {
+    for (int i = 1; i < c->world; ++i) {
+      const int s = accept(c->mc_listen, nullptr, nullptr);
+      if (s < 0) return set_err(CARAMEL_ECUDA, "mc_exchange: accept: %s", strerror(errno));
+      const int rc = mc_send_fd(s, c->mc_fd);
+      close(s);
+      if (rc) return set_err(CARAMEL_ECUDA, "mc_exchange: sending the handle: %s", strerror(errno));
+    }
+    close(c->mc_listen);
+    c->mc_listen = -1;
+  } else {
+    sockaddr_un a;
+    socklen_t len;
+    mc_socket_name(c->mc_name, 0, &a, &len);
+    int s = -1;
+    for (int tries = 0; tries < 600; ++tries) {  // rank 0 listens before the caller's barrier; retry briefly anyway
+      s = socket(AF_UNIX, SOCK_STREAM, 0);
+      if (s >= 0 && connect(s, (sockaddr*)&a, len) == 0) break;
+      if (s >= 0) close(s);
+      s = -1;
+      usleep(10000);
+    }
+    if (s < 0) return set_err(CARAMEL_ECUDA, "mc_exchange: cannot reach rank 0's socket");
+    const int fd = mc_recv_fd(s);
+    close(s);
+    if (fd < 0) return set_err(CARAMEL_ECUDA, "mc_exchange: no handle received");
+    c->mc_fd = fd;
+    CUmemGenericAllocationHandle mc;
+    MC_TRY(g_mc.MemImportFromShareableHandle(&mc, (void*)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR));
+    c->mc_handle = mc;
+  }
+  CUdevice dev;
+  MC_TRY(g_mc.DeviceGet(&dev, c->device));
+  MC_TRY(g_mc.MulticastAddDevice(c->mc_handle, dev));
+  c->mc_state = 2;
+  return 0;
+}
+
+int caramel_mc_bind(caramel_ctx* c, uint64_t* unicast) {
+  if (!c || c->mc_state != 2) return set_err(CARAMEL_ESTATE, "mc_bind: call caramel_mc_exchange first (every rank)");
+  CUdevice dev;
+  MC_TRY(g_mc.DeviceGet(&dev, c->device));
+  MC_TRY(g_mc.MulticastBindMem(c->mc_handle, 0, c->mc_mem, 0, c->mc_bytes, 0));
+  CUmemAccessDesc acc;
+  memset(&acc, 0, sizeof(acc));
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = dev;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  CUdeviceptr mva = 0, uva = 0;
+  MC_TRY(g_mc.MemAddressReserve(&mva, c->mc_bytes, c->mc_gran, 0, 0));
+  MC_TRY(g_mc.MemMap(mva, c->mc_bytes, 0, c->mc_handle, 0));
+  MC_TRY(g_mc.MemSetAccess(mva, c->mc_bytes, &acc, 1));
+  MC_TRY(g_mc.MemAddressReserve(&uva, c->mc_bytes, c->mc_gran, 0, 0));
+  MC_TRY(g_mc.MemMap(uva, c->mc_bytes, 0, c->mc_mem, 0));
+  MC_TRY(g_mc.MemSetAccess(uva, c->mc_bytes, &acc, 1));
+  c->mc_va = mva;
+  c->uc_va = uva;
+  CUDA_TRY(cudaMemset((void*)uva, 0, c->mc_bytes));
+  CUDA_TRY(cudaDeviceSynchronize());
+  if (unicast) *unicast = uva;
+  c->mc_state = 3;
+  return 0;
+}
+
+int caramel_allreduce_nvls(caramel_ctx* c, const caramel_bucket* b, uint32_t epoch, void* stream) {
+  if (!c || !b) return set_err(CARAMEL_EINVAL, "allreduce_nvls: null argument");
+  if (c->mc_state != 3) return set_err(CARAMEL_ESTATE, "allreduce_nvls: no bound multicast arena (caramel_mc_bind)");
+  if (b->numel == 0) return 0;
+  if (b->depth < 1 || b->depth > CARAMEL_MAX_DEPTH || b->ctas < 1)
+    return set_err(CARAMEL_EINVAL, "allreduce_nvls: bad depth or ctas");
+  if ((b->bucket_off & 15) || b->bucket_off + 4 * b->numel > c->mc_bytes)
+    return set_err(CARAMEL_EINVAL, "allreduce_nvls: bucket outside the multicast arena or misaligned");
+  if (b->epilogue == CARAMEL_EPI_SGD &&
+      (!c->param_bytes || (b->param_off & 15) || b->param_off + 4 * b->numel > c->param_bytes))
+    return set_err(CARAMEL_EINVAL, "allreduce_nvls: the SGD epilogue needs the parameter arena");
+  const uint64_t fb = (uint64_t)b->depth * b->ctas * 2 * c->world * 4;
+  if ((b->flag_off & 3) || b->flag_off + fb > c->arena_bytes)
+    return set_err(CARAMEL_EINVAL, "allreduce_nvls: flag block outside the IPC arena");
+  if (!c->imported) return set_err(CARAMEL_ESTATE, "peer arenas not mapped (call caramel_import)");
+  NvlsParams P;
+  memset(&P, 0, sizeof(P));
+  fill_env(c, P.env, epoch);
+  P.b = *b;
+  P.mc = c->mc_va;
+  P.uc = c->uc_va;
+  k_nvls<<<b->ctas, THREADS, 0, (cudaStream_t)stream>>>(P);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+static void mc_release(caramel_ctx* c) {
+  if (!c->mc_state || !mc_load()) return;
+  CUdevice dev;
+  g_mc.DeviceGet(&dev, c->device);
+  if (c->mc_va) { g_mc.MemUnmap(c->mc_va, c->mc_bytes); g_mc.MemAddressFree(c->mc_va, c->mc_bytes); }
+  if (c->uc_va) { g_mc.MemUnmap(c->uc_va, c->mc_bytes); g_mc.MemAddressFree(c->uc_va, c->mc_bytes); }
+  if (c->mc_state == 3) g_mc.MulticastUnbind(c->mc_handle, dev, 0, c->mc_bytes);
+  if (c->mc_handle) g_mc.MemRelease(c->mc_handle);
+  if (c->mc_mem) g_mc.MemRelease(c->mc_mem);
+  if (c->mc_listen >= 0) close(c->mc_listen);
+  if (c->mc_fd >= 0) close(c->mc_fd);
+  c->mc_state = 0;
 }
 
 }  // extern "C"

@@ -92,6 +92,7 @@ def main() -> int:
     failures += overlapped_hooks_check(rank, world, dev)
     failures += overlapped_hooks_check(rank, world, dev, grads="bucket")
     failures += ce_check(rank, world, dev)
+    failures += nvls_check(rank, world, dev)
     failures += overlapped_hooks_check(rank, world, dev, grads="bucket", engine="ce")
     t = torch.tensor([failures], device=dev)
     dist.all_reduce(t)
@@ -243,6 +244,87 @@ def ce_check(rank: int, world: int, dev) -> int:
                     bad = np.nonzero(got.view(np.uint32) != want.view(np.uint32))[0]
                     print(f"rank {rank}: copy-engine mismatch bucket {i} (n={n}) epi={epi} epoch {epoch}: "
                           f"{bad.size} elems, first {bad[:5]}", flush=True)
+    ctx.close()
+    return fails
+
+
+def nvls_check(rank: int, world: int, dev) -> int:
+    """NVLS two-shot (caramel_allreduce_nvls: multimem.ld_reduce / multimem.st
+    through the NVSwitch) -- the non-fixed-order mode.  Every element within
+    1e-6 x sum_r |g_r| of the float64 sum (SURVEY §8c's bound; SGD adds the
+    update's own fp32 rounding), and every replica bit-identical."""
+    rng = np.random.default_rng(900 + rank)
+    th_rng = np.random.default_rng(11)
+    sizes = [5, 1000, 70_001, 1 << 20, (3 << 20) + 7]
+    probe = comm.Context(rank, world, arena_bytes=1 << 20)
+    ok = torch.tensor([probe.nvls_available()], device=dev, dtype=torch.int32)
+    probe.close()
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if not int(ok.item()):
+        if rank == 0:
+            print("nvls: multicast objects not available on this box (skipped)", flush=True)
+        return 0
+    specs, moff, foff, poff = [], 0, 0, 0
+    for n in sizes:
+        for depth in (1, 3):
+            ctas = min(N.bucket_layout(n, depth, N.SHUFFLE, world)[0], 16)
+            fb = N.flag_bytes_for(depth, ctas, N.SHUFFLE, world)
+            specs.append((n, depth, ctas, moff, foff, poff))
+            moff = (moff + 4 * n + 255) // 256 * 256
+            foff = (foff + fb + 255) // 256 * 256
+            poff = (poff + 4 * n + 255) // 256 * 256
+    ctx = comm.Context(rank, world, arena_bytes=foff, param_bytes=poff)
+    ctx.bootstrap()
+    ctx.nvls_setup(moff)
+    stream = torch.cuda.current_stream().cuda_stream
+    fails, epoch, lr = 0, 0, 0.05
+    for epi in (N.EPI_SUM, N.EPI_SCALE, N.EPI_SGD):
+        epoch += 1
+        grads, thetas = [], []
+        for n, depth, ctas, mo, fo, po in specs:
+            g = rng.standard_normal(n).astype(np.float32)
+            th = th_rng.standard_normal(n).astype(np.float32)
+            ctx.nvls_view(mo, n).copy_(torch.from_numpy(g).to(dev))
+            ctx.arena_view(0, po, n, param=True).copy_(torch.from_numpy(th).to(dev))
+            grads.append(g)
+            thetas.append(th)
+        torch.cuda.synchronize()
+        dist.barrier()
+        for (n, depth, ctas, mo, fo, po) in specs:
+            b = comm.make_bucket(n, mo, fo, depth=depth, pattern=N.SHUFFLE, epilogue=epi, ctas=ctas,
+                                 flags=N.F_PARAM_ARENA if epi == N.EPI_SGD else 0, param_off=po, lr=lr,
+                                 scale=1.0 / world)
+            ctx.allreduce_nvls(b, epoch, stream)
+        ctx.status()
+        torch.cuda.synchronize()
+        for i, (n, depth, ctas, mo, fo, po) in enumerate(specs):
+            flat = torch.from_numpy(grads[i]).to(dev)
+            allg = [torch.empty_like(flat) for _ in range(world)]
+            dist.all_gather(allg, flat)
+            G = np.stack([a.cpu().numpy().astype(np.float64) for a in allg])
+            s64, a64 = G.sum(axis=0), np.abs(G).sum(axis=0)
+            if epi == N.EPI_SGD:
+                got = ctx.arena_view(0, po, n, param=True).clone()
+                step = lr * s64 / world
+                ref = thetas[i].astype(np.float64) - step
+                tol = 1e-6 * lr * a64 / world + 2.0 ** -23 * (np.abs(thetas[i]) + np.abs(step))
+            else:
+                got = ctx.nvls_view(mo, n).clone()
+                scale = 1.0 if epi == N.EPI_SUM else 1.0 / world
+                ref, tol = s64 * scale, 1e-6 * a64 * scale
+            err = np.abs(got.cpu().numpy().astype(np.float64) - ref)
+            if not (err <= tol).all():
+                fails += 1
+                k = int(np.argmax(err - tol))
+                print(f"rank {rank}: nvls epi={epi} n={n} depth={depth}: err {err[k]:.3e} > tol {tol[k]:.3e}",
+                      flush=True)
+            reps = [torch.empty_like(got) for _ in range(world)]
+            dist.all_gather(reps, got)
+            if any(not torch.equal(reps[0], r) for r in reps[1:]):
+                fails += 1
+                print(f"rank {rank}: nvls epi={epi} n={n}: replicas differ", flush=True)
+    if rank == 0:
+        print(f"nvls: {len(specs) * 3} bucket checks (1e-6 x sum|g| vs float64, replicas identical)", flush=True)
     ctx.close()
     return fails
 

@@ -1,6 +1,8 @@
-"""Emulated-rank probe of the push kernel: one bucket, pattern SHUFFLE, p ranks
-on cuda:0; prints the protocol, the time and, after a watchdog timeout, the
-flag words of every rank."""
+"""Emulated-rank check of the opt-in push engine (CARAMEL_PUSH=1, read at library
+load, hence a separate process: tests/test_gpu_robustness.py runs it).  Single
+buckets and bucket lists of every protocol (LL, one-shot, two-shot), p ranks on
+cuda:0, bit-exact against the oracle; after a watchdog timeout the flag words
+of every rank are printed.  Prints "MISMATCH" / "TIMEOUT" on failure."""
 import ctypes, sys, time
 from pathlib import Path
 import numpy as np
@@ -47,11 +49,6 @@ def run(n, p, depth, epi=N.EPI_SUM, epochs=2, ctas_cap=None):
     ctx.close()
     return True
 
-if __name__ == "__main__" and len(sys.argv) == 1:
-    for (n, p, d) in [(1 << 20, 2, 1), (70000, 4, 1), (300000, 4, 1), (1 << 20, 4, 1), (1 << 20, 4, 3), (1 << 20, 3, 1), (1 << 22, 8, 2)]:
-        run(n, p, d)
-
-
 def run_list(model, p, mode, epochs=3):
     """Whole plan of `model` as one caramel_allreduce_many list, emulated; on a
     timeout print every bucket whose flags never reached the epoch."""
@@ -89,11 +86,6 @@ def run_list(model, p, mode, epochs=3):
                               f"{low}/{f.size} flag words below epoch {e}")
             break
     ctx.close()
-
-
-if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] != "custom":
-    for m in sys.argv[1:]:
-        run_list(m, 4, N.MANY_FLAGS)
 
 
 def run_custom(sizes, p, mode=N.MANY_FLAGS, depth=1, epochs=3):
@@ -146,9 +138,15 @@ def run_custom(sizes, p, mode=N.MANY_FLAGS, depth=1, epochs=3):
     ctx.close()
 
 
-if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "custom":
-    for p in (4, 2):
-        run_custom([300000, 400000], p)           # two OS
-        run_custom([2000000, 3000000], p)         # two TS (p=4)
-        run_custom([300000, 2000000, 200000], p)  # OS TS OS
+if __name__ == "__main__":
+    for (n, p, d) in [(1 << 20, 2, 1), (70000, 4, 1), (300000, 4, 1), (1 << 20, 4, 1), (1 << 20, 4, 3), (1 << 20, 3, 1),
+                      (1 << 22, 8, 2), (3 << 20, 2, 2)]:
+        run(n, p, d)
+    for p in (4, 2, 8):
+        run_custom([300000, 400000], p)           # one-shot
+        run_custom([2000000, 3000000], p)         # two-shot
         run_custom([1000, 300000, 5000, 2000000, 200, 100000], p)  # LL interleaved
+        run_custom([1000, 300000, 5000, 2000000, 200, 100000], p, mode=N.MANY_FUSED)
+    for m in ("resnet50", "inception_v3"):
+        run_list(m, 4, N.MANY_FLAGS)
+        run_list(m, 8, N.MANY_FUSED)

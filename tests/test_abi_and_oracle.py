@@ -79,13 +79,10 @@ def test_chunk_rule_agrees_with_reference_float_bytes():
 def test_bucket_layout_and_errors():
     N = _lib()
     ctas, bb, fb = N.bucket_layout(1 << 20, 2, N.SHUFFLE, 8)
-    # packed bucket + push region (256 B header, per-item flags: 2 chunks x 16
-    # ranges of 128 KB x {READY, DONE} x 8 sources, 2 x 7 inbox slots mirroring
-    # the bucket) + 7 copy-engine staging slots of ceil(n/8)+3 elements
+    # packed bucket + 7 copy-engine staging slots of ceil(n/8)+3 elements (the
+    # push engine's inbox region is only laid out with CARAMEL_PUSH=1)
     slot = (4 * ((1 << 20) // 8 + 3) + 15) & ~15
-    push = 256 + 2 * 16 * 2 * 8 * 4 + 2 * 7 * (4 << 20)
-    assert 1 <= ctas <= 64 and bb == (4 << 20) + push + 7 * slot and fb > 0
-    # LL buckets (<= 64K elements) carry no push region
+    assert 1 <= ctas <= 64 and bb == (4 << 20) + 7 * slot and fb > 0
     ll = (4 * 1000 + 8 * 1000 * 9 + 255) // 256 * 256  # LL region: bucket + out + 8 in-slots of 8 B words
     assert N.bucket_layout(1000, 1, N.SHUFFLE, 8)[1] == ll + 7 * ((4 * (125 + 3) + 15) & ~15)
     assert N.bucket_layout(1 << 20, 2, N.SHUFFLE, 1)[1] == 4 << 20  # one rank: no staging
@@ -183,6 +180,24 @@ def test_lowering_is_rank_invariant_and_covers_the_plan():
         # regions never overlap
         spans = sorted((b.bucket_off, b.flag_off) for b in plan.buckets)
         assert all(a[1] <= b[0] for a, b in zip(spans, spans[1:]))
+
+
+
+def test_push_engine_layout_adds_the_inbox_region(tmp_path):
+    """With CARAMEL_PUSH=1 every non-LL two-shot bucket also carries the push
+    engine's region: a 256 B header, per-item flags (chunks x 128 KB ranges x
+    {READY, DONE} x sources) and 2 x (p-1) inbox slots mirroring the bucket.
+    Checked in a fresh process (the switch is read once per process)."""
+    import subprocess
+    import sys
+
+    code = ("import sys; sys.path.insert(0, %r); from paper_2004_14020_b200 import _native as N; "
+            "print(N.bucket_layout(1 << 20, 2, N.SHUFFLE, 8)[1])" % str(ROOT))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                         env={**__import__("os").environ, "CARAMEL_PUSH": "1"}, check=True).stdout
+    slot = (4 * ((1 << 20) // 8 + 3) + 15) & ~15
+    push = 256 + 2 * 16 * 2 * 8 * 4 + 2 * 7 * (4 << 20)
+    assert int(out) == (4 << 20) + push + 7 * slot
 
 
 def test_lean_shuffle_oracle_equals_the_chunked_restatement():

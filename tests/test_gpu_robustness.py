@@ -126,3 +126,21 @@ def test_close_returns_torch_owned_storage():
         assert all(np.isfinite(v.cpu().numpy()).all() for v in sd.values())
         model(x).sum().item()
         model.zero_grad(set_to_none=True)
+
+
+def test_push_engine_parity_in_its_own_process():
+    """The TMA push engine (one-shot / two-shot push, CARAMEL_PUSH=1) over
+    single buckets, synthetic lists and full ResNet-50 / Inception-v3 plans,
+    FLAGS and FUSED lists, emulated p = 2..8: bit-exact, no watchdog."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    here = Path(__file__).resolve().parent
+    r = subprocess.run([sys.executable, str(here / "_push_engine_check.py")], capture_output=True, text=True,
+                       timeout=900, env={**os.environ, "CARAMEL_PUSH": "1", "CARAMEL_FUSED_PUSH": "64"})
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "MISMATCH" not in out and "TIMEOUT" not in out, out[-4000:]
+    assert out.count(": ok") >= 40, out[-4000:]

@@ -1,9 +1,13 @@
 #!/bin/bash
 export PYTHONUNBUFFERED=1
 mkdir -p gpurun_out
-CARAMEL_LL_MAX=0 timeout 300 python tools/debug_push.py resnet50 inception_v3 > gpurun_out/debug_list_noll.txt 2>&1; echo "debug rc=$?"
-timeout 900 python -m pytest tests -m gpu -q -x --durations=5 > gpurun_out/gputest.txt 2>&1; echo "gputest rc=$?"
-tail -3 gpurun_out/gputest.txt
-CARAMEL_FUSED_PUSH=64 timeout 900 python -m pytest tests/test_gpu_baseline_sizes.py tests/test_gpu_kernels.py -m gpu -q -x -k "fused or many" > gpurun_out/gputest_fp.txt 2>&1; echo "gputest fused-push rc=$?"
-tail -3 gpurun_out/gputest_fp.txt
+timeout 600 python -m pytest tests/test_multigpu.py -q -x -s > gpurun_out/mgpu.txt 2>&1; echo "mgpu rc=$?"
+grep -i "nvls\|parity" gpurun_out/mgpu.txt | head
+CARAMEL_WATCHDOG_MS=2000 SWEEP_MAX=$((16<<20)) SWEEP_ENGINES=nvls timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+    --master-addr 127.0.0.1 --master-port 29512 tools/sweep.py > gpurun_out/sweep_nvls_only.jsonl 2> gpurun_out/sweep_nvls_only.err
+echo "sweep nvls rc=$?"
+cat gpurun_out/sweep_nvls_only.jsonl | head -20
+CARAMEL_WATCHDOG_MS=2000 SWEEP_MAX=$((16<<20)) SWEEP_ENGINES=single,fused timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+    --master-addr 127.0.0.1 --master-port 29512 tools/sweep.py > gpurun_out/sweep_sf.jsonl 2> gpurun_out/sweep_sf.err
+echo "sweep sf rc=$?"
 echo done

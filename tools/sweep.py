@@ -24,6 +24,12 @@ def main():
     region = (region + (1 << 20)) // (1 << 20) * (1 << 20)
     ctx = comm.Context(rank, world, arena_bytes=region + (256 << 20))
     ctx.bootstrap()
+    if "nvls" in engines:
+        if not ctx.nvls_available():
+            engines = [e for e in engines if e != "nvls"]
+        else:
+            ctx.nvls_setup(max_bytes + (1 << 21))
+            comm._view_fp32(ctx.nvls_base, maxel).normal_()
     base, _ = ctx.arena_ptrs(0)
     buf = comm._view_fp32(base, maxel)
     buf.normal_()
@@ -36,7 +42,7 @@ def main():
           for pat in pats:
             if pat == N.HD and world & (world - 1):
                 continue
-            if engine == "fused" and pat != N.SHUFFLE:
+            if engine in ("fused", "nvls") and pat != N.SHUFFLE:
                 continue
             for depth in depths:
                 ctas, bbytes, fbytes = N.bucket_layout(n, depth, pat, world)
@@ -59,6 +65,8 @@ def main():
                         N.check(N.lib().caramel_allreduce_many(ctx._ctx, host, 1, dlist.data_ptr(), pre.data_ptr(),
                                                                spre.data_ptr(), 0, N.MANY_FUSED, ep,
                                                                ctypes.c_void_p(stream.cuda_stream)))
+                    elif engine == "nvls":
+                        ctx.allreduce_nvls(b, ep, stream.cuda_stream)
                     else:
                         ctx.allreduce(b, ep, stream.cuda_stream)
 
