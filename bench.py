@@ -638,8 +638,12 @@ def bucket_sweep(torch, dist, world, rank, dev, iters=20, network=None):
         c.bootstrap()
         comm._view_fp32(c.arena_ptrs(0)[0], big // 4).normal_()
         ce_ctx["ce"], ce_epoch["ce"] = c, 0
-    # the NVLS (multicast, in-switch reduction) two-shot: the non-fixed-order mode
+    # the NVLS (multicast, in-switch reduction) two-shot: the non-fixed-order mode;
+    # its CTAs only issue switch round trips, so it takes the whole GPU
     nvls_ok = ctx.nvls_available()
+
+    def nvls_ctas(n):
+        return int(max(1, min(148, n // world // 2048)))
     if nvls_ok:
         ctx.nvls_setup(big + (2 << 20))
         comm._view_fp32(ctx.nvls_base, big // 4).normal_()
@@ -724,7 +728,7 @@ def bucket_sweep(torch, dist, world, rank, dev, iters=20, network=None):
                 row[f"{key}_bus_gbs"] = round(bus / us_e, 1)
         if nvls_ok:
             bn = comm.make_bucket(n, 0, region + k * (1 << 20), depth=depth, pattern=N.SHUFFLE,
-                                  epilogue=N.EPI_SUM, flags=0, ctas=min(ctas, 32))
+                                  epilogue=N.EPI_SUM, flags=0, ctas=nvls_ctas(n))
 
             def nvls_call(st=None, bn=bn):
                 st = st or stream

@@ -2944,7 +2944,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_nvls(const __grid_constant__ Nvl
     for (uint64_t x = lo + threadIdx.x; x < a; x += blockDim.x) mc_st1(mcb + x, epi1(epi, mc_ld_reduce1(mcb + x), 0.f, B.scale, B.lr));
     for (uint64_t x = (b > a ? b : a) + threadIdx.x; x < hi; x += blockDim.x)
       mc_st1(mcb + x, epi1(epi, mc_ld_reduce1(mcb + x), 0.f, B.scale, B.lr));
-    constexpr int U = 4;  // switch round trips in flight per thread
+    constexpr int U = 8;  // switch round trips in flight per thread
     const uint64_t T = 4ull * blockDim.x;
     uint64_t v = a + 4ull * threadIdx.x;
     for (; v + (U - 1) * T < b; v += U * T) {
@@ -3167,14 +3167,18 @@ int caramel_bucket_layout(uint64_t numel, int depth, int pattern, int world, int
   if (rc) return rc;
   if (depth < 1 || depth > CARAMEL_MAX_DEPTH)
     return set_err(CARAMEL_EINVAL, "depth must be in [1, %d]", CARAMEL_MAX_DEPTH);
-  uint64_t per = numel / ((uint64_t)depth * world);  // elements per shard per chunk
+  // The CTA count follows the bytes each rank owns (numel / world), NOT the
+  // per-chunk share: chunk-parallel groups then split the same grid, so a
+  // deeper split costs no parallelism (round 1 divided by depth as well, and a
+  // 4 MiB bucket at depth 8 ran on 16 CTAs instead of 64: 55.6 vs 26.6 us).
+  uint64_t per = numel / (uint64_t)world;
   const uint64_t tile = (uint64_t)THREADS * 4 * 2;   // one trip of rs_ag_range
   uint64_t g;
   if (world == 1) {
     g = (numel + 4 * tile - 1) / (4 * tile);
     if (g > 148 * 4) g = 148 * 4;
   } else if (use_ll(pattern, world, numel)) {
-    g = (per + 511) / 512;  // latency-bound: spread the few elements wide
+    g = (per / depth + 511) / 512;  // latency-bound: spread the few elements wide
     if (g > 32) g = 32;
   } else {
     g = (per + tile - 1) / tile;

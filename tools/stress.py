@@ -13,7 +13,6 @@ import torch
 import torch.distributed as dist
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
-sys.path.insert(0, str(ROOT / "tests"))
 
 
 def main():
@@ -27,7 +26,7 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    from test_gpu_baseline_sizes import NVLINK_MODEL
+    NVLINK_MODEL = (10.0, 1.0 / 460e3)  # SURVEY §8a "NVLink-ish" network model
     from paper_2004_14020_b200 import gradsets
     from paper_2004_14020_b200.collective import Pattern, ReduceModel
     from paper_2004_14020_b200.costmodel import NetworkModel
