@@ -2121,7 +2121,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 2) k_local_flat_tma(const __grid_
 // ---------------------------------------------------------------------------
 // K1 / K4 through the TMA unit (caramel_pack / caramel_unpack): the bucket is
 // cut into 32 KB tiles; a persistent CTA per SM streams its tiles through a
-// 4-stage shared-memory ring.  Pack: every member piece of a tile whose source
+// 6-stage shared-memory ring.  Pack: every member piece of a tile whose source
 // and tile position share their 16-byte phase is one cp.async.bulk load into
 // the tile (completion on the stage's mbarrier); the rare misaligned piece is
 // copied into the tile by all threads; the whole tile leaves with ONE bulk
@@ -2132,9 +2132,9 @@ __global__ void __launch_bounds__(TMA_THREADS, 2) k_local_flat_tma(const __grid_
 // ---------------------------------------------------------------------------
 #define KT_THREADS 256
 #define KT_TILE 8192                 // floats per tile (32 KB)
-#define KT_STAGES 4
+#define KT_STAGES 6                  // 4 tiles of loads in flight per SM (HBM latency x bandwidth / 148 SMs ~ 66 KB)
 #define KT_MAXODD 32                 // misaligned pieces remembered per tile (more: the tile goes plain)
-#define KT_MAXSEG 1024               // member tables up to this size are cached in shared memory
+#define KT_MAXSEG 512                // member tables up to this size are cached in shared memory
 
 struct KtOdd { uint64_t src, dst; uint32_t n; };  // a misaligned piece: element addresses, count
 
