@@ -604,6 +604,7 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
 
 SWEEP_SIZES = tuple(4096 * 4 ** i for i in range(10))  # 4 KiB .. 1 GiB
 SWEEP_DEPTHS = (1, 2, 4, 8)
+SWEEP_REPS = 3  # repetitions of every sweep row (median reported, [min, max] kept)
 
 
 def bucket_sweep(torch, dist, world, rank, dev, iters=20, network=None):
@@ -675,19 +676,25 @@ def bucket_sweep(torch, dist, world, rank, dev, iters=20, network=None):
                     torch.cuda.synchronize()
                 except Exception:
                     g = None
-            dist.barrier()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record(stream)
-            if g is not None:
-                g.replay()
-            else:
-                for _ in range(iters):
-                    fn()
-            e.record(stream)
-            e.synchronize()
-            t = torch.tensor([s.elapsed_time(e) / iters], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            return t.item() * 1e3, g is not None  # us
+            # SWEEP_REPS repetitions (each `iters` calls, max over ranks); the
+            # row reports their median and spread
+            reps = []
+            for _ in range(SWEEP_REPS):
+                dist.barrier()
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record(stream)
+                if g is not None:
+                    g.replay()
+                else:
+                    for _ in range(iters):
+                        fn()
+                e.record(stream)
+                e.synchronize()
+                t = torch.tensor([s.elapsed_time(e) / iters], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                reps.append(t.item() * 1e3)
+            spread.append([round(min(reps), 2), round(max(reps), 2)])
+            return _median(reps), g is not None  # us
 
         def caramel(st=None):
             st = st or stream
@@ -695,12 +702,14 @@ def bucket_sweep(torch, dist, world, rank, dev, iters=20, network=None):
             ctx.allreduce(b, 0, st.cuda_stream)  # epoch 0: device counter (graph-replayable)
 
         x = torch.empty(n, device=dev).normal_()
+        spread = []
         us_c, gc = timed(caramel)
         us_n, gn = timed(lambda st=None: dist.all_reduce(x))
         bus = 2 * (world - 1) / world * size / 1e3
         row = {"bytes": size, "depth": depth, "caramel_us": round(us_c, 2),
                "caramel_bus_gbs": round(bus / us_c, 1), "nccl_us": round(us_n, 2),
-               "nccl_bus_gbs": round(bus / us_n, 1), "graphed": [gc, gn]}
+               "nccl_bus_gbs": round(bus / us_n, 1), "graphed": [gc, gn],
+               "spread_us": {"caramel": spread[0], "nccl": spread[1]}, "reps": SWEEP_REPS}
         if size >= (1 << 20):
             fixed = {}
             for d in SWEEP_DEPTHS:
