@@ -48,6 +48,23 @@ ALIGN = 256
 CE_MIN_CONNECTIONS = 16
 
 
+def agree(what: str, payload: str, world: int, group=None) -> None:
+    """All-gather a rank's view of `what` (its hash) and raise DeadlockDetected
+    if any two ranks differ: the flag protocols are only deadlock-free when
+    every rank launches the same buckets, in the same order, the same way."""
+    import torch.distributed as dist
+
+    from .sim import DeadlockDetected
+
+    mine = hashlib.sha256(payload.encode()).hexdigest()
+    allv: list = [None] * world
+    dist.all_gather_object(allv, mine, group=group)
+    if len(set(allv)) != 1:
+        bad = [r for r, v in enumerate(allv) if v != allv[0]]
+        raise DeadlockDetected(f"ranks disagree on the {what} (ranks {bad} differ from rank 0): "
+                               "the flag protocols would deadlock")
+
+
 def ce_connections_ok() -> bool:
     """True if CUDA_DEVICE_MAX_CONNECTIONS gives every stream its own queue."""
     try:
@@ -196,12 +213,7 @@ class Aggregator:
         self.ctx = comm.Context(rank, self.world, plan.arena_bytes,
                                 plan.param_bytes if self.param_arena else 0)
         if self.world > 1 and bootstrap:
-            import torch.distributed as dist
-
-            digests: list = [None] * self.world
-            dist.all_gather_object(digests, plan.digest(), group=group)
-            if len(set(digests)) != 1:
-                raise RuntimeError("ranks disagree on the execution plan (digest mismatch)")
+            agree("execution plan", plan.digest(), self.world, group)
             self.ctx.bootstrap(group)
         if engine == "ce" and not N.lib().caramel_ce_available(self.ctx._ctx):
             raise RuntimeError("engine='ce': this device lacks 64-bit stream memory operations")
@@ -576,18 +588,12 @@ class Aggregator:
         decide it) once, before the first overlapped iteration: a bucket run by
         the copy-engine protocol on one rank and by the SM flag protocol on
         another would hang, so a mismatch raises instead."""
-        import torch.distributed as dist
-
         doc = json.dumps({"plan": self.plan.digest(), "engine": self.engine,
                           "assignment": self.engine_assignment(),
                           "knobs": [self.ce_min_bytes, self.ce_tail_us, self.ce_tail_frac,
                                     self.coalesce_buckets, self.coalesce_bytes, self.coalesce_ctas]})
-        mine = hashlib.sha256(doc.encode()).hexdigest()
-        allv: list = [None] * self.world
-        dist.all_gather_object(allv, mine, group=self._group)
-        if len(set(allv)) != 1:
-            raise RuntimeError("ranks disagree on the engine of some bucket (engine, ce_min_bytes, ce_tail_* "
-                               "or coalescing knobs differ): the flag protocols would deadlock")
+        agree("engine of some bucket (engine, ce_min_bytes, ce_tail_* or coalescing knobs)", doc, self.world,
+              self._group)
         self._engines_checked = True
 
     def _ce_engine_of(self, k: int) -> str:
