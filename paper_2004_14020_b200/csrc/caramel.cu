@@ -699,11 +699,6 @@ __host__ __device__ __forceinline__ uint64_t ll_region_bytes(uint64_t numel, int
 //    coordinates (element x of source q's contribution at slot + 4x, so every
 //    slot keeps the bucket's 16-byte phase and TMA bulk copies line up)]
 //   [copy-engine staging slots (caramel_allreduce_ce)]
-__host__ __device__ __forceinline__ uint64_t kernel_region_bytes(uint64_t numel, int pattern, int world) {
-  const uint64_t e = out_region_elems(numel);
-  return use_ll(pattern, world, numel) ? (ll_region_bytes(numel, world) + 15) & ~15ull
-                                       : 4 * ((world > 1 && pattern != CARAMEL_SHUFFLE) ? 2 * e : e);
-}
 // The push engine is opt-in (CARAMEL_PUSH=1, identical on every rank): on the
 // B200 NVSwitch boxes measured so far the register-pull kernels move the same
 // bytes faster.
@@ -715,6 +710,43 @@ __host__ __device__ __forceinline__ bool push_enabled() {
 #else
   return h_push_enabled != 0;
 #endif
+}
+
+// LL128 ("low latency, 128-byte lines"): two-shot buckets just above the LL
+// cutoff.  Every value travels in a 128-byte line of 30 floats + an 8-byte
+// epoch flag, written by 8 lanes of one warp instruction (16 B each) and read
+// the same way: when the reader sees the flag, the whole line has landed
+// (NVLink delivers the line as one unit -- the property NCCL's LL128 relies
+// on), so data carries its own flag at 120/128 efficiency and a bucket costs
+// two one-way hops with no fence and no flag round trip.  Region after the
+// float bucket: [out: one line per 30 elements][in: p slots of the same lines].
+#define LL128_MAX_ELEMS (1u << 19)  // 2 MiB (p=2: 1 MiB 17.7 vs 22.2 us flags, 4 MiB 26.2 vs 25.5); CARAMEL_LL128_MAX overrides
+#define LL128_FLOATS 30
+__device__ uint64_t d_ll128_max = LL128_MAX_ELEMS;
+static uint64_t h_ll128_max = LL128_MAX_ELEMS;
+__host__ __device__ __forceinline__ bool use_ll128(int pattern, int world, uint64_t numel) {
+#ifdef __CUDA_ARCH__
+  const uint64_t cut = d_ll128_max;
+#else
+  const uint64_t cut = h_ll128_max;
+#endif
+  return pattern == CARAMEL_SHUFFLE && world > 1 && !push_enabled() && !use_ll(pattern, world, numel) &&
+         numel <= cut;
+}
+__host__ __device__ __forceinline__ uint64_t ll128_lines(uint64_t numel) {
+  return (numel + LL128_FLOATS - 1) / LL128_FLOATS;
+}
+__host__ __device__ __forceinline__ uint64_t ll128_out_off(uint64_t numel) {  // bytes from bucket start
+  return (4 * numel + 127) & ~127ull;
+}
+__host__ __device__ __forceinline__ uint64_t ll128_region_bytes(uint64_t numel, int world) {
+  return ll128_out_off(numel) + 128 * ll128_lines(numel) * (1 + (uint64_t)world);
+}
+__host__ __device__ __forceinline__ uint64_t kernel_region_bytes(uint64_t numel, int pattern, int world) {
+  const uint64_t e = out_region_elems(numel);
+  if (use_ll(pattern, world, numel)) return (ll_region_bytes(numel, world) + 15) & ~15ull;
+  if (use_ll128(pattern, world, numel)) return ll128_region_bytes(numel, world);
+  return 4 * ((world > 1 && pattern != CARAMEL_SHUFFLE) ? 2 * e : e);
 }
 __host__ __device__ __forceinline__ bool has_push_region(uint64_t numel, int pattern, int world) {
   return push_enabled() && pattern == CARAMEL_SHUFFLE && world > 1 && numel > 0 && !use_ll(pattern, world, numel);
@@ -1524,6 +1556,176 @@ __device__ void phase_ll_finish(const BucketRun& R) {
     }
 }
 
+// ---- LL128 protocol phases (mid-size two-shot buckets, see use_ll128) -------------
+// Ownership is by LINES (30 elements): shard s = lines [s L / p, (s+1) L / p);
+// CTA j of the bucket takes part j of every shard's lines; inside a CTA, an
+// 8-lane group handles one line per step (lane k: floats 4k..4k+3 of the
+// line; lane 7: floats 28, 29 and the 8-byte flag {epoch, epoch}).
+__device__ __forceinline__ uint4 ll128_ld(const void* p) {
+  uint4 v;
+  asm volatile("ld.relaxed.sys.global.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void ll128_st(void* p, uint4 v) {
+  asm volatile("st.relaxed.sys.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ char* ll128_out(const BucketRun& R, int rank) {
+  return reinterpret_cast<char*>(R.E->arena[rank] + R.B->bucket_off + ll128_out_off(R.B->numel));
+}
+__device__ __forceinline__ char* ll128_in(const BucketRun& R, int rank, int slot) {
+  return ll128_out(R, rank) + 128 * ll128_lines(R.B->numel) * (1 + (uint64_t)slot);
+}
+// lines of shard s handled by this CTA (tile X.j of X.G)
+__device__ __forceinline__ void ll128_part(const BucketRun& R, int s, uint64_t& l0, uint64_t& l1) {
+  const uint64_t L = ll128_lines(R.B->numel);
+  const int p = R.X.world;
+  const uint64_t a = split_at(L, p, s), b = split_at(L, p, s + 1);
+  l0 = a + split_at(b - a, R.X.G, R.X.j);
+  l1 = a + split_at(b - a, R.X.G, R.X.j + 1);
+}
+// Poll one line (this lane's 16 B) until the group's flag word carries `epoch`.
+// Every lane of the warp calls (groups of 8 lanes, possibly different lines or
+// none: active = false).  Returns the lane's 16 B; `bad` set on a watchdog.
+__device__ __forceinline__ uint4 ll128_wait(const char* line, bool active, uint32_t epoch, const Env& E, int& bad) {
+  const int lane = threadIdx.x & 31, k = lane & 7, g7 = (lane & ~7) | 7;
+  uint4 v = active ? ll128_ld(line + 16 * k) : make_uint4(0, 0, 0, 0);
+  bool ok = !active || (k == 7 ? (v.z == epoch && v.w == epoch) : true);
+  ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, g7) != 0;
+  if (__all_sync(0xffffffffu, ok)) return v;
+  const uint64_t t0 = globaltimer();
+  uint32_t spins = 0;
+  while (!__all_sync(0xffffffffu, ok || bad)) {
+    if (!ok && !bad) {
+      v = ll128_ld(line + 16 * k);
+      if ((++spins & 1023u) == 0) {
+        if (poisoned(E)) bad = 1;
+        else if (globaltimer() - t0 > E.timeout_ns) {
+          raise_timeout(E);
+          bad = 1;
+        }
+      }
+    }
+    bool mine_ok = !active || (k == 7 ? (v.z == epoch && v.w == epoch) : true);
+    ok = __shfl_sync(0xffffffffu, mine_ok ? 1 : 0, g7) != 0;
+  }
+  return v;
+}
+
+// A: my contribution to every line of every shard -> the owner's in-slot `me`
+__device__ void phase_ll128_scatter(const BucketRun& R) {
+  const int me = R.X.me, p = R.X.world, k = threadIdx.x & 7;
+  const uint64_t n = R.B->numel;
+  const bool pack = R.B->flags & CARAMEL_F_PACK;
+  const float* bkt = R.bucket(me);
+  Cursor gc;
+  cur_init(gc, R.segs, R.B->nseg);
+  const uint32_t ep = R.X.epoch;
+  const int groups = blockDim.x / 8, gid = threadIdx.x / 8;
+  for (int t = 0; t < p; ++t) {
+    const int s = (me + t) % p;  // rotated: every link starts busy
+    uint64_t l0, l1;
+    ll128_part(R, s, l0, l1);
+    char* dst = ll128_in(R, s, me);
+    for (uint64_t L = l0 + gid; L < l1; L += groups) {
+      float f[4];
+      const int nf = k == 7 ? 2 : 4;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint64_t e = LL128_FLOATS * L + 4 * k + i;
+        f[i] = (i < nf && e < n) ? (pack ? seg_ld1(gc, e, 0) : ld1(bkt + e)) : 0.f;
+      }
+      uint4 v = make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]), __float_as_uint(f[3]));
+      if (k == 7) v.z = v.w = ep;
+      ll128_st(dst + 128 * L + 16 * k, v);
+    }
+  }
+}
+
+// B: my shard's lines -- every source in rank order, epilogue, result to every rank's out
+template <int NP>
+__device__ void phase_ll128_reduce(const BucketRun& R) {
+  const int me = R.X.me, k = threadIdx.x & 7;
+  const uint64_t n = R.B->numel;
+  const uint32_t ep = R.X.epoch;
+  const bool sgd = R.B->epilogue == CARAMEL_EPI_SGD;
+  const float* th = R.theta_flat();
+  Cursor tc;
+  cur_init(tc, R.segs, R.B->nseg);
+  uint64_t l0, l1;
+  ll128_part(R, me, l0, l1);
+  const int groups = blockDim.x / 8, gid = threadIdx.x / 8;
+  const uint64_t iters = (l1 - l0 + groups - 1) / groups;  // warp-uniform trip count
+  int bad = 0;
+  for (uint64_t it = 0; it < iters; ++it) {
+    const uint64_t L = l0 + gid + it * groups;
+    const bool active = L < l1;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const uint4 v = ll128_wait(ll128_in(R, me, q) + 128 * L, active, ep, *R.E, bad);
+      const float f[4] = {__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z), __uint_as_float(v.w)};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i] = q == 0 ? f[i] : __fadd_rn(acc[i], f[i]);
+    }
+    if (!active || bad) continue;  // nothing derived from a missing input is stored
+    const int nf = k == 7 ? 2 : 4;
+    float o[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint64_t e = LL128_FLOATS * L + 4 * k + i;
+      if (i < nf && e < n) {
+        const float t = sgd ? (th ? ld1(th + e) : seg_ld1(tc, e, 1)) : 0.f;
+        o[i] = epi1(R.B->epilogue, acc[i], t, R.B->scale, R.B->lr);
+      }
+    }
+    uint4 v = make_uint4(__float_as_uint(o[0]), __float_as_uint(o[1]), __float_as_uint(o[2]), __float_as_uint(o[3]));
+    if (k == 7) v.z = v.w = ep;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) ll128_st(ll128_out(R, (me + q) % NP) + 128 * L + 16 * k, v);
+  }
+}
+
+// C: my part of every shard's result lines -> parameter arena / bucket / members
+__device__ void phase_ll128_finish(const BucketRun& R) {
+  const int me = R.X.me, p = R.X.world, k = threadIdx.x & 7;
+  const uint64_t n = R.B->numel;
+  const uint32_t ep = R.X.epoch;
+  const bool unpack = (R.B->flags & CARAMEL_F_UNPACK) && !R.arena;
+  const int which = R.B->epilogue == CARAMEL_EPI_SGD ? 1 : 0;
+  float* res = R.arena ? R.out(me) : R.bucket(me);
+  Cursor uc;
+  cur_init(uc, R.segs, R.B->nseg);
+  const char* in = ll128_out(R, me);
+  const int groups = blockDim.x / 8, gid = threadIdx.x / 8;
+  int bad = 0;
+  for (int s = 0; s < p; ++s) {
+    uint64_t l0, l1;
+    ll128_part(R, s, l0, l1);
+    const uint64_t iters = (l1 - l0 + groups - 1) / groups;
+    for (uint64_t it = 0; it < iters; ++it) {
+      const uint64_t L = l0 + gid + it * groups;
+      const bool active = L < l1;
+      const uint4 v = ll128_wait(in + 128 * L, active, ep, *R.E, bad);
+      if (!active || bad) continue;
+      const float f[4] = {__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z), __uint_as_float(v.w)};
+      const int nf = k == 7 ? 2 : 4;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint64_t e = LL128_FLOATS * L + 4 * k + i;
+        if (i < nf && e < n) {
+          if (unpack) seg_st1(uc, e, which, f[i]);
+          else st1(res + e, f[i]);
+        }
+      }
+    }
+  }
+}
+
 // phase 3: (shuffle) wait for every rank's all-gather; fused unpack; (ring/hd)
 // release the buffers I read from
 template <int PAT>
@@ -1577,6 +1779,12 @@ __device__ __forceinline__ void run_bucket(const Env& E, const caramel_bucket& B
     phase_ll_scatter(R);
     phase_ll_reduce<NP>(R);
     phase_ll_finish(R);
+    return;
+  }
+  if (use_ll128(PAT, E.world, B.numel)) {
+    phase_ll128_scatter(R);
+    phase_ll128_reduce<NP>(R);
+    phase_ll128_finish(R);
     return;
   }
   if (PAT == CARAMEL_SHUFFLE) {
@@ -2351,7 +2559,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_collective_many(const __grid_con
           const caramel_bucket B = P.bs[i];
           const int j = my_tile(base, B.ctas);
           base = (base + B.ctas) % G;
-          if (j < 0 || B.numel == 0 || use_ll(PAT, p, B.numel)) continue;
+          if (j < 0 || B.numel == 0 || use_ll(PAT, p, B.numel) || use_ll128(PAT, p, B.numel)) continue;
           const int ns = nslots(PAT, p);
           BucketRun R;
           make_run(R, E, B, PAT, lr_idx, epoch, j);
@@ -2378,6 +2586,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_collective_many(const __grid_con
           if (phase == 0) phase_ll_scatter(R);
           else if (phase == 1) phase_ll_reduce<NP>(R);
           else phase_ll_finish(R);
+          continue;
+        }
+        if (use_ll128(PAT, E.world, B.numel)) {
+          if (phase == 0) phase_ll128_scatter(R);
+          else if (phase == 1) phase_ll128_reduce<NP>(R);
+          else phase_ll128_finish(R);
           continue;
         }
         if (phase == 0) phase_pack<PAT, true>(R);
@@ -3120,6 +3334,8 @@ static void load_ll_max() {
   if (const char* e = getenv("CARAMEL_LL_MAX")) h_ll_max = strtoull(e, 0, 10);
   if (const char* e = getenv("CARAMEL_OS_MAX")) h_os_max = strtoull(e, 0, 10);
   if (const char* e = getenv("CARAMEL_PUSH")) h_push_enabled = atoi(e) != 0;
+  if (const char* e = getenv("CARAMEL_LL128_MAX")) h_ll128_max = strtoull(e, 0, 10);
+  cudaMemcpyToSymbol(d_ll128_max, &h_ll128_max, sizeof(h_ll128_max));
   cudaMemcpyToSymbol(d_ll_max, &h_ll_max, sizeof(h_ll_max));
   cudaMemcpyToSymbol(d_os_max, &h_os_max, sizeof(h_os_max));
   cudaMemcpyToSymbol(d_push_enabled, &h_push_enabled, sizeof(h_push_enabled));
@@ -3175,6 +3391,7 @@ int caramel_bucket_layout(uint64_t numel, int depth, int pattern, int world, int
   if (getenv("CARAMEL_LL_MAX")) h_ll_max = strtoull(getenv("CARAMEL_LL_MAX"), 0, 10);
   if (getenv("CARAMEL_OS_MAX")) h_os_max = strtoull(getenv("CARAMEL_OS_MAX"), 0, 10);
   if (getenv("CARAMEL_PUSH")) h_push_enabled = atoi(getenv("CARAMEL_PUSH")) != 0;
+  if (getenv("CARAMEL_LL128_MAX")) h_ll128_max = strtoull(getenv("CARAMEL_LL128_MAX"), 0, 10);
   int rc = validate_workers(pattern, world);
   if (rc) return rc;
   if (depth < 1 || depth > CARAMEL_MAX_DEPTH)
@@ -3192,6 +3409,9 @@ int caramel_bucket_layout(uint64_t numel, int depth, int pattern, int world, int
   } else if (use_ll(pattern, world, numel)) {
     g = (per / depth + 511) / 512;  // latency-bound: spread the few elements wide
     if (g > 32) g = 32;
+  } else if (use_ll128(pattern, world, numel)) {
+    g = (ll128_lines(numel) / world + 127) / 128;  // ~2 lines per 8-lane group per shard
+    if (g > 96) g = 96;
   } else {
     g = (per + tile - 1) / tile;
     uint64_t cap = (uint64_t)default_max_ctas();
@@ -3528,8 +3748,9 @@ static int validate_bucket(const caramel_ctx* c, const caramel_bucket* b) {
   if (b->ctas < 1) return set_err(CARAMEL_EINVAL, "ctas must be >= 1 (see caramel_bucket_layout)");
   if (b->bucket_off & 15) return set_err(CARAMEL_EINVAL, "bucket_off must be 16-byte aligned");
   if (b->numel == 0) return 0;
-  const uint64_t span = use_ll(b->pattern, c->world, b->numel)
-                            ? ll_region_bytes(b->numel, c->world)
+  const uint64_t span = use_ll(b->pattern, c->world, b->numel) ? ll_region_bytes(b->numel, c->world)
+                        : use_ll128(b->pattern, c->world, b->numel)
+                            ? ll128_region_bytes(b->numel, c->world)
                             : 4 * ((c->world > 1 && b->pattern != CARAMEL_SHUFFLE) ? 2 * out_region_elems(b->numel)
                                                                                    : b->numel);
   const int proto = shuffle_proto(*b, c->world);

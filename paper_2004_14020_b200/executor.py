@@ -357,9 +357,12 @@ class Aggregator:
         """Aggregate every bucket now, in launch order, on `stream` (default:
         the current stream): one launch for the whole list (fused=True) or one
         launch per bucket.  Graph-capturable: epochs come from the device
-        counter advanced first on the same stream."""
+        counter advanced first on the same stream -- except where the launch
+        needs none: the world = 1 update and the fused two-shot (its grid
+        barriers count launches themselves), one kernel per step instead of two."""
         s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
-        N.check(N.lib().caramel_epoch_advance(self.ctx._ctx, ctypes.c_void_p(s)))
+        if self._step_needs_epoch(fused):
+            N.check(N.lib().caramel_epoch_advance(self.ctx._ctx, ctypes.c_void_p(s)))
         if fused:
             self._launch_range(0, len(self._live), s, N.MANY_FUSED, 0)
         else:
@@ -426,8 +429,10 @@ class Aggregator:
         h2d, d2h = self._h2d, self._d2h
         pflat = self.ctx.arena_view(0, 0, self.plan.param_bytes // 4, param=True)
         h2d.wait_stream(cur)
-        N.check(N.lib().caramel_epoch_advance(self.ctx._ctx, ctypes.c_void_p(cur.cuda_stream)))
-        launches = 1
+        launches = 0
+        if self._step_needs_epoch(True):
+            N.check(N.lib().caramel_epoch_advance(self.ctx._ctx, ctypes.c_void_p(cur.cuda_stream)))
+            launches = 1
         for i, j in self.host_groups(group_bytes):
             a = self._live[i].spec.param_off // 4
             last = self._live[j - 1].spec
@@ -467,8 +472,10 @@ class Aggregator:
             self._d2h = torch.cuda.Stream(device=self.device)
         h2d, d2h = self._h2d, self._d2h
         h2d.wait_stream(cur)
-        N.check(N.lib().caramel_epoch_advance(self.ctx._ctx, ctypes.c_void_p(cur.cuda_stream)))
-        launches = 1
+        launches = 0
+        if self._step_needs_epoch(True):
+            N.check(N.lib().caramel_epoch_advance(self.ctx._ctx, ctypes.c_void_p(cur.cuda_stream)))
+            launches = 1
         for i, j in self.host_groups(group_bytes):
             members = [pid for lv in self._live[i:j] for pid in lv.members]
             with torch.cuda.stream(h2d):
@@ -496,8 +503,18 @@ class Aggregator:
             tma = tma and bool(flat_ok) and bool(d.flags & N.F_PARAM_ARENA) and d.epilogue == N.EPI_SGD
         return "k_local_flat_tma" if tma else "k_local_many"
 
+    def _step_needs_epoch(self, fused: bool) -> bool:
+        if not fused:
+            return True
+        if self.world == 1:
+            return False
+        # CARAMEL_FUSED_PUSH routes fused lists to the push engine, whose flags carry epochs
+        return not (self.plan.pattern == N.SHUFFLE and not os.environ.get("CARAMEL_FUSED_PUSH"))
+
     def kernels_per_step(self, fused: bool = True) -> int:
-        return 2 if fused else 1 + len(self._live)
+        if fused:
+            return 1 + int(self._step_needs_epoch(True))
+        return 1 + len(self._live)
 
     # -- overlapped mode: launch when the last gradient of a bucket is ready ----
     def attach_hooks(self) -> None:

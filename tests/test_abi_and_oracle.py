@@ -78,13 +78,19 @@ def test_chunk_rule_agrees_with_reference_float_bytes():
 
 def test_bucket_layout_and_errors():
     N = _lib()
-    ctas, bb, fb = N.bucket_layout(1 << 20, 2, N.SHUFFLE, 8)
+    n = 4 << 20  # above the LL128 cutoff: the plain two-shot region
+    ctas, bb, fb = N.bucket_layout(n, 2, N.SHUFFLE, 8)
     # packed bucket + 7 copy-engine staging slots of ceil(n/8)+3 elements (the
     # push engine's inbox region is only laid out with CARAMEL_PUSH=1)
-    slot = (4 * ((1 << 20) // 8 + 3) + 15) & ~15
-    assert 1 <= ctas <= 64 and bb == (4 << 20) + 7 * slot and fb > 0
+    slot = (4 * (n // 8 + 3) + 15) & ~15
+    assert 1 <= ctas <= 64 and bb == 4 * n + 7 * slot and fb > 0
     ll = (4 * 1000 + 8 * 1000 * 9 + 255) // 256 * 256  # LL region: bucket + out + 8 in-slots of 8 B words
     assert N.bucket_layout(1000, 1, N.SHUFFLE, 8)[1] == ll + 7 * ((4 * (125 + 3) + 15) & ~15)
+    # LL128 (64K < n <= 512K elements): bucket, then out + 8 in-slots of 128 B lines of 30 floats
+    m = 1 << 19
+    lines = (m + 29) // 30
+    ll128 = ((4 * m + 127) // 128 * 128 + 128 * lines * 9 + 255) // 256 * 256
+    assert N.bucket_layout(m, 2, N.SHUFFLE, 8)[1] == ll128 + 7 * ((4 * (m // 8 + 3) + 15) & ~15)
     assert N.bucket_layout(1 << 20, 2, N.SHUFFLE, 1)[1] == 4 << 20  # one rank: no staging
     _, bb_ring, _ = N.bucket_layout(1 << 20, 2, N.RING, 8)
     assert bb_ring == 8 << 20  # input + output halves
@@ -192,12 +198,13 @@ def test_push_engine_layout_adds_the_inbox_region(tmp_path):
     import sys
 
     code = ("import sys; sys.path.insert(0, %r); from paper_2004_14020_b200 import _native as N; "
-            "print(N.bucket_layout(1 << 20, 2, N.SHUFFLE, 8)[1])" % str(ROOT))
+            "print(N.bucket_layout(4 << 20, 2, N.SHUFFLE, 8)[1])" % str(ROOT))
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
                          env={**__import__("os").environ, "CARAMEL_PUSH": "1"}, check=True).stdout
-    slot = (4 * ((1 << 20) // 8 + 3) + 15) & ~15
-    push = 256 + 2 * 16 * 2 * 8 * 4 + 2 * 7 * (4 << 20)
-    assert int(out) == (4 << 20) + push + 7 * slot
+    n = 4 << 20
+    slot = (4 * (n // 8 + 3) + 15) & ~15
+    push = 256 + 2 * 64 * 2 * 8 * 4 + 2 * 7 * (4 * n)  # 2 chunks x 64 ranges of 128 KB
+    assert int(out) == 4 * n + push + 7 * slot
 
 
 def test_lean_shuffle_oracle_equals_the_chunked_restatement():

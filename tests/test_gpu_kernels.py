@@ -314,3 +314,22 @@ def test_many_buckets_unpack_modes(epi):
     N, _ = _native()
     run_emulated_many(N.SHUFFLE, 4, MANY_BUCKETS, MANY_DEPTHS, epi, param_arena=False)
     run_emulated_many(N.SHUFFLE, 1, MANY_BUCKETS, MANY_DEPTHS, epi, param_arena=False)
+
+
+# 64K < n <= 512K elements: the LL128 protocol (128-byte lines: 30 floats + an epoch flag)
+SHAPES_LL128 = [(3, 33331), (7,), (1,), (250, 401)]      # 200,107 elements: a ragged last line
+SHAPES_LL128_EDGE = [(1 << 19,)]                          # exactly the LL128 cutoff
+
+
+@pytest.mark.parametrize("p", [2, 3, 5, 8])
+def test_ll128_bitexact(p):
+    N, _ = _native()
+    assert_bitexact(run_emulated(N.SHUFFLE, p, 2, SHAPES_LL128, N.EPI_SGD, epochs=3))
+    assert_bitexact(run_emulated(N.SHUFFLE, p, 1, SHAPES_LL128, N.EPI_SUM, misalign=True, epochs=2))
+
+
+@pytest.mark.parametrize("p", [2, 4])
+def test_ll128_cutoff_and_param_arena(p):
+    N, _ = _native()
+    assert_bitexact(run_emulated(N.SHUFFLE, p, 1, SHAPES_LL128_EDGE, N.EPI_SGD, param_arena=True, epochs=2))
+    assert_bitexact(run_emulated(N.SHUFFLE, p, 3, SHAPES_LL128_EDGE, N.EPI_SCALE, unpack=False))
