@@ -1159,9 +1159,11 @@ __device__ __forceinline__ void make_run(BucketRun& R, const Env& E, const caram
   R.arena = (B.flags & CARAMEL_F_PARAM_ARENA) && B.epilogue == CARAMEL_EPI_SGD;
   // Two-shot (not LL): chunk c's shard s is owned by rank s whatever the CTA,
   // so every CTA takes its tile of every chunk and reduces them in ONE flat
-  // loop (rs_ag_multi) behind one fence; the per-(chunk, tile) flags keep the
-  // plan's split.  Round 1 gave each chunk its own CTA group, which made a
-  // deeper split slower (4 MiB: depth 8 = 55.6 us, depth 1 = 26.6 us).
+  // loop (rs_ag_multi); the chunks are an ownership map, and since every
+  // consumer waits for all of its chunks anyway, ONE flag per (tile, rank)
+  // (chunk 0's slot) synchronises them all.  Per-chunk flags on a flat pass
+  // cost 4-13% at depth 3-8 (more flag traffic per CTA); chunk-parallel CTA
+  // groups (round 1) cost up to 2x.
   R.flat = pattern == CARAMEL_SHUFFLE && !use_ll(pattern, E.world, B.numel);
   // shuffle all-gathers in place; ring/hd write results to a second region
   // of the bucket so a fast neighbour never overwrites a partial sum that a
@@ -1207,12 +1209,13 @@ __device__ void phase_pack(const BucketRun& R) {
       }
     }
     if (PAT == CARAMEL_SHUFFLE) {
-      if (!DEFER) R.X.publish_all(c, SLOT_READY);
+      if (!DEFER && !R.flat) R.X.publish_all(c, SLOT_READY);
     } else {
       int t = (PAT == CARAMEL_RING) ? (me + 1) % p : (me ^ (p >> 1));
       R.X.publish(c, SLOT_READY, &t, 1);
     }
   }
+  if (PAT == CARAMEL_SHUFFLE && !DEFER && R.flat) R.X.publish_all(0, SLOT_READY);  // one READY for all chunks
 }
 
 // Reduce + epilogue + all-gather of several ranges (this CTA's tile of my
@@ -1255,14 +1258,16 @@ __device__ void rs_ag_multi(const Env& E, const caramel_bucket& B, bool arena, C
     }
   }
   const uint64_t V = vpre[nr], T = blockDim.x;
-  auto pos = [&](uint64_t v) {  // flat vector index -> bucket element position
-    int k = 0;
+  // flat vector index -> bucket element position; v only grows, so each of
+  // the two streams keeps its own range cursor (no rescan per vector)
+  int k0 = 0, k1 = 0;
+  auto pos = [&](uint64_t v, int& k) {
     while (v >= vpre[k + 1]) ++k;
     return va[k] + 4 * (v - vpre[k]);
   };
   uint64_t v = threadIdx.x;
   for (; v + T < V; v += 2 * T) {
-    const uint64_t x0 = pos(v), x1 = pos(v + T);
+    const uint64_t x0 = pos(v, k0), x1 = pos(v + T, k1);
     float4 p0[NP], p1[NP];
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
@@ -1288,7 +1293,7 @@ __device__ void rs_ag_multi(const Env& E, const caramel_bucket& B, bool arena, C
     }
   }
   if (v < V) {
-    const uint64_t x0 = pos(v);
+    const uint64_t x0 = pos(v, k0);
     float4 s0 = ld4(src[0] + x0);
 #pragma unroll
     for (int q = 1; q < NP; ++q) s0 = add4(s0, ld4(src[q] + x0));
@@ -1307,16 +1312,18 @@ template <int NP, bool DEFER = false>
 __device__ void phase_shuffle(const BucketRun& R) {
   Cursor tc;
   cur_init(tc, R.segs, R.B->nseg);
-  if (DEFER) {
+  if (DEFER || R.flat) {
     uint64_t lo[CARAMEL_MAX_DEPTH], hi[CARAMEL_MAX_DEPTH];
     int nr = 0;
+    if (R.flat) R.X.wait_all(0, SLOT_READY, R.X.epoch);  // one READY covers every chunk
     for (int c = 0; c < R.B->depth; ++c) {
       if (!R.mine(c)) continue;
-      R.X.wait_all(c, SLOT_READY, R.X.epoch);
+      if (!R.flat) R.X.wait_all(c, SLOT_READY, R.X.epoch);
       R.shard(c, R.X.me, lo[nr], hi[nr]);
       ++nr;
     }
     rs_ag_multi<NP>(*R.E, *R.B, R.arena, tc, lo, hi, nr, R.X.me);
+    if (!DEFER) R.X.publish_all(0, SLOT_DONE);  // flat, per-bucket list: DONE right away
     return;
   }
   for (int c = 0; c < R.B->depth; ++c) {
@@ -1732,7 +1739,7 @@ template <int PAT>
 __device__ void phase_finish(const BucketRun& R) {
   const int me = R.X.me, p = R.X.world;
   if (PAT == CARAMEL_SHUFFLE)
-    for (int c = 0; c < R.B->depth; ++c)
+    for (int c = 0; c < (R.flat ? 1 : R.B->depth); ++c)
       if (R.mine(c)) R.X.wait_all(c, SLOT_DONE, R.X.epoch);
   if ((R.B->flags & CARAMEL_F_UNPACK) && !R.arena) {
     const bool to_param = (R.B->epilogue == CARAMEL_EPI_SGD);
@@ -1765,7 +1772,7 @@ __device__ __forceinline__ void publish_chunks(const BucketRun& R, int slot) {
   if (threadIdx.x < 32) {
     fence_acq_rel_sys();
     const int p = R.X.world;
-    for (int idx = threadIdx.x; idx < R.B->depth * p; idx += 32)
+    for (int idx = threadIdx.x; idx < (R.flat ? 1 : R.B->depth) * p; idx += 32)
       if (R.mine(idx / p)) st_relaxed_sys(R.X.flag(idx % p, idx / p, slot, R.X.me), R.X.epoch);
   }
 }
@@ -2563,7 +2570,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_collective_many(const __grid_con
           const int ns = nslots(PAT, p);
           BucketRun R;
           make_run(R, E, B, PAT, lr_idx, epoch, j);
-          for (int idx = threadIdx.x; idx < B.depth * p; idx += 32) {
+          for (int idx = threadIdx.x; idx < (R.flat ? 1 : B.depth) * p; idx += 32) {
             const int c = idx / p, q = idx % p;
             if (!R.mine(c)) continue;
             uint32_t* f = reinterpret_cast<uint32_t*>(E.arena[q] + B.flag_off) +

@@ -120,9 +120,9 @@ def test_step_host_pipelined_matches_sgd():
     theta0 = {k: v.detach().cpu().clone() for k, v in params.items()}
     host_g = {k: torch.randn(v.numel()).pin_memory() for k, v in params.items()}
     host_p = {k: torch.empty(v.numel()).pin_memory() for k, v in params.items()}
-    n = agg.step_host(host_g, host_p, group_bytes=4096)  # several groups
+    n = agg.step_host(host_g, host_p, group_bytes=4096)  # several groups, one launch each
     torch.cuda.synchronize()
-    assert n >= 3
+    assert n >= 2
     for k in params:
         want = theta0[k].view(-1) - lr * host_g[k]
         assert torch.equal(host_p[k], want), k
