@@ -1157,14 +1157,12 @@ __device__ __forceinline__ void make_run(BucketRun& R, const Env& E, const caram
   R.tab = &g_tab;
   R.lr_idx = lr_idx;
   R.arena = (B.flags & CARAMEL_F_PARAM_ARENA) && B.epilogue == CARAMEL_EPI_SGD;
-  // Two-shot (not LL): chunk c's shard s is owned by rank s whatever the CTA,
-  // so every CTA takes its tile of every chunk and reduces them in ONE flat
-  // loop (rs_ag_multi); the chunks are an ownership map, and since every
-  // consumer waits for all of its chunks anyway, ONE flag per (tile, rank)
-  // (chunk 0's slot) synchronises them all.  Per-chunk flags on a flat pass
-  // cost 4-13% at depth 3-8 (more flag traffic per CTA); chunk-parallel CTA
-  // groups (round 1) cost up to 2x.
-  R.flat = pattern == CARAMEL_SHUFFLE && !use_ll(pattern, E.world, B.numel);
+  // One flat pass over every chunk (each CTA its tile of all chunks, one flag
+  // per tile) was measured against chunk-parallel CTA groups (each CTA one
+  // chunk's tile, per-chunk flags): the groups won at every depth > 1 (p=2,
+  // 16 MiB depth 3: 44.3 vs 51.6 us; 256 MiB depth 8: 416 vs 481 us; depth 1
+  // is identical), so the flat mode stays off; it remains for experiments.
+  R.flat = false;
   // shuffle all-gathers in place; ring/hd write results to a second region
   // of the bucket so a fast neighbour never overwrites a partial sum that a
   // slower one has yet to pull
