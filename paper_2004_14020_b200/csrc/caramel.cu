@@ -3119,6 +3119,7 @@ struct NvlsParams {
   caramel_bucket b;
   uint64_t mc;   // multicast address of the NVLS arena
   uint64_t uc;   // this rank's unicast view of it
+  int probe;     // diagnostics only (CARAMEL_NVLS_PROBE): 1 = in-switch reduce, unicast store; 2 = unicast load, multicast store
 };
 
 __device__ __forceinline__ float4 mc_ld_reduce4(const float* a) {
@@ -3178,6 +3179,23 @@ __global__ void __launch_bounds__(THREADS, 1) k_nvls(const __grid_constant__ Nvl
     constexpr int U = 8;  // switch round trips in flight per thread
     const uint64_t T = 4ull * blockDim.x;
     uint64_t v = a + 4ull * threadIdx.x;
+    if (P.probe == 1) {  // diagnostics: the switch's reduce alone
+      for (; v + (U - 1) * T < b; v += U * T) {
+        float4 s[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) s[u] = mc_ld_reduce4(mcb + v + u * T);
+#pragma unroll
+        for (int u = 0; u < U; ++u) st4(ucb + v + u * T, s[u]);
+      }
+    } else if (P.probe == 2) {  // diagnostics: the switch's broadcast alone
+      for (; v + (U - 1) * T < b; v += U * T) {
+        float4 s[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) s[u] = ld4(ucb + v + u * T);
+#pragma unroll
+        for (int u = 0; u < U; ++u) mc_st4(mcb + v + u * T, s[u]);
+      }
+    }
     for (; v + (U - 1) * T < b; v += U * T) {
       float4 s[U];
 #pragma unroll
@@ -4645,6 +4663,9 @@ int caramel_allreduce_nvls(caramel_ctx* c, const caramel_bucket* b, uint32_t epo
   P.b = *b;
   P.mc = c->mc_va;
   P.uc = c->uc_va;
+  static int probe = -1;
+  if (probe < 0) probe = getenv("CARAMEL_NVLS_PROBE") ? atoi(getenv("CARAMEL_NVLS_PROBE")) : 0;
+  P.probe = probe;
   k_nvls<<<b->ctas, THREADS, 0, (cudaStream_t)stream>>>(P);
   CUDA_TRY(cudaGetLastError());
   return 0;

@@ -1,8 +1,9 @@
 #!/bin/bash
 export PYTHONUNBUFFERED=1
 mkdir -p gpurun_out
-for g in 4 8 16 32; do
-CARAMEL_E2E_GROUP_MB=$g timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-exposed > gpurun_out/e2e_g$g.json 2>gpurun_out/e2e_g$g.err; echo "g=$g rc=$?"
+for probe in 0 1 2; do
+CARAMEL_NVLS_PROBE=$probe SWEEP_MAX=$((1<<30)) SWEEP_ENGINES=nvls timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+    --master-addr 127.0.0.1 --master-port 2951$probe tools/sweep.py > gpurun_out/sweep_nvls_probe$probe.jsonl 2> gpurun_out/sweep_nvls_probe$probe.err
+echo "probe $probe rc=$?"
 done
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1; echo "smoke rc=$?"
 echo done

@@ -48,6 +48,8 @@ def main():
                 ctas, bbytes, fbytes = N.bucket_layout(n, depth, pat, world)
                 if os.environ.get("SWEEP_CTAS"):
                     ctas = min(ctas, int(os.environ["SWEEP_CTAS"]))
+                if engine == "nvls":  # switch round trips only: the whole GPU
+                    ctas = int(max(1, min(int(os.environ.get("SWEEP_NVLS_CTAS", 148)), n // world // 2048)))
                 foff = region
                 b = comm.make_bucket(n, 0, foff, depth=depth, pattern=pat, epilogue=N.EPI_SUM, flags=0, ctas=ctas)
                 key = (engine, pat, depth, ctas)
