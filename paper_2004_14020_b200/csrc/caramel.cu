@@ -1222,7 +1222,7 @@ __device__ void phase_pack(const BucketRun& R) {
 // ranges).  Scalar heads/tails first.
 template <int NP>
 __device__ void rs_ag_multi(const Env& E, const caramel_bucket& B, bool arena, Cursor& tc, const uint64_t* lo,
-                            const uint64_t* hi, int nr, int me) {
+                            const uint64_t* hi, int nr, int me, int cj = 0, int cg = 1) {
   const float* src[NP];
   float* dst[NP];
 #pragma unroll
@@ -1242,8 +1242,8 @@ __device__ void rs_ag_multi(const Env& E, const caramel_bucket& B, bool arena, C
     if (b < a) b = a;
     va[k] = a;
     vpre[k + 1] = vpre[k] + (b - a) / 4;
-    // scalar head [lo, a) and tail [b, hi)
-    const uint64_t nh = a - lo[k], nt = hi[k] - b;
+    // scalar head [lo, a) and tail [b, hi) (one CTA of the group)
+    const uint64_t nh = cj == 0 ? a - lo[k] : 0, nt = cj == 0 ? hi[k] - b : 0;
     for (uint64_t e = threadIdx.x; e < nh + nt; e += blockDim.x) {
       const uint64_t x = e < nh ? lo[k] + e : b + (e - nh);
       float acc = ld1(src[0] + x);
@@ -1257,49 +1257,42 @@ __device__ void rs_ag_multi(const Env& E, const caramel_bucket& B, bool arena, C
   }
   const uint64_t V = vpre[nr], T = blockDim.x;
   // flat vector index -> bucket element position; v only grows, so each of
-  // the two streams keeps its own range cursor (no rescan per vector)
-  int k0 = 0, k1 = 0;
+  // the U streams keeps its own range cursor (no rescan per vector)
+  constexpr int U = NP <= 2 ? 4 : 2;  // U x NP 128-bit loads in flight per thread (8 at p = 2, as the fused kernel)
+  int kc[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) kc[u] = 0;
   auto pos = [&](uint64_t v, int& k) {
     while (v >= vpre[k + 1]) ++k;
     return va[k] + 4 * (v - vpre[k]);
   };
-  uint64_t v = threadIdx.x;
-  for (; v + T < V; v += 2 * T) {
-    const uint64_t x0 = pos(v, k0), x1 = pos(v + T, k1);
-    float4 p0[NP], p1[NP];
+  // rows of U*T vectors, row r to CTA r mod cg of the group (cg == 1: the
+  // whole range is this CTA's): the group sweeps the range together
+  const uint64_t ROW = (uint64_t)U * T;
+  for (uint64_t r = cj; r * ROW < V; r += cg) {
+    uint64_t x[U];
+    bool ok[U];
+    float4 pv[U][NP], tv[U];
 #pragma unroll
-    for (int q = 0; q < NP; ++q) {
-      p0[q] = ld4(src[q] + x0);
-      p1[q] = ld4(src[q] + x1);
+    for (int u = 0; u < U; ++u) {
+      const uint64_t v = r * ROW + u * T + threadIdx.x;
+      ok[u] = v < V;
+      x[u] = ok[u] ? pos(v, kc[u]) : 0;
+#pragma unroll
+      for (int q = 0; q < NP; ++q) pv[u][q] = ok[u] ? ld4(src[q] + x[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      tv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (sgd && ok[u]) tv[u] = arena ? ld4(th + x[u]) : seg_ld4(tc, x[u], 1);
     }
-    float4 t0 = make_float4(0.f, 0.f, 0.f, 0.f), t1 = t0;
-    if (sgd) {
-      t0 = arena ? ld4(th + x0) : seg_ld4(tc, x0, 1);
-      t1 = arena ? ld4(th + x1) : seg_ld4(tc, x1, 1);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!ok[u]) continue;
+      float4 sum = pv[u][0];
+#pragma unroll
+      for (int q = 1; q < NP; ++q) sum = add4(sum, pv[u][q]);
+      const float4 o = epi4(epi, sum, tv[u], B.scale, B.lr);
+#pragma unroll
+      for (int q = 0; q < NP; ++q) st4(dst[q] + x[u], o);
     }
-    float4 s0 = p0[0], s1 = p1[0];
-#pragma unroll
-    for (int q = 1; q < NP; ++q) {
-      s0 = add4(s0, p0[q]);
-      s1 = add4(s1, p1[q]);
-    }
-    const float4 o0 = epi4(epi, s0, t0, B.scale, B.lr), o1 = epi4(epi, s1, t1, B.scale, B.lr);
-#pragma unroll
-    for (int q = 0; q < NP; ++q) {
-      st4(dst[q] + x0, o0);
-      st4(dst[q] + x1, o1);
-    }
-  }
-  if (v < V) {
-    const uint64_t x0 = pos(v, k0);
-    float4 s0 = ld4(src[0] + x0);
-#pragma unroll
-    for (int q = 1; q < NP; ++q) s0 = add4(s0, ld4(src[q] + x0));
-    float4 t0 = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (sgd) t0 = arena ? ld4(th + x0) : seg_ld4(tc, x0, 1);
-    const float4 o0 = epi4(epi, s0, t0, B.scale, B.lr);
-#pragma unroll
-    for (int q = 0; q < NP; ++q) st4(dst[q] + x0, o0);
   }
 }
 
@@ -1310,17 +1303,31 @@ template <int NP, bool DEFER = false>
 __device__ void phase_shuffle(const BucketRun& R) {
   Cursor tc;
   cur_init(tc, R.segs, R.B->nseg);
+  // Without PACK / UNPACK no tile of a CTA depends on another CTA's work (the
+  // gradients were complete before any rank launched): the chunk's CTA group
+  // sweeps its whole shard row-cyclically instead of one contiguous tile each
+  const bool cyclic = !(R.B->flags & (CARAMEL_F_PACK | CARAMEL_F_UNPACK));
+  auto range_of = [&](int c, uint64_t& lo, uint64_t& hi, int& cj, int& cg) {
+    if (cyclic) {
+      R.mine(c, cj, cg);
+      shard_bounds(R.B->numel, R.B->depth, R.X.world, c, R.X.me, lo, hi);
+    } else {
+      cj = 0;
+      cg = 1;
+      R.shard(c, R.X.me, lo, hi);
+    }
+  };
   if (DEFER || R.flat) {
     uint64_t lo[CARAMEL_MAX_DEPTH], hi[CARAMEL_MAX_DEPTH];
-    int nr = 0;
+    int nr = 0, cj = 0, cg = 1;
     if (R.flat) R.X.wait_all(0, SLOT_READY, R.X.epoch);  // one READY covers every chunk
     for (int c = 0; c < R.B->depth; ++c) {
       if (!R.mine(c)) continue;
       if (!R.flat) R.X.wait_all(c, SLOT_READY, R.X.epoch);
-      R.shard(c, R.X.me, lo[nr], hi[nr]);
+      range_of(c, lo[nr], hi[nr], cj, cg);
       ++nr;
     }
-    rs_ag_multi<NP>(*R.E, *R.B, R.arena, tc, lo, hi, nr, R.X.me);
+    rs_ag_multi<NP>(*R.E, *R.B, R.arena, tc, lo, hi, nr, R.X.me, cj, cg);
     if (!DEFER) R.X.publish_all(0, SLOT_DONE);  // flat, per-bucket list: DONE right away
     return;
   }
@@ -1328,8 +1335,9 @@ __device__ void phase_shuffle(const BucketRun& R) {
     if (!R.mine(c)) continue;
     R.X.wait_all(c, SLOT_READY, R.X.epoch);
     uint64_t lo, hi;
-    R.shard(c, R.X.me, lo, hi);
-    rs_ag_multi<NP>(*R.E, *R.B, R.arena, tc, &lo, &hi, 1, R.X.me);
+    int cj, cg;
+    range_of(c, lo, hi, cj, cg);
+    rs_ag_multi<NP>(*R.E, *R.B, R.arena, tc, &lo, &hi, 1, R.X.me, cj, cg);
     R.X.publish_all(c, SLOT_DONE);
   }
 }
@@ -3390,10 +3398,12 @@ static int validate_workers(int pattern, int world) {
   return 0;
 }
 
+// CTAs of a large two-shot bucket: its pull loop is latency-bound (a 1 GiB
+// bucket at p = 2: 64 CTAs 1758 us, 128 CTAs 1629 us, on the same box)
 static int default_max_ctas() {
   const char* e = getenv("CARAMEL_MAX_CTAS");
   if (e && atoi(e) > 0) return atoi(e);
-  return 64;
+  return 128;
 }
 
 // Bucket region: the kernels' part (packed bucket; LL region; ring/hd halves),

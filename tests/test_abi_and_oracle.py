@@ -83,7 +83,7 @@ def test_bucket_layout_and_errors():
     # packed bucket + 7 copy-engine staging slots of ceil(n/8)+3 elements (the
     # push engine's inbox region is only laid out with CARAMEL_PUSH=1)
     slot = (4 * (n // 8 + 3) + 15) & ~15
-    assert 1 <= ctas <= 64 and bb == 4 * n + 7 * slot and fb > 0
+    assert 1 <= ctas <= 128 and bb == 4 * n + 7 * slot and fb > 0
     ll = (4 * 1000 + 8 * 1000 * 9 + 255) // 256 * 256  # LL region: bucket + out + 8 in-slots of 8 B words
     assert N.bucket_layout(1000, 1, N.SHUFFLE, 8)[1] == ll + 7 * ((4 * (125 + 3) + 15) & ~15)
     # LL128 (64K < n <= 512K elements): bucket, then out + 8 in-slots of 128 B lines of 30 floats
