@@ -65,8 +65,10 @@ def parse_args():
     ap.add_argument("--exposed-iters", type=int, default=20)
     ap.add_argument("--exposed-grads", default="bucket", choices=["flat", "bucket"],
                     help="gradient storage of the overlapped Aggregator (bucket = zero-copy)")
-    ap.add_argument("--exposed-engine", default="both", choices=["sm", "ce", "both"],
-                    help="overlapped-path engine(s) measured; 'both' reports each and the faster")
+    ap.add_argument("--exposed-engine", default="all", choices=["sm", "ce", "gated", "all"],
+                    help="overlapped-path engine(s) measured; 'all' reports each and the fastest")
+    ap.add_argument("--comm-priority", type=int, default=None,
+                    help="CUDA priority of the overlapped comm stream (default: Aggregator.comm_priority)")
     ap.add_argument("--ce-min-mb", type=float, default=None,
                     help="copy-engine engine: buckets below this size use the SM kernels (default: Aggregator's)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the bucket-size sweep (N > 1)")
@@ -497,13 +499,15 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
     # zero-copy gradients, "ce" (copy-engine two-shot, no SM held while bytes
     # move); each measured in 3 rounds alternating with compute-only rounds
     # (clock / thermal drift hits both alike), medians over rounds
-    engines = ["sm"] + (["ce"] if world > 1 and args.exposed_grads == "bucket" else [])
-    if args.exposed_engine != "both":
+    engines = ["sm"] + (["gated", "ce"] if world > 1 and args.exposed_grads == "bucket" else [])
+    if args.exposed_engine != "all":
         engines = [args.exposed_engine]
     cs, per_engine, gated = [], {}, 0
 
     def run_engine(engine, cs, per_engine):
         nonlocal gated
+        if args.comm_priority is not None:
+            Aggregator.comm_priority = args.comm_priority
         agg = Aggregator(mplan, dict(ing.params), rank=rank, lr=LR, epilogue="sgd", grads=args.exposed_grads,
                          engine=engine)
         try:
@@ -549,7 +553,7 @@ def measure_exposed(args, plan, ids, world, rank, dev, dist, network=None):
     torch.cuda.empty_cache()
 
     nccl_ms = nccl_exp = None
-    if dist is not None:
+    if dist is not None and not args.no_nccl:
         from torch.nn.parallel import DistributedDataParallel as DDP
 
         m2 = make()
@@ -639,6 +643,11 @@ def bucket_sweep(torch, dist, world, rank, dev, iters=20, network=None):
         c.bootstrap()
         comm._view_fp32(c.arena_ptrs(0)[0], big // 4).normal_()
         ce_ctx["ce"], ce_epoch["ce"] = c, 0
+        # the gated SM engine (stream-front-end waits around a k_gated launch)
+        c = comm.Context(rank, world, arena_bytes=region + (32 << 20))
+        c.bootstrap()
+        comm._view_fp32(c.arena_ptrs(0)[0], big // 4).normal_()
+        ce_ctx["gated"], ce_epoch["gated"] = c, 0
     # the NVLS (multicast, in-switch reduction) two-shot: the non-fixed-order mode;
     # its CTAs only issue switch round trips, so it takes the whole GPU
     nvls_ok = ctx.nvls_available()
@@ -725,13 +734,15 @@ def bucket_sweep(torch, dist, world, rank, dev, iters=20, network=None):
                 fixed[str(d)] = round(timed(fixed_call)[0], 2)
             row["fixed_depth_us"] = fixed
         if size >= (1 << 20) and ce_ctx:
-            # the copy-engine two-shot (eager: its host-side tags cannot replay)
+            # the copy-engine two-shot and the gated SM engine (eager: their
+            # host-side tags cannot replay)
             for key, c in ce_ctx.items():
-                def ce_call(st=None, c=c):
+                fn = N.lib().caramel_allreduce_gated if key == "gated" else N.lib().caramel_allreduce_ce
+
+                def ce_call(st=None, c=c, key=key, fn=fn):
                     ce_epoch[key] += 1
-                    N.check(N.lib().caramel_allreduce_ce(c._ctx, ctypes.byref(b), 1, 0, ce_epoch[key],
-                                                         ctypes.c_void_p(stream.cuda_stream),
-                                                         ctypes.c_void_p(stream.cuda_stream)))
+                    N.check(fn(c._ctx, ctypes.byref(b), 1, 0, ce_epoch[key], ctypes.c_void_p(stream.cuda_stream),
+                               ctypes.c_void_p(stream.cuda_stream)))
                 us_e, _ = timed(ce_call, graphed=False)
                 row[f"{key}_us"] = round(us_e, 2)
                 row[f"{key}_bus_gbs"] = round(bus / us_e, 1)

@@ -224,17 +224,35 @@ int caramel_allreduce_many(caramel_ctx* ctx, const caramel_bucket* host, int32_t
  * memory operations (caramel_ce_available). */
 int caramel_allreduce_ce(caramel_ctx* ctx, const caramel_bucket* host, int32_t count,
                          uint32_t index0, uint32_t epoch, void* grad_stream, void* stream);
-/* 1 if caramel_allreduce_ce can run on this context, else 0. */
+/* 1 if caramel_allreduce_ce / caramel_allreduce_gated can run on this
+ * context, else 0. */
 int caramel_ce_available(caramel_ctx* ctx);
+/* The gated SM engine: the same two-shot as caramel_allreduce with every wait
+ * moved from the SMs to the stream front end.  READY (a 64-bit stream write
+ * of (epoch << 32 | index0 + count) into every peer, issued after
+ * `grad_stream`'s gradients), a stream wait on every peer's READY, one
+ * k_gated launch of at most CARAMEL_GATED_CTAS CTAs (default 32) that pulls
+ * my shard of every bucket from every rank, sums in ascending rank order,
+ * applies the epilogue and stores into every replica, then DONE and a stream
+ * wait on every peer's DONE.  No CTA spins on a peer, so while it overlaps a
+ * backward pass the kernel holds SMs only while bytes move.  Arguments,
+ * requirements, tags and results as caramel_allreduce_ce (the two engines
+ * share the READY / DONE words and may alternate in one launch order); no
+ * staging slots are used.  Replaces, like caramel_allreduce, the modelled
+ * collective of pipeline.py:94. */
+int caramel_allreduce_gated(caramel_ctx* ctx, const caramel_bucket* host, int32_t count,
+                            uint32_t index0, uint32_t epoch, void* grad_stream, void* stream);
 /* Engines of caramel_ce_submit. */
 #define CARAMEL_ENGINE_CE 0  /* caramel_allreduce_ce                                  */
 #define CARAMEL_ENGINE_SM 1  /* caramel_allreduce[_update] per bucket, epoch 0 (device counter) */
+#define CARAMEL_ENGINE_GATED 2  /* caramel_allreduce_gated                            */
 
 /* Asynchronous launch: validates, records "gradients ready" on grad_stream in
  * the caller's stream order, and hands the call to the context's worker
  * thread, which issues it on `stream` -- the calling thread (autograd's) pays
  * a few microseconds instead of the whole issue cost.  CARAMEL_ENGINE_CE
- * issues caramel_allreduce_ce(host, count, index0, epoch); CARAMEL_ENGINE_SM
+ * issues caramel_allreduce_ce(host, count, index0, epoch), CARAMEL_ENGINE_GATED
+ * caramel_allreduce_gated(host, count, index0, epoch); CARAMEL_ENGINE_SM
  * launches the SM kernel of each bucket with the device epoch counter
  * (caramel_epoch_advance on `stream` once per iteration).  Calls are issued in
  * submission order, so both engines can share `stream` in launch order.

@@ -19,7 +19,7 @@ RING, HD, SHUFFLE = 0, 1, 2
 EPI_SUM, EPI_SCALE, EPI_SGD = 0, 1, 2
 F_PACK, F_UNPACK, F_PARAM_ARENA, F_FLAT = 1, 2, 4, 8
 MANY_FUSED, MANY_FLAGS = 0, 1
-ENGINE_CE, ENGINE_SM = 0, 1
+ENGINE_CE, ENGINE_SM, ENGINE_GATED = 0, 1, 2
 MAX_RANKS = 8
 MAX_DEPTH = 8
 
@@ -102,6 +102,8 @@ SIGNATURES = {
                                               ctypes.c_int32, ctypes.c_uint32, ctypes.c_void_p]),
     "caramel_allreduce_ce": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Bucket), ctypes.c_int32,
                                             ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p]),
+    "caramel_allreduce_gated": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Bucket), ctypes.c_int32,
+                                               ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p]),
     "caramel_ce_available": (ctypes.c_int, [ctypes.c_void_p]),
     "caramel_ce_submit": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Bucket), ctypes.c_int32, ctypes.c_uint32,
                                          ctypes.c_uint32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,

@@ -1961,7 +1961,10 @@ __device__ void grid_barrier(const Env& E, int me, int k, uint32_t S) {
 // float4s per lane per item of the fused NVLink phase: about 8 loads in
 // flight per lane whatever p is (V * NP), at least 2
 template <int NP>
-struct FusedV { static constexpr int V = NP >= 4 ? 2 : 8 / NP; };
+#ifndef CARAMEL_FUSED_V2
+#define CARAMEL_FUSED_V2 4
+#endif
+struct FusedV { static constexpr int V = NP >= 4 ? 2 : NP == 2 ? CARAMEL_FUSED_V2 : 8 / NP; };
 
 // items of my shard range [lo, hi): one edge item (scalar head + tail) and
 // one per 32*V float4s of the 16-byte aligned interior
@@ -2364,10 +2367,19 @@ __global__ void __launch_bounds__(TMA_THREADS, 2) k_local_flat_tma(const __grid_
 // 53% DRAM throughput, 26.7 of 53.7 cycles per instruction on long scoreboard).
 // ---------------------------------------------------------------------------
 #define KT_THREADS 256
+#ifndef KT_TILE
 #define KT_TILE 8192                 // floats per tile (32 KB)
+#endif
+#ifndef KT_STAGES
 #define KT_STAGES 6                  // 4 tiles of loads in flight per SM (HBM latency x bandwidth / 148 SMs ~ 66 KB)
+#endif
+#ifndef KT_CTAS_PER_SM
+#define KT_CTAS_PER_SM 1
+#endif
 #define KT_MAXODD 32                 // misaligned pieces remembered per tile (more: the tile goes plain)
+#ifndef KT_MAXSEG
 #define KT_MAXSEG 512                // member tables up to this size are cached in shared memory
+#endif
 
 struct KtOdd { uint64_t src, dst; uint32_t n; };  // a misaligned piece: element addresses, count
 
@@ -2399,7 +2411,7 @@ __device__ __forceinline__ void kt_pieces(const caramel_segment* segs, int nseg,
 // UNPACK = false: members -> bucket.  UNPACK = true: bucket -> members
 // (to_param selects .param instead of .grad).
 template <bool UNPACK>
-__global__ void __launch_bounds__(KT_THREADS, 1) k_pack_tma(const caramel_segment* segs, int nseg, uint64_t numel,
+__global__ void __launch_bounds__(KT_THREADS, KT_CTAS_PER_SM) k_pack_tma(const caramel_segment* segs, int nseg, uint64_t numel,
                                                             float* bucket, int to_param) {
   extern __shared__ __align__(128) unsigned char dyn_smem[];
   KtSmem& S = *reinterpret_cast<KtSmem*>(dyn_smem);
@@ -2622,6 +2634,46 @@ __global__ void __launch_bounds__(THREADS, 1) k_collective_many(const __grid_con
       if (j < 0 || B.numel == 0) continue;
       run_bucket<PAT, NP>(E, B, lr_idx, epoch, j);
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Gated SM engine (CARAMEL_ENGINE_GATED): the two-shot over NVLink done by SM
+// kernels, every wait done by the stream front end.  The caller's stream
+// waits (cuStreamWaitValue64) until every peer has written its READY tag --
+// issued after its gradients, so all inputs are complete before a CTA is
+// scheduled -- then this kernel pulls my shard of every bucket from every
+// rank, sums in rank order, applies the epilogue and stores the result into
+// every replica; a stream write publishes DONE after the kernel and a stream
+// wait collects the peers' DONE.  No CTA ever spins on a peer, so the kernel
+// holds its SMs only while bytes move (the flag kernels may sit on up to 128
+// SMs while a peer is still in its backward pass).  Ownership is the depth-1
+// shard split (values are the same rank-order sums whoever owns them).
+#define GATED_MAX 32
+struct GParams {
+  Env env;
+  int nb;
+  caramel_bucket b[GATED_MAX];
+};
+
+template <int NP>
+__global__ void __launch_bounds__(THREADS, 1) k_gated(const __grid_constant__ GParams P) {
+  const Env E = P.env;
+  if (cta_poisoned(E)) return;
+  const int me = E.rank_base, G = gridDim.x;
+  constexpr int U = NP <= 2 ? 4 : 2;  // rs_ag_multi's row: U vectors per thread
+  const uint64_t row = 4ull * U * blockDim.x;
+  uint64_t rot = 0;  // the first row of bucket i goes to CTA rot mod G: small buckets spread over the grid
+  for (int i = 0; i < P.nb; ++i) {
+    const caramel_bucket& B = P.b[i];
+    uint64_t lo = split_at(B.numel, NP, me), hi = split_at(B.numel, NP, me + 1);
+    if (lo >= hi) continue;
+    const bool arena = (B.flags & CARAMEL_F_PARAM_ARENA) && B.epilogue == CARAMEL_EPI_SGD;
+    const int cj = (int)(((uint64_t)blockIdx.x + G - rot % G) % G);
+    Cursor tc;
+    cur_init(tc, reinterpret_cast<const caramel_segment*>(B.segs), B.nseg);
+    rs_ag_multi<NP>(E, B, arena, tc, &lo, &hi, 1, me, cj, G);
+    rot += (hi - lo + row - 1) / row;
   }
 }
 
@@ -3327,6 +3379,7 @@ struct caramel_ctx {
   uint32_t* epoch_dev;
   uint64_t timeout_ns;
   // copy-engine two-shot (caramel_allreduce_ce), created on first use
+  int gated_ctas;  // grid cap of a k_gated launch (CARAMEL_GATED_CTAS, default 32)
   bool ce_ready;
   cudaStream_t ce_send;  // reduce-scatter pushes + READY: never waits on a peer
   cudaEvent_t ce_grads;  // gradients produced (recorded on the caller's grad stream)
@@ -3484,6 +3537,10 @@ int caramel_init(int rank, int world, int nlocal, uint64_t arena_bytes, uint64_t
   c->param_bytes = param_arena_bytes ? (param_arena_bytes + G2 - 1) / G2 * G2 : 0;
   c->timeout_ns = 5ull * 1000 * 1000 * 1000;
   if (const char* e = getenv("CARAMEL_WATCHDOG_MS")) c->timeout_ns = strtoull(e, 0, 10) * 1000000ull;
+  c->gated_ctas = 32;
+  if (const char* e = getenv("CARAMEL_GATED_CTAS")) c->gated_ctas = atoi(e);
+  if (c->gated_ctas < 1) c->gated_ctas = 1;
+  if (c->gated_ctas > 148) c->gated_ctas = 148;
   int rc = 0;
   cudaError_t e;
   if ((e = cudaGetDevice(&c->device)) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "cudaGetDevice: %s", cudaGetErrorString(e)); goto fail; }
@@ -3664,7 +3721,8 @@ static int pack_tma(const caramel_segment* segs, int32_t nseg, uint64_t numel, f
     attr[unpack] = true;
   }
   const uint64_t tiles = (numel + KT_TILE - 1) / KT_TILE;
-  const int grid = (int)(tiles < (uint64_t)sms ? tiles : (uint64_t)sms);
+  const uint64_t slots = (uint64_t)sms * KT_CTAS_PER_SM;
+  const int grid = (int)(tiles < slots ? tiles : slots);
   fn<<<grid, KT_THREADS, sizeof(KtSmem), (cudaStream_t)stream>>>(segs, nseg, numel, bucket, to_param);
   CUDA_TRY(cudaGetLastError());
   return 0;
@@ -4203,7 +4261,10 @@ int caramel_ce_available(caramel_ctx* c) {
   return c && c->nlocal == 1 && c->world > 1 && ce_probe(c) ? 1 : 0;
 }
 
-static int ce_validate(caramel_ctx* c, const caramel_bucket* host, int32_t count, uint32_t epoch) {
+// staging: the copy engines' reduce-scatter slots must fit (CE); the gated
+// SM engine pulls straight from the peers' buckets and needs none
+static int ce_validate(caramel_ctx* c, const caramel_bucket* host, int32_t count, uint32_t epoch,
+                       bool staging = true) {
   if (!c || !host || count < 1) return set_err(CARAMEL_EINVAL, "allreduce_ce: null argument or empty list");
   if (c->nlocal != 1 || c->world < 2) return set_err(CARAMEL_ESTATE, "allreduce_ce: one rank per process, world >= 2");
   if (!c->imported) return set_err(CARAMEL_ESTATE, "peer arenas not mapped (call caramel_import)");
@@ -4223,7 +4284,7 @@ static int ce_validate(caramel_ctx* c, const caramel_bucket* host, int32_t count
     int rc = validate_bucket(c, &b);
     if (rc) return rc;
     const uint64_t end = b.bucket_off + ce_stage_off(b.numel, b.depth, CARAMEL_SHUFFLE, p) + (uint64_t)(p - 1) * ce_slot_bytes(b.numel, p);
-    if (b.numel && end > c->arena_bytes)
+    if (staging && b.numel && end > c->arena_bytes)
       return set_err(CARAMEL_EINVAL, "allreduce_ce: bucket + staging slots exceed the arena (size it with caramel_bucket_layout)");
   }
   return ce_setup(c);
@@ -4314,6 +4375,78 @@ static int ce_enqueue(caramel_ctx* c, const caramel_bucket* host, int32_t count,
   return 0;
 }
 
+typedef void (*gfn_t)(GParams);
+static gfn_t pick_gated(int world) {
+  switch (world) {
+    case 2: return k_gated<2>;
+    case 3: return k_gated<3>;
+    case 4: return k_gated<4>;
+    case 5: return k_gated<5>;
+    case 6: return k_gated<6>;
+    case 7: return k_gated<7>;
+    default: return k_gated<8>;
+  }
+}
+
+// CTAs of a gated launch: enough rows for every CTA, at most gated_ctas
+// (CARAMEL_GATED_CTAS, default 32 -- the rest of the GPU stays with the
+// backward pass the launch overlaps)
+static int gated_grid(const caramel_ctx* c, const caramel_bucket* b, int n) {
+  const int U = c->world <= 2 ? 4 : 2;
+  const uint64_t row = 4ull * U * THREADS;
+  uint64_t rows = 0;
+  for (int i = 0; i < n; ++i) rows += (b[i].numel / c->world + row) / row;
+  int cap = c->gated_ctas;
+  return (int)(rows < (uint64_t)cap ? (rows ? rows : 1) : cap);
+}
+
+// Gated SM engine: READY on the send stream after the gradients, wait for
+// every peer's READY on `s`, the k_gated launch(es), DONE, wait for every
+// peer's DONE.  Same READY / DONE words and tags as the copy-engine engine,
+// so calls of both engines can alternate in one launch order.
+static int gated_enqueue(caramel_ctx* c, const caramel_bucket* host, int32_t count, uint32_t index0,
+                         uint32_t epoch, cudaEvent_t grads, cudaStream_t s) {
+  const int me = c->rank, p = c->world;
+  const uint64_t tag = ((uint64_t)epoch << 32) | (uint64_t)(index0 + (uint32_t)count);
+  const uint64_t ready = c->arena_bytes + CE_FLAG_OFF, done = ready + 8 * MAXR;
+  uint64_t peer_ready[MAXR], my_ready[MAXR], peer_done[MAXR], my_done[MAXR];
+  int np_ = 0;
+  for (int q = 0; q < p; ++q) {
+    if (q == me) continue;
+    peer_ready[np_] = c->arena[q] + ready + 8 * me;
+    my_ready[np_] = c->arena[me] + ready + 8 * q;
+    peer_done[np_] = c->arena[q] + done + 8 * me;
+    my_done[np_] = c->arena[me] + done + 8 * q;
+    ++np_;
+  }
+  CUDA_TRY(cudaStreamWaitEvent(c->ce_send, grads, 0));
+  CU_TRY(ce_memops(c->ce_send, false, peer_ready, np_, tag));
+  CUDA_TRY(cudaStreamWaitEvent(s, grads, 0));
+  CU_TRY(ce_memops(s, true, my_ready, np_, tag));
+  const gfn_t fn = pick_gated(p);
+  for (int i0 = 0; i0 < count; i0 += GATED_MAX) {
+    GParams P;
+    memset(&P, 0, sizeof(P));
+    fill_env(c, P.env, 1);
+    P.nb = count - i0 < GATED_MAX ? count - i0 : GATED_MAX;
+    for (int i = 0; i < P.nb; ++i) P.b[i] = host[i0 + i];
+    fn<<<gated_grid(c, P.b, P.nb), THREADS, 0, s>>>(P);
+    CUDA_TRY(cudaGetLastError());
+  }
+  CU_TRY(ce_memops(s, false, peer_done, np_, tag));
+  CU_TRY(ce_memops(s, true, my_done, np_, tag));
+  return 0;
+}
+
+int caramel_allreduce_gated(caramel_ctx* c, const caramel_bucket* host, int32_t count, uint32_t index0,
+                            uint32_t epoch, void* grad_stream, void* stream) {
+  int rc = ce_validate(c, host, count, epoch, false);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaEventRecord(c->ce_grads, grad_stream ? (cudaStream_t)grad_stream : s));
+  return gated_enqueue(c, host, count, index0, epoch, c->ce_grads, s);
+}
+
 int caramel_allreduce_ce(caramel_ctx* c, const caramel_bucket* host, int32_t count, uint32_t index0,
                          uint32_t epoch, void* grad_stream, void* stream) {
   int rc = ce_validate(c, host, count, epoch);
@@ -4339,6 +4472,9 @@ static void ce_worker_main(caramel_ctx* c) {
       if (job.engine == CARAMEL_ENGINE_CE) {
         rc = ce_enqueue(c, job.buckets.data(), (int32_t)job.buckets.size(), job.index0, job.epoch, job.grads,
                         job.stream);
+      } else if (job.engine == CARAMEL_ENGINE_GATED) {
+        rc = gated_enqueue(c, job.buckets.data(), (int32_t)job.buckets.size(), job.index0, job.epoch, job.grads,
+                           job.stream);
       } else {  // the SM kernels, one launch per bucket, device epoch counter
         cudaError_t e = cudaStreamWaitEvent(job.stream, job.grads, 0);
         if (e != cudaSuccess) rc = set_err(CARAMEL_ECUDA, "cudaStreamWaitEvent: %s", cudaGetErrorString(e));
@@ -4362,11 +4498,11 @@ static void ce_worker_main(caramel_ctx* c) {
 
 int caramel_ce_submit(caramel_ctx* c, const caramel_bucket* host, int32_t count, uint32_t index0, uint32_t epoch,
                       int32_t engine, void* grad_stream, void* stream, void* done_event) {
-  if (engine != CARAMEL_ENGINE_CE && engine != CARAMEL_ENGINE_SM)
+  if (engine != CARAMEL_ENGINE_CE && engine != CARAMEL_ENGINE_SM && engine != CARAMEL_ENGINE_GATED)
     return set_err(CARAMEL_EINVAL, "ce_submit: unknown engine %d", engine);
   int rc = 0;
-  if (engine == CARAMEL_ENGINE_CE) {
-    rc = ce_validate(c, host, count, epoch);
+  if (engine == CARAMEL_ENGINE_CE || engine == CARAMEL_ENGINE_GATED) {
+    rc = ce_validate(c, host, count, epoch, engine == CARAMEL_ENGINE_CE);
   } else {
     if (!c || !host || count < 1) return set_err(CARAMEL_EINVAL, "ce_submit: null argument or empty list");
     if (!c->imported) return set_err(CARAMEL_ESTATE, "peer arenas not mapped (call caramel_import)");

@@ -189,16 +189,20 @@ class Aggregator:
                ranks wait on stream memory operations, so the backward kernels
                keep every SM; buckets under `ce_min_bytes` still take the SM
                kernels.  Needs grads="bucket", world > 1, SHUFFLE.
+               "gated": the NVLink SM kernels with every wait on the stream
+               front end (caramel_allreduce_gated): the kernel is scheduled
+               only once every peer's gradients are ready, so it never holds
+               an SM while waiting; same requirements as "ce".
                step() / step_host*() always use the SM kernels.
     """
 
     def __init__(self, plan: ExecPlan, params: dict[str, torch.Tensor], *, rank: int = 0, lr: float = 0.01,
                  epilogue: str = "sgd", param_arena: bool = True, grads: str = "bucket", group=None,
                  bootstrap: bool = True, engine: str = "auto"):
-        if engine not in ("auto", "sm", "ce"):
-            raise ValueError("engine must be 'auto', 'sm' or 'ce'")
-        if engine == "ce" and (grads != "bucket" or plan.world < 2 or plan.pattern != N.SHUFFLE):
-            raise ValueError("engine='ce' needs grads='bucket', world > 1 and the SHUFFLE pattern")
+        if engine not in ("auto", "sm", "ce", "gated"):
+            raise ValueError("engine must be 'auto', 'sm', 'ce' or 'gated'")
+        if engine in ("ce", "gated") and (grads != "bucket" or plan.world < 2 or plan.pattern != N.SHUFFLE):
+            raise ValueError(f"engine={engine!r} needs grads='bucket', world > 1 and the SHUFFLE pattern")
         self.engine = engine
         self.plan = plan
         self.rank, self.world = rank, plan.world
@@ -215,10 +219,10 @@ class Aggregator:
         if self.world > 1 and bootstrap:
             agree("execution plan", plan.digest(), self.world, group)
             self.ctx.bootstrap(group)
-        if engine == "ce" and not N.lib().caramel_ce_available(self.ctx._ctx):
-            raise RuntimeError("engine='ce': this device lacks 64-bit stream memory operations")
-        if engine == "ce" and not ce_connections_ok():
-            raise RuntimeError(f"engine='ce' needs CUDA_DEVICE_MAX_CONNECTIONS >= {CE_MIN_CONNECTIONS} in the "
+        if engine in ("ce", "gated") and not N.lib().caramel_ce_available(self.ctx._ctx):
+            raise RuntimeError(f"engine={engine!r}: this device lacks 64-bit stream memory operations")
+        if engine in ("ce", "gated") and not ce_connections_ok():
+            raise RuntimeError(f"engine={engine!r} needs CUDA_DEVICE_MAX_CONNECTIONS >= {CE_MIN_CONNECTIONS} in the "
                                "environment before CUDA initialises: a stream-memory-op wait stalls its hardware "
                                "queue, and with shared queues it can stall the backward pass behind a peer")
         if engine == "auto":
@@ -260,13 +264,13 @@ class Aggregator:
         for p in params.values():
             if p.grad is None:
                 p.grad = torch.zeros_like(p)
-        self.comm_stream = torch.cuda.Stream(device=dev)
+        self.comm_stream = torch.cuda.Stream(device=dev, priority=self.comm_priority)
         self._live = [self._make_live(b) for b in plan.buckets]
         self._by_param = {}
         for lv in self._live:
             for pid in lv.members:
                 self._by_param[pid] = lv
-        if self.engine == "ce":
+        if self.engine in ("ce", "gated"):
             for lv in self._live:  # materialised now, recorded by the worker thread later
                 lv.ce_done = torch.cuda.Event()
                 lv.ce_done.record(self.comm_stream)
@@ -300,7 +304,7 @@ class Aggregator:
             # zero-copy: the bucket IS the gradient storage; results land in the
             # parameter arena (SGD) or in place (mean / sum; ring/hd unpack)
             flags = N.F_PARAM_ARENA if self.param_arena else N.F_UNPACK
-            if self.engine == "ce" and not self.param_arena:
+            if self.engine in ("ce", "gated") and not self.param_arena:
                 flags = 0  # the copy-engine all-gather lands in the bucket = the gradients
         else:
             flags = N.F_PACK | (N.F_PARAM_ARENA if self.param_arena else N.F_UNPACK)
@@ -548,6 +552,10 @@ class Aggregator:
                                               ctypes.c_void_p(self.comm_stream.cuda_stream)))
         self._ce_epoch += 1
 
+    #: CUDA priority of the comm stream (lower = higher; torch clamps to the
+    #: device's range): a high-priority stream's CTAs are scheduled ahead of
+    #: queued backward CTAs as SMs free up
+    comm_priority = 0
     #: overlapped mode: while the comm stream is busy, ready buckets are held
     #: back and coalesced into one list launch (per-bucket flags, so ranks may
     #: group differently) until this many are pending or this many bytes
@@ -573,7 +581,7 @@ class Aggregator:
         if j == self._next:
             return
         pending_bytes = 4 * (self._prefix[j] - self._prefix[self._next])
-        if self.engine == "ce":
+        if self.engine in ("ce", "gated"):
             self._drain_ce(j)
             return
         if not force and self._comm_busy() and j - self._next < self.coalesce_buckets \
@@ -596,6 +604,8 @@ class Aggregator:
 
     def engine_assignment(self) -> list[str]:
         """Engine of every bucket in launch order (overlapped mode)."""
+        if self.engine == "gated":
+            return ["gated"] * len(self._live)
         if self.engine != "ce":
             return ["sm"] * len(self._live)
         return [self._ce_engine_of(k) for k in range(len(self._live))]
@@ -639,7 +649,10 @@ class Aggregator:
         bsz = ctypes.sizeof(N.Bucket)
         for k in range(self._next, j):
             lv = self._live[k]
-            eng = N.ENGINE_CE if self._ce_engine_of(k) == "ce" else N.ENGINE_SM
+            if self.engine == "gated":
+                eng = N.ENGINE_GATED
+            else:
+                eng = N.ENGINE_CE if self._ce_engine_of(k) == "ce" else N.ENGINE_SM
             host = ctypes.cast(ctypes.byref(self._host_list, k * bsz), ctypes.POINTER(N.Bucket))
             N.check(N.lib().caramel_ce_submit(self.ctx._ctx, host, 1, k, self._ce_epoch, eng, ctypes.c_void_p(cur),
                                               ctypes.c_void_p(s), ctypes.c_void_p(lv.ce_done.cuda_event)))
@@ -648,7 +661,7 @@ class Aggregator:
         self._next = j
 
     def _ce_flush(self) -> None:
-        if self.engine == "ce":
+        if self.engine in ("ce", "gated"):
             N.check(N.lib().caramel_ce_flush(self.ctx._ctx))
 
     def finish_iteration(self, postpone: bool = False) -> None:

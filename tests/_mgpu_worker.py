@@ -92,8 +92,10 @@ def main() -> int:
     failures += overlapped_hooks_check(rank, world, dev)
     failures += overlapped_hooks_check(rank, world, dev, grads="bucket")
     failures += ce_check(rank, world, dev)
+    failures += ce_check(rank, world, dev, gated=True)
     failures += nvls_check(rank, world, dev)
     failures += overlapped_hooks_check(rank, world, dev, grads="bucket", engine="ce")
+    failures += overlapped_hooks_check(rank, world, dev, grads="bucket", engine="gated")
     t = torch.tensor([failures], device=dev)
     dist.all_reduce(t)
     if rank == 0:
@@ -171,12 +173,16 @@ def mixed_grouping_check(rank: int, world: int, dev) -> int:
     return fails
 
 
-def ce_check(rank: int, world: int, dev) -> int:
-    """Copy-engine two-shot (caramel_allreduce_ce) through the C ABI: six
-    buckets, gradients in the bucket arena, SUM and fused SGD, the same launch
-    order grouped differently per rank (rank 0: one call; odd ranks: one call
-    per bucket; others: two calls).  Bit-exact with the oracle's SHUFFLE order."""
+def ce_check(rank: int, world: int, dev, gated: bool = False) -> int:
+    """Copy-engine two-shot (caramel_allreduce_ce) -- or, gated=True, the
+    gated SM engine (caramel_allreduce_gated) -- through the C ABI: six
+    buckets, gradients in the bucket arena, SUM and fused SGD, the launch
+    order in one call, one call per bucket, and two calls.  Bit-exact with the
+    oracle's SHUFFLE order."""
     import ctypes
+
+    fn = N.lib().caramel_allreduce_gated if gated else N.lib().caramel_allreduce_ce
+    what = "gated SM engine" if gated else "copy-engine"
 
     rng = np.random.default_rng(500 + rank)
     theta_rng = np.random.default_rng(9)
@@ -216,8 +222,7 @@ def ce_check(rank: int, world: int, dev) -> int:
 
             def call(i, j):
                 h = ctypes.cast(ctypes.byref(host, i * bsz), ctypes.POINTER(N.Bucket))
-                N.check(N.lib().caramel_allreduce_ce(ctx._ctx, h, j - i, i, epoch, ctypes.c_void_p(stream),
-                                                     ctypes.c_void_p(side.cuda_stream)))
+                N.check(fn(ctx._ctx, h, j - i, i, epoch, ctypes.c_void_p(stream), ctypes.c_void_p(side.cuda_stream)))
 
             torch.cuda.synchronize()
             dist.barrier()
@@ -242,7 +247,7 @@ def ce_check(rank: int, world: int, dev) -> int:
                 if not np.array_equal(got.view(np.uint32), want.view(np.uint32)):
                     fails += 1
                     bad = np.nonzero(got.view(np.uint32) != want.view(np.uint32))[0]
-                    print(f"rank {rank}: copy-engine mismatch bucket {i} (n={n}) epi={epi} epoch {epoch}: "
+                    print(f"rank {rank}: {what} mismatch bucket {i} (n={n}) epi={epi} epoch {epoch}: "
                           f"{bad.size} elems, first {bad[:5]}", flush=True)
     ctx.close()
     return fails

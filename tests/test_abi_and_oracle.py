@@ -246,3 +246,33 @@ def test_robust_calibration_ignores_an_outlier():
     mn = fit_network_model_robust(meas, "min")
     assert mn.latency_us + mn.per_byte_us * 64 == pytest.approx(min(small))
     assert mn.latency_us + mn.per_byte_us * (4 << 20) == pytest.approx(min(big))
+
+
+def test_overlapped_engine_arguments_are_checked_before_any_device_work():
+    """engine= is validated first: an unknown engine, and "ce" / "gated" on a
+    configuration they cannot run (world 1, flat gradients, ring), raise
+    ValueError on a CPU-only host before the Aggregator touches CUDA."""
+    _lib()
+    import torch
+
+    from paper_2004_14020_b200 import gradsets
+    from paper_2004_14020_b200.collective import Pattern, ReduceModel
+    from paper_2004_14020_b200.costmodel import NetworkModel
+    from paper_2004_14020_b200.executor import Aggregator, lower
+    from paper_2004_14020_b200.pipeline import run_pipeline
+    from paper_2004_14020_b200.sim import SimConfig
+
+    ts = gradsets.gradient_set("alexnet")
+    numels = {gradsets.param_id(i, len(ts)): t.numel for i, t in enumerate(ts)}
+    params = {pid: torch.zeros(1) for pid in numels}
+    for workers, pattern in ((1, Pattern.SHUFFLE), (2, Pattern.RING), (2, Pattern.SHUFFLE)):
+        art = run_pipeline(gradsets.layered_chain_dag(ts),
+                           SimConfig(workers=max(workers, 2), network=NetworkModel(10.0, 1 / 460e3),
+                                     reduce=ReduceModel(400, 10)))
+        plan = lower(art, numels, workers, pattern)
+        with pytest.raises(ValueError, match="engine must be"):
+            Aggregator(plan, params, engine="nccl")
+        for engine in ("ce", "gated"):
+            grads = "flat" if (workers, pattern) == (2, Pattern.SHUFFLE) else "bucket"
+            with pytest.raises(ValueError, match="needs grads='bucket', world > 1 and the SHUFFLE pattern"):
+                Aggregator(plan, params, engine=engine, grads=grads)

@@ -73,7 +73,9 @@ def compute_only():
 
 
 net = calibrate_network_model(world, rank)[0] if world > 1 else None
-ing, art, plan, net = bench.ingested_plan(args, model, compute_only, world, D, dev, net)
+ing, art, plan, net = bench.ingested_plan(args, model, compute_only, world, D, dev, net, example_inputs=(x,))
+if "PRIO" in os.environ:
+    Aggregator.comm_priority = int(os.environ["PRIO"])
 agg = Aggregator(plan, dict(ing.params), rank=rank, lr=0.01, epilogue="sgd", grads=os.environ.get("GRADS", "bucket"),
                  engine=os.environ.get("ENGINE", "sm"))
 gated = agg.gate_forward(ing.modules)
