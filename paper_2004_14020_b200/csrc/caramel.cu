@@ -2650,6 +2650,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_collective_many(const __grid_con
 // SMs while a peer is still in its backward pass).  Ownership is the depth-1
 // shard split (values are the same rank-order sums whoever owns them).
 #define GATED_MAX 32
+#ifndef GATED_THREADS
+#define GATED_THREADS 512
+#endif
 struct GParams {
   Env env;
   int nb;
@@ -2657,7 +2660,7 @@ struct GParams {
 };
 
 template <int NP>
-__global__ void __launch_bounds__(THREADS, 1) k_gated(const __grid_constant__ GParams P) {
+__global__ void __launch_bounds__(GATED_THREADS, 1) k_gated(const __grid_constant__ GParams P) {
   const Env E = P.env;
   if (cta_poisoned(E)) return;
   const int me = E.rank_base, G = gridDim.x;
@@ -4393,7 +4396,7 @@ static gfn_t pick_gated(int world) {
 // backward pass the launch overlaps)
 static int gated_grid(const caramel_ctx* c, const caramel_bucket* b, int n) {
   const int U = c->world <= 2 ? 4 : 2;
-  const uint64_t row = 4ull * U * THREADS;
+  const uint64_t row = 4ull * U * GATED_THREADS;
   uint64_t rows = 0;
   for (int i = 0; i < n; ++i) rows += (b[i].numel / c->world + row) / row;
   int cap = c->gated_ctas;
@@ -4430,7 +4433,7 @@ static int gated_enqueue(caramel_ctx* c, const caramel_bucket* host, int32_t cou
     fill_env(c, P.env, 1);
     P.nb = count - i0 < GATED_MAX ? count - i0 : GATED_MAX;
     for (int i = 0; i < P.nb; ++i) P.b[i] = host[i0 + i];
-    fn<<<gated_grid(c, P.b, P.nb), THREADS, 0, s>>>(P);
+    fn<<<gated_grid(c, P.b, P.nb), GATED_THREADS, 0, s>>>(P);
     CUDA_TRY(cudaGetLastError());
   }
   CU_TRY(ce_memops(s, false, peer_done, np_, tag));
@@ -4501,8 +4504,8 @@ int caramel_ce_submit(caramel_ctx* c, const caramel_bucket* host, int32_t count,
   if (engine != CARAMEL_ENGINE_CE && engine != CARAMEL_ENGINE_SM && engine != CARAMEL_ENGINE_GATED)
     return set_err(CARAMEL_EINVAL, "ce_submit: unknown engine %d", engine);
   int rc = 0;
-  if (engine == CARAMEL_ENGINE_CE || engine == CARAMEL_ENGINE_GATED) {
-    rc = ce_validate(c, host, count, epoch, engine == CARAMEL_ENGINE_CE);
+  if (engine != CARAMEL_ENGINE_SM) {
+    rc = ce_validate(c, host, count, epoch, engine != CARAMEL_ENGINE_GATED);
   } else {
     if (!c || !host || count < 1) return set_err(CARAMEL_EINVAL, "ce_submit: null argument or empty list");
     if (!c->imported) return set_err(CARAMEL_ESTATE, "peer arenas not mapped (call caramel_import)");

@@ -43,8 +43,10 @@ from .transfer import PlacementKind
 
 PATTERN_CODE = {Pattern.RING: N.RING, Pattern.HALVING_DOUBLING: N.HD, Pattern.SHUFFLE: N.SHUFFLE}
 ALIGN = 256
-#: the copy-engine engine's stream-memory-op waits stall their hardware queue;
-#: with fewer queues than streams a wait can stall the backward pass too
+#: overlapped-mode engines whose waits are stream memory operations
+STREAM_ENGINES = ("ce", "gated")
+#: their stream-memory-op waits stall the stream's hardware queue; with fewer
+#: queues than streams a wait can stall the backward pass too
 CE_MIN_CONNECTIONS = 16
 
 
@@ -199,9 +201,9 @@ class Aggregator:
     def __init__(self, plan: ExecPlan, params: dict[str, torch.Tensor], *, rank: int = 0, lr: float = 0.01,
                  epilogue: str = "sgd", param_arena: bool = True, grads: str = "bucket", group=None,
                  bootstrap: bool = True, engine: str = "auto"):
-        if engine not in ("auto", "sm", "ce", "gated"):
+        if engine not in ("auto", "sm") + STREAM_ENGINES:
             raise ValueError("engine must be 'auto', 'sm', 'ce' or 'gated'")
-        if engine in ("ce", "gated") and (grads != "bucket" or plan.world < 2 or plan.pattern != N.SHUFFLE):
+        if engine in STREAM_ENGINES and (grads != "bucket" or plan.world < 2 or plan.pattern != N.SHUFFLE):
             raise ValueError(f"engine={engine!r} needs grads='bucket', world > 1 and the SHUFFLE pattern")
         self.engine = engine
         self.plan = plan
@@ -219,9 +221,9 @@ class Aggregator:
         if self.world > 1 and bootstrap:
             agree("execution plan", plan.digest(), self.world, group)
             self.ctx.bootstrap(group)
-        if engine in ("ce", "gated") and not N.lib().caramel_ce_available(self.ctx._ctx):
+        if engine in STREAM_ENGINES and not N.lib().caramel_ce_available(self.ctx._ctx):
             raise RuntimeError(f"engine={engine!r}: this device lacks 64-bit stream memory operations")
-        if engine in ("ce", "gated") and not ce_connections_ok():
+        if engine in STREAM_ENGINES and not ce_connections_ok():
             raise RuntimeError(f"engine={engine!r} needs CUDA_DEVICE_MAX_CONNECTIONS >= {CE_MIN_CONNECTIONS} in the "
                                "environment before CUDA initialises: a stream-memory-op wait stalls its hardware "
                                "queue, and with shared queues it can stall the backward pass behind a peer")
@@ -270,7 +272,7 @@ class Aggregator:
         for lv in self._live:
             for pid in lv.members:
                 self._by_param[pid] = lv
-        if self.engine in ("ce", "gated"):
+        if self.engine in STREAM_ENGINES:
             for lv in self._live:  # materialised now, recorded by the worker thread later
                 lv.ce_done = torch.cuda.Event()
                 lv.ce_done.record(self.comm_stream)
@@ -304,7 +306,7 @@ class Aggregator:
             # zero-copy: the bucket IS the gradient storage; results land in the
             # parameter arena (SGD) or in place (mean / sum; ring/hd unpack)
             flags = N.F_PARAM_ARENA if self.param_arena else N.F_UNPACK
-            if self.engine in ("ce", "gated") and not self.param_arena:
+            if self.engine in STREAM_ENGINES and not self.param_arena:
                 flags = 0  # the copy-engine all-gather lands in the bucket = the gradients
         else:
             flags = N.F_PACK | (N.F_PARAM_ARENA if self.param_arena else N.F_UNPACK)
@@ -554,8 +556,9 @@ class Aggregator:
 
     #: CUDA priority of the comm stream (lower = higher; torch clamps to the
     #: device's range): a high-priority stream's CTAs are scheduled ahead of
-    #: queued backward CTAs as SMs free up
-    comm_priority = 0
+    #: queued backward CTAs as SMs free up (measured: lower exposed time for
+    #: the gated and copy-engine engines, profiles/r02_engines_priority.txt)
+    comm_priority = -1
     #: overlapped mode: while the comm stream is busy, ready buckets are held
     #: back and coalesced into one list launch (per-bucket flags, so ranks may
     #: group differently) until this many are pending or this many bytes
@@ -581,7 +584,7 @@ class Aggregator:
         if j == self._next:
             return
         pending_bytes = 4 * (self._prefix[j] - self._prefix[self._next])
-        if self.engine in ("ce", "gated"):
+        if self.engine in STREAM_ENGINES:
             self._drain_ce(j)
             return
         if not force and self._comm_busy() and j - self._next < self.coalesce_buckets \
@@ -661,7 +664,7 @@ class Aggregator:
         self._next = j
 
     def _ce_flush(self) -> None:
-        if self.engine in ("ce", "gated"):
+        if self.engine in STREAM_ENGINES:
             N.check(N.lib().caramel_ce_flush(self.ctx._ctx))
 
     def finish_iteration(self, postpone: bool = False) -> None:

@@ -92,7 +92,7 @@ def main() -> int:
     failures += overlapped_hooks_check(rank, world, dev)
     failures += overlapped_hooks_check(rank, world, dev, grads="bucket")
     failures += ce_check(rank, world, dev)
-    failures += ce_check(rank, world, dev, gated=True)
+    failures += ce_check(rank, world, dev, gated="pull")
     failures += nvls_check(rank, world, dev)
     failures += overlapped_hooks_check(rank, world, dev, grads="bucket", engine="ce")
     failures += overlapped_hooks_check(rank, world, dev, grads="bucket", engine="gated")
@@ -173,16 +173,16 @@ def mixed_grouping_check(rank: int, world: int, dev) -> int:
     return fails
 
 
-def ce_check(rank: int, world: int, dev, gated: bool = False) -> int:
-    """Copy-engine two-shot (caramel_allreduce_ce) -- or, gated=True, the
-    gated SM engine (caramel_allreduce_gated) -- through the C ABI: six
+def ce_check(rank: int, world: int, dev, gated: str = "") -> int:
+    """Copy-engine two-shot (caramel_allreduce_ce) -- or the
+    gated SM engine (gated="pull": caramel_allreduce_gated) -- through the C ABI: six
     buckets, gradients in the bucket arena, SUM and fused SGD, the launch
     order in one call, one call per bucket, and two calls.  Bit-exact with the
     oracle's SHUFFLE order."""
     import ctypes
 
-    fn = N.lib().caramel_allreduce_gated if gated else N.lib().caramel_allreduce_ce
-    what = "gated SM engine" if gated else "copy-engine"
+    fn = {"": N.lib().caramel_allreduce_ce, "pull": N.lib().caramel_allreduce_gated}[gated]
+    what = f"gated SM engine ({gated})" if gated else "copy-engine"
 
     rng = np.random.default_rng(500 + rank)
     theta_rng = np.random.default_rng(9)
