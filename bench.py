@@ -661,8 +661,12 @@ def bucket_sweep(torch, dist, world, rank, dev, iters=20, network=None):
         n = size // 4
         depth = adaptive_depth(size, thr)
         ctas, _, _ = N.bucket_layout(n, depth, N.SHUFFLE, world)
+        # one kernel per call: the launch takes the device epoch + 1 and its last
+        # CTA advances the counter (CARAMEL_F_AUTO_EPOCH), like NCCL's one kernel
         b = comm.make_bucket(n, 0, region + k * (1 << 20), depth=depth, pattern=N.SHUFFLE, epilogue=N.EPI_SUM,
-                             flags=0, ctas=ctas)
+                             flags=N.F_AUTO_EPOCH, ctas=ctas)
+        b_ce = comm.make_bucket(n, 0, region + k * (1 << 20), depth=depth, pattern=N.SHUFFLE, epilogue=N.EPI_SUM,
+                                flags=0, ctas=ctas)
 
         def timed(fn, graphed=True):
             """Per-call device time of `fn`: `iters` calls captured in one CUDA
@@ -707,8 +711,7 @@ def bucket_sweep(torch, dist, world, rank, dev, iters=20, network=None):
 
         def caramel(st=None):
             st = st or stream
-            N.check(N.lib().caramel_epoch_advance(ctx._ctx, ctypes.c_void_p(st.cuda_stream)))
-            ctx.allreduce(b, 0, st.cuda_stream)  # epoch 0: device counter (graph-replayable)
+            ctx.allreduce(b, 0, st.cuda_stream)  # epoch 0 + AUTO_EPOCH: device counter (graph-replayable)
 
         x = torch.empty(n, device=dev).normal_()
         spread = []
@@ -724,12 +727,10 @@ def bucket_sweep(torch, dist, world, rank, dev, iters=20, network=None):
             for d in SWEEP_DEPTHS:
                 cd, _, _ = N.bucket_layout(n, d, N.SHUFFLE, world)
                 bd = comm.make_bucket(n, 0, region + k * (1 << 20), depth=d, pattern=N.SHUFFLE,
-                                      epilogue=N.EPI_SUM, flags=0, ctas=cd)
+                                      epilogue=N.EPI_SUM, flags=N.F_AUTO_EPOCH, ctas=cd)
 
                 def fixed_call(st=None, bd=bd):
-                    st = st or stream
-                    N.check(N.lib().caramel_epoch_advance(ctx._ctx, ctypes.c_void_p(st.cuda_stream)))
-                    ctx.allreduce(bd, 0, st.cuda_stream)
+                    ctx.allreduce(bd, 0, (st or stream).cuda_stream)
 
                 fixed[str(d)] = round(timed(fixed_call)[0], 2)
             row["fixed_depth_us"] = fixed
@@ -741,7 +742,7 @@ def bucket_sweep(torch, dist, world, rank, dev, iters=20, network=None):
 
                 def ce_call(st=None, c=c, key=key, fn=fn):
                     ce_epoch[key] += 1
-                    N.check(fn(c._ctx, ctypes.byref(b), 1, 0, ce_epoch[key], ctypes.c_void_p(stream.cuda_stream),
+                    N.check(fn(c._ctx, ctypes.byref(b_ce), 1, 0, ce_epoch[key], ctypes.c_void_p(stream.cuda_stream),
                                ctypes.c_void_p(stream.cuda_stream)))
                 us_e, _ = timed(ce_call, graphed=False)
                 row[f"{key}_us"] = round(us_e, 2)

@@ -60,6 +60,12 @@ extern "C" {
                                     contiguous, 16-byte aligned gradient segment
                                     (nseg == 1) -- enables the TMA bulk-copy
                                     streaming path                              */
+#define CARAMEL_F_AUTO_EPOCH 16u /* caramel_allreduce[_update] with epoch 0 only:
+                                    the launch uses the device epoch counter + 1
+                                    and its last CTA advances the counter -- one
+                                    kernel per call, graph-replayable (instead of
+                                    caramel_epoch_advance + the call); rejected
+                                    by list / stream-engine calls               */
 
 /* One member tensor of a fusion bucket.  Members are listed in bucket order
  * (BatchGroup.param_ids, batching.py:28-33) with contiguous offsets. */

@@ -17,7 +17,7 @@ HEADER = HERE.parent / "include" / "caramel.h"
 
 RING, HD, SHUFFLE = 0, 1, 2
 EPI_SUM, EPI_SCALE, EPI_SGD = 0, 1, 2
-F_PACK, F_UNPACK, F_PARAM_ARENA, F_FLAT = 1, 2, 4, 8
+F_PACK, F_UNPACK, F_PARAM_ARENA, F_FLAT, F_AUTO_EPOCH = 1, 2, 4, 8, 16
 MANY_FUSED, MANY_FLAGS = 0, 1
 ENGINE_CE, ENGINE_SM, ENGINE_GATED = 0, 1, 2
 MAX_RANKS = 8

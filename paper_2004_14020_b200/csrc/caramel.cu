@@ -597,7 +597,7 @@ struct Env {
   int world;
   int rank_base;          // first rank hosted by this launch (blockIdx.y adds)
   uint32_t epoch;         // 0: read *epoch_dev (graph-replayable launches)
-  const uint32_t* epoch_dev;
+  uint32_t* epoch_dev;    // [0] device epoch counter, [1] CTAs finished (CARAMEL_F_AUTO_EPOCH)
   uint64_t timeout_ns;
   int* status;            // device status word: 0, or CARAMEL_ETIMEOUT (sticky: the context is poisoned)
   int* hstatus;           // host-mapped mirror of *status (caramel_poll reads it without a sync)
@@ -1825,7 +1825,21 @@ __global__ void __launch_bounds__(THREADS, 1) k_collective(const __grid_constant
   const Env E = P.env;
   if (cta_poisoned(E)) return;
   const caramel_bucket B = P.b;
-  run_bucket<PAT, NP>(E, B, lr_idx, launch_epoch(E), blockIdx.x);
+  const bool autoep = (B.flags & CARAMEL_F_AUTO_EPOCH) && !E.epoch;
+  run_bucket<PAT, NP>(E, B, lr_idx, launch_epoch(E) + (autoep ? 1 : 0), blockIdx.x);
+  if (autoep) {
+    // one kernel per call: the last CTA to finish advances the device epoch
+    // (every CTA read it at entry, and the next launch on the stream sees it)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(E.epoch_dev + 1, 1u) == gridDim.x * gridDim.y - 1) {
+        E.epoch_dev[1] = 0;
+        E.epoch_dev[0] += 1;
+        __threadfence();
+      }
+    }
+  }
 }
 
 // world == 1, many buckets: the concatenated element space is tiled evenly
@@ -3559,8 +3573,8 @@ int caramel_init(int rank, int world, int nlocal, uint64_t arena_bytes, uint64_t
     c->arena[r] = (uint64_t)c->arena_local[i];
     c->parena[r] = (uint64_t)c->param_local[i];
   }
-  if ((e = cudaMalloc(&c->status, 2 * sizeof(int))) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "cudaMalloc status: %s", cudaGetErrorString(e)); goto fail; }
-  if ((e = cudaMemset(c->status, 0, 2 * sizeof(int))) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "memset: %s", cudaGetErrorString(e)); goto fail; }
+  if ((e = cudaMalloc(&c->status, 3 * sizeof(int))) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "cudaMalloc status: %s", cudaGetErrorString(e)); goto fail; }
+  if ((e = cudaMemset(c->status, 0, 3 * sizeof(int))) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "memset: %s", cudaGetErrorString(e)); goto fail; }
   c->epoch_dev = reinterpret_cast<uint32_t*>(c->status + 1);
   if ((e = cudaHostAlloc((void**)&c->hstatus, sizeof(int), cudaHostAllocMapped)) != cudaSuccess) { rc = set_err(CARAMEL_ECUDA, "cudaHostAlloc status: %s", cudaGetErrorString(e)); goto fail; }
   *(volatile int*)c->hstatus = 0;
@@ -3995,9 +4009,15 @@ static int launch(caramel_ctx* c, const caramel_bucket* b, uint32_t epoch, void*
   int rc = validate_bucket(c, b);
   if (rc) return rc;
   if (b->numel == 0) return 0;
+  if ((b->flags & CARAMEL_F_AUTO_EPOCH) && epoch != 0)
+    return set_err(CARAMEL_EINVAL, "CARAMEL_F_AUTO_EPOCH takes its epoch from the device counter: pass epoch 0");
   if (c->world > 1) {
     const int pr = shuffle_proto(*b, c->world);
-    if (pr == PROTO_OS || pr == PROTO_TS) return push_launch(c, b, 1, 0, 0, epoch, stream);
+    if (pr == PROTO_OS || pr == PROTO_TS) {
+      if (b->flags & CARAMEL_F_AUTO_EPOCH)
+        return set_err(CARAMEL_EINVAL, "CARAMEL_F_AUTO_EPOCH is not supported by the push engine");
+      return push_launch(c, b, 1, 0, 0, epoch, stream);
+    }
   }
   KParams P;
   fill_env(c, P.env, epoch);
@@ -4048,6 +4068,8 @@ int caramel_allreduce_many(caramel_ctx* c, const caramel_bucket* host, int32_t c
     if (host[i].pattern != pattern || host[i].epilogue != host[0].epilogue ||
         (host[i].flags & ~CARAMEL_F_FLAT) != (host[0].flags & ~CARAMEL_F_FLAT))
       return set_err(CARAMEL_EINVAL, "allreduce_many: buckets must share pattern, epilogue and flags");
+    if (host[i].flags & CARAMEL_F_AUTO_EPOCH)
+      return set_err(CARAMEL_EINVAL, "allreduce_many: CARAMEL_F_AUTO_EPOCH is for single-bucket calls");
     int rc = validate_bucket(c, &host[i]);
     if (rc) return rc;
     if (host[i].ctas > gmax) gmax = host[i].ctas;
@@ -4280,8 +4302,9 @@ static int ce_validate(caramel_ctx* c, const caramel_bucket* host, int32_t count
     if (b.pattern != CARAMEL_SHUFFLE) return set_err(CARAMEL_EINVAL, "allreduce_ce: SHUFFLE buckets only");
     if (b.epilogue != epi || b.flags != host[0].flags)
       return set_err(CARAMEL_EINVAL, "allreduce_ce: buckets must share epilogue and flags");
-    if (b.flags & (CARAMEL_F_PACK | CARAMEL_F_UNPACK))
-      return set_err(CARAMEL_EINVAL, "allreduce_ce: gradients must live in the bucket arena (no PACK/UNPACK)");
+    if (b.flags & (CARAMEL_F_PACK | CARAMEL_F_UNPACK | CARAMEL_F_AUTO_EPOCH))
+      return set_err(CARAMEL_EINVAL, "allreduce_ce: gradients must live in the bucket arena (no PACK/UNPACK), "
+                                     "epochs are explicit (no AUTO_EPOCH)");
     if (epi == CARAMEL_EPI_SGD && !(b.flags & CARAMEL_F_PARAM_ARENA))
       return set_err(CARAMEL_EINVAL, "allreduce_ce: the SGD epilogue needs PARAM_ARENA");
     int rc = validate_bucket(c, &b);

@@ -46,7 +46,7 @@ def _flat(ts):
 
 
 def run_emulated(pattern, p, depth, shapes, epi, *, unpack=True, param_arena=False, epochs=1,
-                 ctas=None, misalign=False, seed=0, int_valued=False):
+                 ctas=None, misalign=False, seed=0, int_valued=False, auto_epoch=False):
     N, comm = _native()
     dev = torch.device("cuda:0")
     numel = sum(int(np.prod(s)) for s in shapes)
@@ -65,6 +65,7 @@ def run_emulated(pattern, p, depth, shapes, epi, *, unpack=True, param_arena=Fal
             ctx.arena_view(r, 0, numel, param=True).copy_(torch.from_numpy(O.np_pack(theta)).to(dev))
     stream = torch.cuda.current_stream().cuda_stream
     flags = N.F_PACK | (N.F_UNPACK if unpack else 0) | (N.F_PARAM_ARENA if param_arena else 0)
+    flags |= N.F_AUTO_EPOCH if auto_epoch else 0
     results = []
     for e in range(1, epochs + 1):
         if int_valued:
@@ -76,7 +77,7 @@ def run_emulated(pattern, p, depth, shapes, epi, *, unpack=True, param_arena=Fal
             [comm.segments_for(g_dev[r], None if param_arena else th_dev[r]) for r in range(p)], dev)
         b = comm.make_bucket(numel, 0, flag_off, depth=depth, pattern=pattern, epilogue=epi, flags=flags,
                              ctas=ctas, segs=table, nseg=len(shapes), lr=lr, scale=scale)
-        ctx.allreduce(b, e, stream)
+        ctx.allreduce(b, 0 if auto_epoch else e, stream)
         ctx.status()
         torch.cuda.synchronize()
         theta_flat = O.np_pack(theta)
@@ -157,6 +158,36 @@ def test_epochs_reuse_flags(pattern):
     N, _ = _native()
     pat = {"ring": N.RING, "hd": N.HD, "shuffle": N.SHUFFLE}[pattern]
     assert_bitexact(run_emulated(pat, 8, 3, SHAPES_SMALL, N.EPI_SGD, epochs=4, ctas=3))
+
+
+@pytest.mark.parametrize("pattern", ["ring", "hd", "shuffle"])
+@pytest.mark.parametrize("shapes", [SHAPES_SMALL, [(300, 1000)], SHAPES_LARGE], ids=["ll", "ll128", "plain"])
+def test_auto_epoch_one_kernel_per_call(pattern, shapes):
+    """CARAMEL_F_AUTO_EPOCH: epoch 0, the device counter + 1, advanced by the
+    launch's last CTA -- consecutive calls with no caramel_epoch_advance
+    between them stay bit-exact (each call's flags carry a fresh epoch)."""
+    N, _ = _native()
+    pat = {"ring": N.RING, "hd": N.HD, "shuffle": N.SHUFFLE}[pattern]
+    assert_bitexact(run_emulated(pat, 4, 2, shapes, N.EPI_SGD, epochs=4, auto_epoch=True))
+
+
+def test_auto_epoch_is_rejected_where_it_cannot_apply():
+    N, comm = _native()
+    import ctypes
+
+    ctx = comm.Context(0, 2, arena_bytes=1 << 20, nlocal=2)
+    b = comm.make_bucket(1000, 0, 1 << 19, pattern=N.SHUFFLE, epilogue=N.EPI_SUM, flags=N.F_AUTO_EPOCH, ctas=2)
+    stream = torch.cuda.current_stream().cuda_stream
+    with pytest.raises(RuntimeError, match="AUTO_EPOCH"):
+        ctx.allreduce(b, 3, stream)  # an explicit epoch with the flag
+    host = (N.Bucket * 1)(b)
+    dl = torch.frombuffer(bytearray(bytes(host)), dtype=torch.uint8).to("cuda:0")
+    pre = torch.tensor([0, 1000], dtype=torch.int64, device="cuda:0")
+    spre = torch.tensor([0, 0], dtype=torch.int64, device="cuda:0")
+    rc = N.lib().caramel_allreduce_many(ctx._ctx, host, 1, dl.data_ptr(), pre.data_ptr(), spre.data_ptr(), 0,
+                                        N.MANY_FLAGS, 0, ctypes.c_void_p(stream))
+    assert rc != 0 and b"AUTO_EPOCH" in N.lib().caramel_last_error()
+    ctx.close()
 
 
 def test_misaligned_members():
