@@ -1266,17 +1266,19 @@ __device__ void rs_ag_multi(const Env& E, const caramel_bucket& B, bool arena, C
     while (v >= vpre[k + 1]) ++k;
     return va[k] + 4 * (v - vpre[k]);
   };
-  // rows of U*T vectors, row r to CTA r mod cg of the group (cg == 1: the
-  // whole range is this CTA's): the group sweeps the range together
-  const uint64_t ROW = (uint64_t)U * T;
-  for (uint64_t r = cj; r * ROW < V; r += cg) {
+  // the group's cg CTAs split [0, V) into balanced contiguous ranges (cg ==
+  // 1: the whole range is this CTA's).  Whole rows of U*T vectors per CTA
+  // left up to one row of imbalance: 85 rows over 42 CTAs (16 MiB, depth 3)
+  // ran 3 rows on some CTAs and 2 on most, 10% over depth 1.
+  const uint64_t v_lo = V * (uint64_t)cj / (uint64_t)cg, v_hi = V * (uint64_t)(cj + 1) / (uint64_t)cg;
+  for (uint64_t base = v_lo; base < v_hi; base += (uint64_t)U * T) {
     uint64_t x[U];
     bool ok[U];
     float4 pv[U][NP], tv[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const uint64_t v = r * ROW + u * T + threadIdx.x;
-      ok[u] = v < V;
+      const uint64_t v = base + u * T + threadIdx.x;
+      ok[u] = v < v_hi;
       x[u] = ok[u] ? pos(v, kc[u]) : 0;
 #pragma unroll
       for (int q = 0; q < NP; ++q) pv[u][q] = ok[u] ? ld4(src[q] + x[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1828,16 +1830,15 @@ __global__ void __launch_bounds__(THREADS, 1) k_collective(const __grid_constant
   const bool autoep = (B.flags & CARAMEL_F_AUTO_EPOCH) && !E.epoch;
   run_bucket<PAT, NP>(E, B, lr_idx, launch_epoch(E) + (autoep ? 1 : 0), blockIdx.x);
   if (autoep) {
-    // one kernel per call: the last CTA to finish advances the device epoch
-    // (every CTA read it at entry, and the next launch on the stream sees it)
+    // one kernel per call: the last CTA to finish advances the device epoch.
+    // Every CTA consumed its entry read of the counter in its flag waits
+    // before it gets here, and the next launch on the stream sees the new
+    // value at the kernel boundary -- no fence (a gpu-scope fence would also
+    // wait for this CTA's outstanding NVLink stores)
     __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      if (atomicAdd(E.epoch_dev + 1, 1u) == gridDim.x * gridDim.y - 1) {
-        E.epoch_dev[1] = 0;
-        E.epoch_dev[0] += 1;
-        __threadfence();
-      }
+    if (threadIdx.x == 0 && atomicAdd(E.epoch_dev + 1, 1u) == gridDim.x * gridDim.y - 1) {
+      E.epoch_dev[1] = 0;
+      E.epoch_dev[0] += 1;
     }
   }
 }
