@@ -1104,6 +1104,8 @@ struct BucketRun {
   int lr_idx;
   bool arena;
   bool flat;         // two-shot over flags: every CTA takes its tile of EVERY chunk
+  uint32_t cmask;    // chunks this CTA works on (bit c), and its tile / group size in them
+  int cjj, cgg;
   uint64_t out_off;
   const caramel_segment* segs;
 
@@ -1120,20 +1122,17 @@ struct BucketRun {
   // group c = CTAs [s_c, e_c) works on chunk c only (several chunks share a
   // CTA when G < depth).  mine(c): does this CTA take part in chunk c, and as
   // which tile of how many.
+  // (computed once per CTA in make_run: evaluating the group bounds here, per
+  // chunk and per call, cost ~1 us per extra chunk in integer divisions)
   __device__ __forceinline__ bool mine(int c, int& jj, int& gg) const {
     if (flat) {  // the chunks are an ownership map only: one flat pass over all of them
       jj = X.j;
       gg = X.G;
       return true;
     }
-    const int G = X.G, k = B->depth;
-    const int s0 = (int)(((int64_t)c * G) / k);
-    int e0 = (int)(((int64_t)(c + 1) * G) / k);
-    if (e0 <= s0) e0 = s0 + 1;
-    if (X.j < s0 || X.j >= e0) return false;
-    jj = X.j - s0;
-    gg = e0 - s0;
-    return true;
+    jj = cjj;
+    gg = cgg;
+    return (cmask >> c) & 1u;
   }
   __device__ __forceinline__ bool mine(int c) const {
     int a, b;
@@ -1176,6 +1175,22 @@ __device__ __forceinline__ void make_run(BucketRun& R, const Env& E, const caram
   R.X.G = B.ctas;
   R.X.ns = nslots(pattern, E.world);
   R.X.epoch = epoch;
+  // chunk-parallel CTA groups: chunk c = CTAs [s_c, e_c), s_c = floor(c*G/k)
+  // (at least one CTA each; with G < k every group is one CTA)
+  const int G = B.ctas, k = B.depth;
+  R.cmask = 0;
+  R.cjj = 0;
+  R.cgg = 1;
+  for (int c = 0; c < k; ++c) {
+    const int s0 = (c * G) / k;
+    int e0 = ((c + 1) * G) / k;
+    if (e0 <= s0) e0 = s0 + 1;
+    if (j >= s0 && j < e0) {
+      R.cmask |= 1u << c;
+      R.cjj = j - s0;
+      R.cgg = e0 - s0;
+    }
+  }
 }
 
 // phase 1 (all patterns): ring/hd buffer-reuse guard, fused pack, ready flags
