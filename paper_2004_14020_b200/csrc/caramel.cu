@@ -1251,24 +1251,38 @@ __device__ void rs_ag_multi(const Env& E, const caramel_bucket& B, bool arena, C
   const bool sgd = epi == CARAMEL_EPI_SGD;
   uint64_t va[CARAMEL_MAX_DEPTH], vpre[CARAMEL_MAX_DEPTH + 1];
   vpre[0] = 0;
+  // The vector part of a range starts and ends on 128-byte lines (32 floats):
+  // a warp's 32 float4s then cover exactly 4 lines instead of straddling 5,
+  // which over NVLink cost an unaligned (depth-3) bucket 9%.  Scalar heads
+  // [lo, a) and tails [b, hi) (< 32 each, CTA cj == 0 of the group): thread t
+  // takes the t-th one; its loads are issued here and consumed after the
+  // vector loop, so their round trip overlaps the vectors.  At most 62 per
+  // range and 8 ranges: every caller runs >= 496 threads (static_asserts at
+  // k_collective / k_gated).
+  bool has_s = false;
+  uint64_t sx = 0;
+  uint32_t scnt = 0;
   for (int k = 0; k < nr; ++k) {
-    uint64_t a = (lo[k] + 3) & ~3ull, b = hi[k] & ~3ull;
+    uint64_t a = (lo[k] + 31) & ~31ull, b = hi[k] & ~31ull;
     if (a > hi[k]) a = hi[k];
     if (b < a) b = a;
     va[k] = a;
     vpre[k + 1] = vpre[k] + (b - a) / 4;
-    // scalar head [lo, a) and tail [b, hi) (one CTA of the group)
-    const uint64_t nh = cj == 0 ? a - lo[k] : 0, nt = cj == 0 ? hi[k] - b : 0;
-    for (uint64_t e = threadIdx.x; e < nh + nt; e += blockDim.x) {
-      const uint64_t x = e < nh ? lo[k] + e : b + (e - nh);
-      float acc = ld1(src[0] + x);
-#pragma unroll
-      for (int q = 1; q < NP; ++q) acc = __fadd_rn(acc, ld1(src[q] + x));
-      const float t = sgd ? (arena ? ld1(th + x) : seg_ld1(tc, x, 1)) : 0.f;
-      const float o = epi1(epi, acc, t, B.scale, B.lr);
-#pragma unroll
-      for (int q = 0; q < NP; ++q) st1(dst[q] + x, o);
+    if (cj == 0) {
+      const uint64_t nh = a - lo[k], nt = hi[k] - b;
+      if (threadIdx.x >= scnt && threadIdx.x < scnt + nh + nt) {
+        const uint64_t e = threadIdx.x - scnt;
+        sx = e < nh ? lo[k] + e : b + (e - nh);
+        has_s = true;
+      }
+      scnt += (uint32_t)(nh + nt);
     }
+  }
+  float sv[NP], s_th = 0.f;
+  if (has_s) {
+#pragma unroll
+    for (int q = 0; q < NP; ++q) sv[q] = ld1(src[q] + sx);
+    if (sgd) s_th = arena ? ld1(th + sx) : seg_ld1(tc, sx, 1);
   }
   const uint64_t V = vpre[nr], T = blockDim.x;
   // flat vector index -> bucket element position; v only grows, so each of
@@ -1285,7 +1299,11 @@ __device__ void rs_ag_multi(const Env& E, const caramel_bucket& B, bool arena, C
   // 1: the whole range is this CTA's).  Whole rows of U*T vectors per CTA
   // left up to one row of imbalance: 85 rows over 42 CTAs (16 MiB, depth 3)
   // ran 3 rows on some CTAs and 2 on most, 10% over depth 1.
-  const uint64_t v_lo = V * (uint64_t)cj / (uint64_t)cg, v_hi = V * (uint64_t)(cj + 1) / (uint64_t)cg;
+  // (in units of 8 vectors = one 128-byte line)
+  const uint64_t V8 = (V + 7) / 8;
+  uint64_t v_lo = 8 * (V8 * (uint64_t)cj / (uint64_t)cg), v_hi = 8 * (V8 * (uint64_t)(cj + 1) / (uint64_t)cg);
+  if (v_lo > V) v_lo = V;
+  if (v_hi > V) v_hi = V;
   for (uint64_t base = v_lo; base < v_hi; base += (uint64_t)U * T) {
     uint64_t x[U];
     bool ok[U];
@@ -1310,6 +1328,14 @@ __device__ void rs_ag_multi(const Env& E, const caramel_bucket& B, bool arena, C
 #pragma unroll
       for (int q = 0; q < NP; ++q) st4(dst[q] + x[u], o);
     }
+  }
+  if (has_s) {
+    float acc = sv[0];
+#pragma unroll
+    for (int q = 1; q < NP; ++q) acc = __fadd_rn(acc, sv[q]);
+    const float o = epi1(epi, acc, s_th, B.scale, B.lr);
+#pragma unroll
+    for (int q = 0; q < NP; ++q) st1(dst[q] + sx, o);
   }
 }
 
@@ -1834,6 +1860,7 @@ __device__ __forceinline__ void run_bucket(const Env& E, const caramel_bucket& B
 
 __global__ void k_epoch_advance(uint32_t* e) { *e += 1; }
 
+static_assert(THREADS >= 62 * CARAMEL_MAX_DEPTH, "rs_ag_multi: one thread per scalar head/tail element");
 template <int PAT, int NP>
 __global__ void __launch_bounds__(THREADS, 1) k_collective(const __grid_constant__ KParams P) {
   const int lr_idx = blockIdx.y;
@@ -1998,10 +2025,19 @@ struct FusedV { static constexpr int V = NP >= 4 ? 2 : NP == 2 ? CARAMEL_FUSED_V
 
 // items of my shard range [lo, hi): one edge item (scalar head + tail) and
 // one per 32*V float4s of the 16-byte aligned interior
+// The vector interior [a, e) of a shard starts and ends on 128-byte lines
+// (32 floats), so a warp's 32 float4s cover 4 lines, not 5 (a bucket's shard
+// boundaries fall anywhere: most shards were misaligned).
+__device__ __forceinline__ void line_interior(uint64_t lo, uint64_t hi, uint64_t& a, uint64_t& e) {
+  a = (lo + 31) & ~31ull;
+  e = hi & ~31ull;
+}
+
 template <int V>
 __device__ __forceinline__ uint32_t shard_items(uint64_t lo, uint64_t hi) {
   if (lo >= hi) return 0;
-  const uint64_t a = (lo + 3) & ~3ull, e = hi & ~3ull;
+  uint64_t a, e;
+  line_interior(lo, hi, a, e);
   return 1 + (e > a ? (uint32_t)(((e - a) / 4 + 32 * V - 1) / (32 * V)) : 0);
 }
 
@@ -2136,13 +2172,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_shuffle_fused(const __grid_const
       }
       const float* th = arena ? reinterpret_cast<const float*>(E.parena[me] + B.param_off) : nullptr;
       const bool sgd = B.epilogue == CARAMEL_EPI_SGD;
-      const uint64_t a = (lo + 3) & ~3ull, e = hi & ~3ull;
+      uint64_t a, e;
+      line_interior(lo, hi, a, e);
       if (li == 0) {  // edge item: scalar head [lo, a) and tail [e, hi) (whole range if no interior)
         const bool interior = e > a;
         const uint64_t n_head = interior ? a - lo : hi - lo;
         const uint64_t n_tail = interior ? hi - e : 0;
-        if ((uint64_t)lane < n_head + n_tail) {
-          const uint64_t x = (uint64_t)lane < n_head ? lo + lane : e + (lane - n_head);
+        for (uint64_t l = lane; l < n_head + n_tail; l += 32) {
+          const uint64_t x = l < n_head ? lo + l : e + (l - n_head);
           float acc = ld1(src[0] + x);
 #pragma unroll
           for (int q = 1; q < NP; ++q) acc = __fadd_rn(acc, ld1(src[q] + x));
@@ -2689,6 +2726,7 @@ struct GParams {
   caramel_bucket b[GATED_MAX];
 };
 
+static_assert(GATED_THREADS >= 62, "rs_ag_multi: one thread per scalar head/tail element");
 template <int NP>
 __global__ void __launch_bounds__(GATED_THREADS, 1) k_gated(const __grid_constant__ GParams P) {
   const Env E = P.env;
