@@ -174,6 +174,27 @@ class _Live:
     gate_modules: list = field(default_factory=list)
 
 
+def host_groups(sizes: list[int], group_bytes: int, taper_bytes: int = 0) -> list[tuple[int, int]]:
+    """Consecutive ranges [i, j) of `sizes` (bytes, launch order) of about
+    `group_bytes` each, every range non-empty; taper_bytes > 0 caps a range
+    at max(taper_bytes, min(group_bytes, bytes before it, half the bytes
+    after its start)) -- see Aggregator.host_groups."""
+    total = sum(sizes)
+    out, i, done = [], 0, 0
+    while i < len(sizes):
+        target = group_bytes
+        if taper_bytes:
+            target = max(taper_bytes, min(group_bytes, done, (total - done) // 2))
+        j, acc = i, 0
+        while j < len(sizes) and (j == i or acc + sizes[j] <= target):
+            acc += sizes[j]
+            j += 1
+        out.append((i, j))
+        done += acc
+        i = j
+    return out
+
+
 class Aggregator:
     """Runs an ExecPlan's bucket collectives on this rank.
 
@@ -396,18 +417,14 @@ class Aggregator:
                                              ctypes.c_void_p(stream)))
         self.launches += 1
 
-    def host_groups(self, group_bytes: int = 16 << 20) -> list[tuple[int, int]]:
+    def host_groups(self, group_bytes: int = 16 << 20, taper_bytes: int = 0) -> list[tuple[int, int]]:
         """Consecutive launch-order bucket ranges of about `group_bytes` each
-        (identical on every rank)."""
-        out, i = [], 0
-        while i < len(self._live):
-            j, acc = i, 0
-            while j < len(self._live) and (j == i or acc + 4 * self._live[j].spec.numel <= group_bytes):
-                acc += 4 * self._live[j].spec.numel
-                j += 1
-            out.append((i, j))
-            i = j
-        return out
+        (identical on every rank).  taper_bytes > 0: the groups grow from
+        about taper_bytes (doubling: at most the bytes already grouped) and
+        shrink the same way towards the end (at most half of what is left),
+        so the upload of the first group and the download of the last -- the
+        two transfers a two-stream pipeline cannot overlap -- are short."""
+        return host_groups([4 * lv.spec.numel for lv in self._live], group_bytes, taper_bytes)
 
     def flat_layout(self) -> list[tuple[str, int, int]]:
         """(param id, element offset, numel) of every parameter in the flat
@@ -421,11 +438,12 @@ class Aggregator:
         return out
 
     def step_host_flat(self, host_grads: torch.Tensor, host_params: torch.Tensor | None = None,
-                       group_bytes: int = 16 << 20) -> int:
+                       group_bytes: int = 16 << 20, taper_bytes: int = 2 << 20) -> int:
         """step_host for flat pinned buffers in the parameter-arena layout
         (flat_layout()): per group of buckets one H2D (grads="flat"; one per
         bucket with grads="bucket") and one D2H cudaMemcpyAsync, overlapped with
-        the group's aggregation kernel."""
+        the group's aggregation kernel; groups tapered at both ends
+        (host_groups)."""
         if self.grads not in ("flat", "bucket") or not self.param_arena:
             raise RuntimeError("step_host_flat needs grads='flat' or 'bucket' and the parameter arena")
         cur = torch.cuda.current_stream(self.device)
@@ -439,7 +457,7 @@ class Aggregator:
         if self._step_needs_epoch(True):
             N.check(N.lib().caramel_epoch_advance(self.ctx._ctx, ctypes.c_void_p(cur.cuda_stream)))
             launches = 1
-        for i, j in self.host_groups(group_bytes):
+        for i, j in self.host_groups(group_bytes, taper_bytes):
             a = self._live[i].spec.param_off // 4
             last = self._live[j - 1].spec
             b = last.param_off // 4 + last.numel
@@ -466,7 +484,8 @@ class Aggregator:
             v = lv._view = self.ctx.arena_view(0, lv.spec.bucket_off, lv.spec.numel)
         return v
 
-    def step_host(self, host_grads: dict, host_params: dict | None = None, group_bytes: int = 16 << 20) -> int:
+    def step_host(self, host_grads: dict, host_params: dict | None = None, group_bytes: int = 16 << 20,
+                  taper_bytes: int = 2 << 20) -> int:
         """The plugin path with HOST buffers: pinned host gradients -> device,
         aggregation + fused update, updated parameters -> pinned host, pipelined
         per group of buckets on two copy streams so H2D of group i+1, the
@@ -482,7 +501,7 @@ class Aggregator:
         if self._step_needs_epoch(True):
             N.check(N.lib().caramel_epoch_advance(self.ctx._ctx, ctypes.c_void_p(cur.cuda_stream)))
             launches = 1
-        for i, j in self.host_groups(group_bytes):
+        for i, j in self.host_groups(group_bytes, taper_bytes):
             members = [pid for lv in self._live[i:j] for pid in lv.members]
             with torch.cuda.stream(h2d):
                 for pid in members:

@@ -276,3 +276,23 @@ def test_overlapped_engine_arguments_are_checked_before_any_device_work():
             grads = "flat" if (workers, pattern) == (2, Pattern.SHUFFLE) else "bucket"
             with pytest.raises(ValueError, match="needs grads='bucket', world > 1 and the SHUFFLE pattern"):
                 Aggregator(plan, params, engine=engine, grads=grads)
+
+
+def test_host_groups_taper_at_both_ends():
+    """The host-buffer pipeline's groups (executor.host_groups): contiguous,
+    covering, every group non-empty; flat groups stay under group_bytes (or
+    hold one bucket); tapered groups start and end small and double / halve."""
+    from paper_2004_14020_b200 import gradsets
+    from paper_2004_14020_b200.executor import host_groups
+
+    for sizes in ([4 * t.numel for t in gradsets.gradient_set("resnet50")], [1 << 20] * 100, [5, 7, 1 << 24, 3]):
+        for taper in (0, 2 << 20):
+            g = host_groups(sizes, 16 << 20, taper)
+            assert g[0][0] == 0 and g[-1][1] == len(sizes)
+            assert all(a < b for a, b in g) and all(g[k][1] == g[k + 1][0] for k in range(len(g) - 1))
+            nbytes = [sum(sizes[a:b]) for a, b in g]
+            assert all(n <= (16 << 20) or b - a == 1 for n, (a, b) in zip(nbytes, g))
+            if taper and len(g) > 2:
+                assert nbytes[0] <= max(2 << 20, sizes[0]) and nbytes[-1] <= max(2 << 20, max(sizes[g[-1][0]:]))
+    g = host_groups([1 << 20] * 100, 16 << 20, 2 << 20)
+    assert [sum(1 for _ in range(a, b)) for a, b in g][:4] == [2, 2, 4, 8]
