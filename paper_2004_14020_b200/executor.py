@@ -177,14 +177,14 @@ class _Live:
 def host_groups(sizes: list[int], group_bytes: int, taper_bytes: int = 0) -> list[tuple[int, int]]:
     """Consecutive ranges [i, j) of `sizes` (bytes, launch order) of about
     `group_bytes` each, every range non-empty; taper_bytes > 0 caps a range
-    at max(taper_bytes, min(group_bytes, bytes before it, half the bytes
-    after its start)) -- see Aggregator.host_groups."""
+    at min(group_bytes, max(taper_bytes, min(bytes before it, half the bytes
+    from its start))) -- see Aggregator.host_groups."""
     total = sum(sizes)
     out, i, done = [], 0, 0
     while i < len(sizes):
         target = group_bytes
         if taper_bytes:
-            target = max(taper_bytes, min(group_bytes, done, (total - done) // 2))
+            target = min(group_bytes, max(taper_bytes, min(done, (total - done) // 2)))
         j, acc = i, 0
         while j < len(sizes) and (j == i or acc + sizes[j] <= target):
             acc += sizes[j]

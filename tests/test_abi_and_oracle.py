@@ -296,3 +296,5 @@ def test_host_groups_taper_at_both_ends():
                 assert nbytes[0] <= max(2 << 20, sizes[0]) and nbytes[-1] <= max(2 << 20, max(sizes[g[-1][0]:]))
     g = host_groups([1 << 20] * 100, 16 << 20, 2 << 20)
     assert [sum(1 for _ in range(a, b)) for a, b in g][:4] == [2, 2, 4, 8]
+    # group_bytes below the taper still bounds every group
+    assert all(b - a == 1 for a, b in host_groups([1 << 20] * 10, 4096, 2 << 20))
