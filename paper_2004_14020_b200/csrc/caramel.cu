@@ -1235,7 +1235,7 @@ __device__ void phase_pack(const BucketRun& R) {
 // shard in every chunk) as ONE flat vector loop: chunk boundaries cost no
 // extra memory round trip (2*NP 128-bit loads in flight per thread across
 // ranges).  Scalar heads/tails first.
-template <int NP>
+template <int NP, int UV = 0>
 __device__ void rs_ag_multi(const Env& E, const caramel_bucket& B, bool arena, Cursor& tc, const uint64_t* lo,
                             const uint64_t* hi, int nr, int me, int cj = 0, int cg = 1) {
   const float* src[NP];
@@ -1287,7 +1287,8 @@ __device__ void rs_ag_multi(const Env& E, const caramel_bucket& B, bool arena, C
   const uint64_t V = vpre[nr], T = blockDim.x;
   // flat vector index -> bucket element position; v only grows, so each of
   // the U streams keeps its own range cursor (no rescan per vector)
-  constexpr int U = NP <= 2 ? 4 : 2;  // U x NP 128-bit loads in flight per thread (8 at p = 2, as the fused kernel)
+  // U x NP 128-bit loads in flight per thread (8 at p = 2, as the fused kernel)
+  constexpr int U = UV ? UV : NP <= 2 ? 4 : 2;
   int kc[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) kc[u] = 0;
@@ -2720,6 +2721,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_collective_many(const __grid_con
 #ifndef GATED_THREADS
 #define GATED_THREADS 512
 #endif
+#ifndef GATED_U
+#define GATED_U 0  // float4s in flight per thread and rank (0: rs_ag_multi's default)
+#endif
 struct GParams {
   Env env;
   int nb;
@@ -2732,7 +2736,7 @@ __global__ void __launch_bounds__(GATED_THREADS, 1) k_gated(const __grid_constan
   const Env E = P.env;
   if (cta_poisoned(E)) return;
   const int me = E.rank_base, G = gridDim.x;
-  constexpr int U = NP <= 2 ? 4 : 2;  // rs_ag_multi's row: U vectors per thread
+  constexpr int U = GATED_U ? GATED_U : NP <= 2 ? 4 : 2;  // rs_ag_multi's row: U vectors per thread
   const uint64_t row = 4ull * U * blockDim.x;
   uint64_t rot = 0;  // the first row of bucket i goes to CTA rot mod G: small buckets spread over the grid
   for (int i = 0; i < P.nb; ++i) {
@@ -2743,7 +2747,7 @@ __global__ void __launch_bounds__(GATED_THREADS, 1) k_gated(const __grid_constan
     const int cj = (int)(((uint64_t)blockIdx.x + G - rot % G) % G);
     Cursor tc;
     cur_init(tc, reinterpret_cast<const caramel_segment*>(B.segs), B.nseg);
-    rs_ag_multi<NP>(E, B, arena, tc, &lo, &hi, 1, me, cj, G);
+    rs_ag_multi<NP, GATED_U>(E, B, arena, tc, &lo, &hi, 1, me, cj, G);
     rot += (hi - lo + row - 1) / row;
   }
 }
@@ -4472,7 +4476,7 @@ static gfn_t pick_gated(int world) {
 // (CARAMEL_GATED_CTAS, default 32 -- the rest of the GPU stays with the
 // backward pass the launch overlaps)
 static int gated_grid(const caramel_ctx* c, const caramel_bucket* b, int n) {
-  const int U = c->world <= 2 ? 4 : 2;
+  const int U = GATED_U ? GATED_U : c->world <= 2 ? 4 : 2;
   const uint64_t row = 4ull * U * GATED_THREADS;
   uint64_t rows = 0;
   for (int i = 0; i < n; ++i) rows += (b[i].numel / c->world + row) / row;
