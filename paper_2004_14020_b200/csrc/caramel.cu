@@ -1103,7 +1103,6 @@ struct BucketRun {
   Ctx X;
   int lr_idx;
   bool arena;
-  bool flat;         // two-shot over flags: every CTA takes its tile of EVERY chunk
   uint32_t cmask;    // chunks this CTA works on (bit c), and its tile / group size in them
   int cjj, cgg;
   uint64_t out_off;
@@ -1125,11 +1124,6 @@ struct BucketRun {
   // (computed once per CTA in make_run: evaluating the group bounds here, per
   // chunk and per call, cost ~1 us per extra chunk in integer divisions)
   __device__ __forceinline__ bool mine(int c, int& jj, int& gg) const {
-    if (flat) {  // the chunks are an ownership map only: one flat pass over all of them
-      jj = X.j;
-      gg = X.G;
-      return true;
-    }
     jj = cjj;
     gg = cgg;
     return (cmask >> c) & 1u;
@@ -1156,12 +1150,10 @@ __device__ __forceinline__ void make_run(BucketRun& R, const Env& E, const caram
   R.tab = &g_tab;
   R.lr_idx = lr_idx;
   R.arena = (B.flags & CARAMEL_F_PARAM_ARENA) && B.epilogue == CARAMEL_EPI_SGD;
-  // One flat pass over every chunk (each CTA its tile of all chunks, one flag
-  // per tile) was measured against chunk-parallel CTA groups (each CTA one
-  // chunk's tile, per-chunk flags): the groups won at every depth > 1 (p=2,
-  // 16 MiB depth 3: 44.3 vs 51.6 us; 256 MiB depth 8: 416 vs 481 us; depth 1
-  // is identical), so the flat mode stays off; it remains for experiments.
-  R.flat = false;
+  // (one flat pass over every chunk -- each CTA its tile of all chunks, one
+  // flag per tile -- was measured against these chunk-parallel CTA groups and
+  // lost at every depth > 1: p=2, 16 MiB depth 3 44.3 vs 51.6 us, 256 MiB
+  // depth 8 416 vs 481 us; it was removed)
   // shuffle all-gathers in place; ring/hd write results to a second region
   // of the bucket so a fast neighbour never overwrites a partial sum that a
   // slower one has yet to pull
@@ -1222,13 +1214,12 @@ __device__ void phase_pack(const BucketRun& R) {
       }
     }
     if (PAT == CARAMEL_SHUFFLE) {
-      if (!DEFER && !R.flat) R.X.publish_all(c, SLOT_READY);
+      if (!DEFER) R.X.publish_all(c, SLOT_READY);
     } else {
       int t = (PAT == CARAMEL_RING) ? (me + 1) % p : (me ^ (p >> 1));
       R.X.publish(c, SLOT_READY, &t, 1);
     }
   }
-  if (PAT == CARAMEL_SHUFFLE && !DEFER && R.flat) R.X.publish_all(0, SLOT_READY);  // one READY for all chunks
 }
 
 // Reduce + epilogue + all-gather of several ranges (this CTA's tile of my
@@ -1349,10 +1340,10 @@ __device__ void phase_shuffle(const BucketRun& R) {
   cur_init(tc, R.segs, R.B->nseg);
   // Without PACK / UNPACK no tile of a CTA depends on another CTA's work (the
   // gradients were complete before any rank launched): the chunk's CTA group
-  // sweeps its whole shard row-cyclically instead of one contiguous tile each
-  const bool cyclic = !(R.B->flags & (CARAMEL_F_PACK | CARAMEL_F_UNPACK));
+  // sweeps its whole shard (balanced contiguous ranges) instead of one tile each
+  const bool group_sweep = !(R.B->flags & (CARAMEL_F_PACK | CARAMEL_F_UNPACK));
   auto range_of = [&](int c, uint64_t& lo, uint64_t& hi, int& cj, int& cg) {
-    if (cyclic) {
+    if (group_sweep) {
       R.mine(c, cj, cg);
       shard_bounds(R.B->numel, R.B->depth, R.X.world, c, R.X.me, lo, hi);
     } else {
@@ -1361,18 +1352,16 @@ __device__ void phase_shuffle(const BucketRun& R) {
       R.shard(c, R.X.me, lo, hi);
     }
   };
-  if (DEFER || R.flat) {
+  if (DEFER) {
     uint64_t lo[CARAMEL_MAX_DEPTH], hi[CARAMEL_MAX_DEPTH];
     int nr = 0, cj = 0, cg = 1;
-    if (R.flat) R.X.wait_all(0, SLOT_READY, R.X.epoch);  // one READY covers every chunk
     for (int c = 0; c < R.B->depth; ++c) {
       if (!R.mine(c)) continue;
-      if (!R.flat) R.X.wait_all(c, SLOT_READY, R.X.epoch);
+      R.X.wait_all(c, SLOT_READY, R.X.epoch);
       range_of(c, lo[nr], hi[nr], cj, cg);
       ++nr;
     }
     rs_ag_multi<NP>(*R.E, *R.B, R.arena, tc, lo, hi, nr, R.X.me, cj, cg);
-    if (!DEFER) R.X.publish_all(0, SLOT_DONE);  // flat, per-bucket list: DONE right away
     return;
   }
   for (int c = 0; c < R.B->depth; ++c) {
@@ -1789,7 +1778,7 @@ template <int PAT>
 __device__ void phase_finish(const BucketRun& R) {
   const int me = R.X.me, p = R.X.world;
   if (PAT == CARAMEL_SHUFFLE)
-    for (int c = 0; c < (R.flat ? 1 : R.B->depth); ++c)
+    for (int c = 0; c < R.B->depth; ++c)
       if (R.mine(c)) R.X.wait_all(c, SLOT_DONE, R.X.epoch);
   if ((R.B->flags & CARAMEL_F_UNPACK) && !R.arena) {
     const bool to_param = (R.B->epilogue == CARAMEL_EPI_SGD);
@@ -1822,7 +1811,7 @@ __device__ __forceinline__ void publish_chunks(const BucketRun& R, int slot) {
   if (threadIdx.x < 32) {
     fence_acq_rel_sys();
     const int p = R.X.world;
-    for (int idx = threadIdx.x; idx < (R.flat ? 1 : R.B->depth) * p; idx += 32)
+    for (int idx = threadIdx.x; idx < R.B->depth * p; idx += 32)
       if (R.mine(idx / p)) st_relaxed_sys(R.X.flag(idx % p, idx / p, slot, R.X.me), R.X.epoch);
   }
 }
@@ -2656,7 +2645,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_collective_many(const __grid_con
           const int ns = nslots(PAT, p);
           BucketRun R;
           make_run(R, E, B, PAT, lr_idx, epoch, j);
-          for (int idx = threadIdx.x; idx < (R.flat ? 1 : B.depth) * p; idx += 32) {
+          for (int idx = threadIdx.x; idx < B.depth * p; idx += 32) {
             const int c = idx / p, q = idx % p;
             if (!R.mine(c)) continue;
             uint32_t* f = reinterpret_cast<uint32_t*>(E.arena[q] + B.flag_off) +
