@@ -478,6 +478,23 @@ class Aggregator:
         cur.wait_stream(d2h)
         return launches
 
+    def capture_step_host_flat(self, host_grads: torch.Tensor, host_params: torch.Tensor | None = None,
+                               group_bytes: int = 16 << 20, taper_bytes: int = 2 << 20) -> torch.cuda.CUDAGraph:
+        """step_host_flat captured in a CUDA graph: every replay() is one full
+        step -- the H2D copies from `host_grads`, the aggregation launches and
+        the D2H copies into `host_params` (fixed pinned buffers; write the next
+        step's gradients into host_grads between replays) -- with no per-step
+        host issue cost, so a busy host does not stall the copy pipeline."""
+        self.step_host_flat(host_grads, host_params, group_bytes, taper_bytes)  # lazy streams / views
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
+            self.step_host_flat(host_grads, host_params, group_bytes, taper_bytes)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        return g
+
     def _bucket_view(self, lv: _Live) -> torch.Tensor:
         v = getattr(lv, "_view", None)
         if v is None:

@@ -305,3 +305,33 @@ def test_persisted_reference_plan_drives_the_executor(case):
         want = (theta0[k].cpu().numpy() - np.float32(lr) * p.grad.cpu().numpy()).astype(np.float32)
         assert np.array_equal(p.detach().cpu().numpy().view(np.uint32), want.view(np.uint32)), k
     agg.close()
+
+
+def test_captured_host_step_replays_full_steps():
+    """capture_step_host_flat: every replay is a whole step -- new host
+    gradients in, SGD applied, parameters out -- bit-exact, twice in a row."""
+    from paper_2004_14020_b200.executor import Aggregator
+
+    lr = 0.1
+    model = _tiny_model(5)
+    plan, params = _plan_for(model)
+    agg = Aggregator(plan, params, lr=lr, epilogue="sgd", grads="flat")
+    hg = torch.zeros(plan.param_bytes // 4).pin_memory()
+    hp = torch.zeros(plan.param_bytes // 4).pin_memory()
+    layout = agg.flat_layout()
+    theta = {pid: params[pid].detach().cpu().clone().view(-1) for pid, _, _ in layout}
+    for pid, off, n in layout:
+        hg[off:off + n].normal_()
+    g = agg.capture_step_host_flat(hg, hp, group_bytes=4096)  # runs one eager step first
+    torch.cuda.synchronize()
+    for pid, off, n in layout:
+        theta[pid] = theta[pid] - lr * hg[off:off + n]
+    for _ in range(2):
+        for pid, off, n in layout:
+            hg[off:off + n].normal_()
+        g.replay()
+        torch.cuda.synchronize()
+        for pid, off, n in layout:
+            theta[pid] = theta[pid] - lr * hg[off:off + n]
+            assert torch.equal(hp[off:off + n], theta[pid]), pid
+    agg.close()
