@@ -3380,10 +3380,10 @@ struct CeItem {
 
 struct CeJob {
   std::vector<caramel_bucket> buckets;
-  int engine;  // CARAMEL_ENGINE_CE / _SM / _GATED
+  int engine;  // CARAMEL_ENGINE_CE / CARAMEL_ENGINE_SM
   uint32_t index0, epoch;
   cudaEvent_t grads, done;
-  cudaStream_t stream, gstream;  // issue stream, stream `grads` was recorded on
+  cudaStream_t stream;
 };
 
 struct CeParams {
@@ -4538,26 +4538,6 @@ static void ce_worker_main(caramel_ctx* c) {
     if (c->ce_jobs.empty()) return;  // stop requested and drained
     CeJob job = std::move(c->ce_jobs.front());
     c->ce_jobs.pop_front();
-    // Gated jobs queued behind this one that continue its launch order merge
-    // into it: one stream wait, one launch, one DONE round trip for the whole
-    // backlog instead of one each (Inception-v3's tail: ~160 small buckets
-    // ready within microseconds of each other).  Tags are >= comparisons, so a
-    // peer that grouped the same launch order differently still matches; the
-    // last merged job's gradient event covers every merged bucket (recorded
-    // later on the same stream).
-    std::vector<cudaEvent_t> dones(1, job.done);
-    uint64_t merged = 1;
-    while (job.engine == CARAMEL_ENGINE_GATED && !c->ce_jobs.empty()) {
-      CeJob& nx = c->ce_jobs.front();
-      if (nx.engine != CARAMEL_ENGINE_GATED || nx.epoch != job.epoch || nx.stream != job.stream ||
-          nx.gstream != job.gstream || nx.index0 != job.index0 + (uint32_t)job.buckets.size())
-        break;
-      job.buckets.insert(job.buckets.end(), nx.buckets.begin(), nx.buckets.end());
-      job.grads = nx.grads;
-      dones.push_back(nx.done);
-      c->ce_jobs.pop_front();
-      ++merged;
-    }
     c->ce_busy = true;
     lk.unlock();
     int rc = 0;
@@ -4574,9 +4554,8 @@ static void ce_worker_main(caramel_ctx* c) {
         for (size_t i = 0; !rc && i < job.buckets.size(); ++i) rc = launch(c, &job.buckets[i], 0, job.stream);
       }
     }
-    for (cudaEvent_t d : dones) {
-      if (rc || !d) continue;
-      cudaError_t e = cudaEventRecord(d, job.stream);
+    if (!rc && job.done) {
+      cudaError_t e = cudaEventRecord(job.done, job.stream);
       if (e != cudaSuccess) rc = set_err(CARAMEL_ECUDA, "cudaEventRecord(done): %s", cudaGetErrorString(e));
     }
     lk.lock();
@@ -4584,7 +4563,7 @@ static void ce_worker_main(caramel_ctx* c) {
       c->ce_rc = rc;
       snprintf(c->ce_err, sizeof(c->ce_err), "%s", caramel_last_error());
     }
-    c->ce_consumed += merged;
+    ++c->ce_consumed;
     c->ce_busy = false;
     c->ce_cv.notify_all();
   }
@@ -4622,7 +4601,6 @@ int caramel_ce_submit(caramel_ctx* c, const caramel_bucket* host, int32_t count,
   job.epoch = epoch;
   job.grads = ev;
   job.stream = s;
-  job.gstream = grad_stream ? (cudaStream_t)grad_stream : s;
   job.done = (cudaEvent_t)done_event;
   c->ce_jobs.push_back(std::move(job));
   ++c->ce_submitted;
